@@ -1,0 +1,149 @@
+/*
+ * rbc.h -- C ABI of the B200-native randomized bilinear-computation (BC)
+ * matrix-multiply engine (librbc.so).
+ *
+ * Drop-in boundary.  The reference (`randbc`, pure Python/numpy) funnels every
+ * multiply through two engine functions that its L2 callers resolve by module
+ * attribute at call time:
+ *
+ *   randbc._engine.apply_levels(levels, a, b, mode, stats=None)
+ *       -- reference pkg/src/randbc/_engine.py:117-149
+ *   randbc._engine.leaf_matmul(x, y, mode)
+ *       -- reference pkg/src/randbc/_engine.py:42-61
+ *
+ * rbc_apply_levels / rbc_leaf_matmul are exactly those two calls over plain
+ * pointers (host buffers, synchronous, GIL-free under ctypes).  The Python
+ * binding paper_1905_07439_b200.engine exposes them with the reference's
+ * signatures and installs them into randbc._engine.
+ *
+ * Everything else is an accelerator-side extension:
+ *   - *_async twins take device pointers and a cudaStream_t and never
+ *     synchronise (throughput path, CUDA-graph capturable);
+ *   - the plan path (rbc_apply_plans*) evaluates exact +-1 formulas straight
+ *     from the randomization plans (reference randomize.py:163-178 hatted
+ *     tensors, folded into the kernels);
+ *   - rbc_truth_async / rbc_rel_errors_async are the binary64 ground truth and
+ *     relative Frobenius error of experiments.py:251-261.
+ *
+ * Layouts are the reference's, C-contiguous:
+ *   operands a, b : (T0, N, N)        T0 in {1, T}
+ *   level q u/v/w : (Tc_q, R_q, n_q, n_q)  Tc_q in {1, T}, levels[0] splits A
+ *   result        : (T, N, N)
+ * dtype codes: RBC_F64 (binary64), RBC_F32 (binary32), RBC_F16 (binary16).
+ *
+ * Arithmetic contract: every output element follows the reference's rounding
+ * sequence (one IEEE RNE rounding per multiply and per add, fixed fold orders),
+ * so results are bitwise equal in value to the reference's.
+ *
+ * Status codes map to the reference's exceptions:
+ *   RBC_EVALUE       -> ValueError        (shapes, empty level list, ...)
+ *   RBC_EOVERFLOW    -> OverflowError     (non-finite result, _engine.py:147-148)
+ *   RBC_ERUNTIME     -> RuntimeError      (CUDA failure)
+ *   RBC_EUNSUPPORTED -> NotImplementedError
+ * rbc_last_error() returns the message of the calling thread's last failure.
+ */
+#ifndef RBC_H_
+#define RBC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBC_ABI_VERSION 1
+
+#define RBC_F64 0
+#define RBC_F32 1
+#define RBC_F16 2
+
+#define RBC_FORMULA_STRASSEN 1  /* reference formula.py:98-114           */
+#define RBC_FORMULA_LADERMAN 2  /* formulas/laderman.txt    */
+#define RBC_FORMULA_STANDARD2 3 /* reference formula.py:117-137, n = 2    */
+#define RBC_FORMULA_STANDARD3 4 /* reference formula.py:117-137, n = 3    */
+
+#define RBC_OK 0
+#define RBC_EVALUE 1
+#define RBC_EOVERFLOW 2
+#define RBC_ERUNTIME 3
+#define RBC_EUNSUPPORTED 4
+
+/* Bytes of one packed plan level (see rbc_pack_plans). */
+#define RBC_PLAN_BYTES 40
+
+int rbc_abi_version(void);
+const char* rbc_last_error(void);
+int rbc_device_count(void);
+
+/* ---- reference engine boundary (host buffers, synchronous) --------------- */
+
+/* randbc._engine.apply_levels  (_engine.py:117-149).
+ * n[q], R[q], Tc[q]: level shapes; u[q], v[q], w[q]: host coefficient tables.
+ * T must equal max(T0, Tc[*]).  leaf_multiplies (optional) += T * prod(R). */
+int rbc_apply_levels(int dtype, int Q, const int32_t* n, const int32_t* R, const int64_t* Tc,
+                     const void* const* u, const void* const* v, const void* const* w,
+                     int64_t T0, int64_t N, const void* a, const void* b, int64_t T, void* out,
+                     uint64_t* leaf_multiplies);
+
+/* randbc._engine.leaf_matmul  (_engine.py:42-61), batched x (.., M, K) @ y (.., K, N);
+ * x_bstride / y_bstride are 0 (broadcast) or M*K / K*N. */
+int rbc_leaf_matmul(int dtype, int64_t batch, int64_t x_bstride, int64_t y_bstride, int64_t M,
+                    int64_t K, int64_t N, const void* x, const void* y, void* out);
+
+/* ---- plan path (exact +-1 formulas) -------------------------------------- */
+
+/* Pack `count` plan levels (reference RandomizationPlan: perms (3, n) int64,
+ * signs (3, n) binary64 in {-1, +1}) into RBC_PLAN_BYTES-byte device records.
+ * Returns RBC_EVALUE for n > 4 or entries that are not a signed permutation. */
+int rbc_pack_plans(int n, int64_t count, const int64_t* perms, const double* signs, void* packed);
+
+/* Q-level evaluation of an exact formula under per-trial plans
+ * packed_plans: (Tp, Q) packed levels, Tp in {1, T}, level 0 outermost.
+ * nonfinite (optional, T bytes) receives per-trial overflow flags; the call
+ * returns RBC_EOVERFLOW when any is set. */
+int rbc_apply_plans(int dtype, int formula, int Q, int64_t Tp, const void* packed_plans,
+                    int64_t T0, int64_t N, const void* a, const void* b, int64_t T, void* out,
+                    uint8_t* nonfinite, uint64_t* leaf_multiplies);
+
+/* ---- device-pointer twins (stream ordered, no synchronisation) ------------ */
+
+size_t rbc_levels_workspace_bytes(int dtype, int Q, const int32_t* n, const int32_t* R,
+                                  int64_t T, int64_t N);
+int rbc_apply_levels_async(int dtype, int Q, const int32_t* n, const int32_t* R,
+                           const int64_t* Tc, const void* const* u, const void* const* v,
+                           const void* const* w, int64_t T0, int64_t N, const void* a,
+                           const void* b, int64_t T, void* out, uint8_t* nonfinite,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+size_t rbc_plans_workspace_bytes(int dtype, int formula, int Q, int64_t T, int64_t N);
+int rbc_apply_plans_async(int dtype, int formula, int Q, int64_t Tp, const void* packed_plans,
+                          int64_t T0, int64_t N, const void* a, const void* b, int64_t T,
+                          void* out, uint8_t* nonfinite, void* workspace, size_t workspace_bytes,
+                          void* stream);
+
+int rbc_leaf_matmul_async(int dtype_in, int dtype_out, int64_t batch, int64_t x_bstride,
+                          int64_t y_bstride, int64_t M, int64_t K, int64_t N, const void* x,
+                          const void* y, void* out, void* stream);
+
+/* ---- error check (experiments.py:251-261) -------------------------------- */
+
+/* ref[t] = standard_multiply(widen(a[t]), widen(b[t]), DOUBLE): the binary64
+ * inner-product product of the mode-rounded operands, k ascending. */
+int rbc_truth_async(int dtype_in, int64_t T, int64_t N, const void* a, const void* b,
+                    double* ref, void* stream);
+
+size_t rbc_rel_errors_scratch_bytes(int64_t T);
+/* err[t] = ||widen(c[t]) - ref[t * ref_tstride/N^2]||_F / ||ref[..]||_F, ref_tstride in {0, N*N}. */
+int rbc_rel_errors_async(int dtype, int64_t T, int64_t N, const void* c, const double* ref,
+                         int64_t ref_tstride, double* err, void* scratch, void* stream);
+
+/* nonfinite[t] = 1 if x[t] (N*N elements) holds a non-finite value. */
+int rbc_nonfinite_async(int dtype, int64_t T, int64_t N, const void* x, uint8_t* nonfinite,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RBC_H_ */

@@ -1,0 +1,217 @@
+// Common device helpers for the B200 BC-multiply engine.
+//
+// Every arithmetic operation on the data path goes through the Arith<T>
+// traits below, which use the explicitly rounded intrinsics (__fmul_rn,
+// __fadd_rn, __dmul_rn, __dadd_rn, __hmul_rn, __hadd_rn, and the half2
+// forms).  These are never contracted into FMA, so each multiply and each
+// add rounds once (IEEE RNE), which is the per-element rounding sequence of
+// the reference engine (pkg/src/randbc/_engine.py:3-18).  The library is
+// also compiled with -fmad=false as a second line of defence.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rbc {
+
+// ---------------------------------------------------------------- arith ----
+template <class T> struct Arith;
+
+template <> struct Arith<float> {
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float neg(float a) { return -a; }
+  static __device__ __forceinline__ bool finite(float a) { return isfinite(a); }
+  static __device__ __forceinline__ double widen(float a) { return (double)a; }
+};
+
+template <> struct Arith<double> {
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double neg(double a) { return -a; }
+  static __device__ __forceinline__ bool finite(double a) { return isfinite(a); }
+  static __device__ __forceinline__ double widen(double a) { return a; }
+};
+
+template <> struct Arith<__half> {
+  static __device__ __forceinline__ __half mul(__half a, __half b) { return __hmul_rn(a, b); }
+  static __device__ __forceinline__ __half add(__half a, __half b) { return __hadd_rn(a, b); }
+  static __device__ __forceinline__ __half sub(__half a, __half b) { return __hsub_rn(a, b); }
+  static __device__ __forceinline__ __half neg(__half a) { return __hneg(a); }
+  static __device__ __forceinline__ bool finite(__half a) { return !(__hisinf(a) || __hisnan(a)); }
+  static __device__ __forceinline__ double widen(__half a) { return (double)__half2float(a); }
+};
+
+template <> struct Arith<__half2> {
+  static __device__ __forceinline__ __half2 mul(__half2 a, __half2 b) { return __hmul2_rn(a, b); }
+  static __device__ __forceinline__ __half2 add(__half2 a, __half2 b) { return __hadd2_rn(a, b); }
+  static __device__ __forceinline__ __half2 sub(__half2 a, __half2 b) { return __hsub2_rn(a, b); }
+  static __device__ __forceinline__ __half2 neg(__half2 a) { return __hneg2(a); }
+};
+
+// Bit-exact sign flip (used for the signed permutations of a plan).
+__device__ __forceinline__ float flip_sign(float x, uint32_t m) {
+  return __uint_as_float(__float_as_uint(x) ^ m);
+}
+__device__ __forceinline__ double flip_sign(double x, uint32_t m) {
+  return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)m << 32));
+}
+__device__ __forceinline__ __half flip_sign(__half x, uint32_t m) {
+  return __ushort_as_half((unsigned short)(__half_as_ushort(x) ^ (m >> 16)));
+}
+// mask for a sign: 0 (positive) or the sign bit of a 32-bit word
+__device__ __forceinline__ uint32_t sign_mask(int negative) { return negative ? 0x80000000u : 0u; }
+
+// ----------------------------------------------------------------- pack ----
+// W consecutive elements handled by one thread; loaded and stored with one
+// vector access when the address is sizeof(Pack)-aligned.
+template <class T, int W> struct alignas(sizeof(T) * W) Pack {
+  T v[W];
+};
+
+template <class T, int W>
+__device__ __forceinline__ Pack<T, W> pload(const T* p) {
+  return *reinterpret_cast<const Pack<T, W>*>(p);
+}
+template <class T, int W>
+__device__ __forceinline__ void pstore(T* p, const Pack<T, W>& x) {
+  *reinterpret_cast<Pack<T, W>*>(p) = x;
+}
+
+// Elementwise ops on packs.  Half packs with an even width use half2 SIMD
+// (HADD2/HMUL2), which rounds each lane exactly like the scalar forms.
+template <class T, int W> struct PackOps {
+  using P = Pack<T, W>;
+  static __device__ __forceinline__ P add(const P& a, const P& b) {
+    P r;
+#pragma unroll
+    for (int i = 0; i < W; ++i) r.v[i] = Arith<T>::add(a.v[i], b.v[i]);
+    return r;
+  }
+  static __device__ __forceinline__ P sub(const P& a, const P& b) {
+    P r;
+#pragma unroll
+    for (int i = 0; i < W; ++i) r.v[i] = Arith<T>::sub(a.v[i], b.v[i]);
+    return r;
+  }
+  static __device__ __forceinline__ P neg(const P& a) {
+    P r;
+#pragma unroll
+    for (int i = 0; i < W; ++i) r.v[i] = Arith<T>::neg(a.v[i]);
+    return r;
+  }
+  static __device__ __forceinline__ P mul_scalar(T c, const P& a) {
+    P r;
+#pragma unroll
+    for (int i = 0; i < W; ++i) r.v[i] = Arith<T>::mul(c, a.v[i]);
+    return r;
+  }
+  static __device__ __forceinline__ P flip(const P& a, uint32_t m) {
+    P r;
+#pragma unroll
+    for (int i = 0; i < W; ++i) r.v[i] = flip_sign(a.v[i], m);
+    return r;
+  }
+  static __device__ __forceinline__ P select(bool c, const P& a, const P& b) {
+    P r;
+#pragma unroll
+    for (int i = 0; i < W; ++i) r.v[i] = c ? a.v[i] : b.v[i];
+    return r;
+  }
+  static __device__ __forceinline__ bool all_finite(const P& a) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < W; ++i) ok = ok && Arith<T>::finite(a.v[i]);
+    return ok;
+  }
+};
+
+#define RBC_HALF2_PACK(W)                                                              \
+  template <> struct PackOps<__half, W> {                                              \
+    using P = Pack<__half, W>;                                                         \
+    static __device__ __forceinline__ const __half2* h2(const P& a) {                  \
+      return reinterpret_cast<const __half2*>(a.v);                                    \
+    }                                                                                  \
+    static __device__ __forceinline__ __half2* h2(P& a) {                              \
+      return reinterpret_cast<__half2*>(a.v);                                          \
+    }                                                                                  \
+    static __device__ __forceinline__ P add(const P& a, const P& b) {                  \
+      P r;                                                                             \
+      _Pragma("unroll") for (int i = 0; i < W / 2; ++i) h2(r)[i] = __hadd2_rn(h2(a)[i], h2(b)[i]); \
+      return r;                                                                        \
+    }                                                                                  \
+    static __device__ __forceinline__ P sub(const P& a, const P& b) {                  \
+      P r;                                                                             \
+      _Pragma("unroll") for (int i = 0; i < W / 2; ++i) h2(r)[i] = __hsub2_rn(h2(a)[i], h2(b)[i]); \
+      return r;                                                                        \
+    }                                                                                  \
+    static __device__ __forceinline__ P neg(const P& a) {                              \
+      P r;                                                                             \
+      _Pragma("unroll") for (int i = 0; i < W / 2; ++i) h2(r)[i] = __hneg2(h2(a)[i]);  \
+      return r;                                                                        \
+    }                                                                                  \
+    static __device__ __forceinline__ P mul_scalar(__half c, const P& a) {             \
+      P r;                                                                             \
+      __half2 cc = __half2half2(c);                                                    \
+      _Pragma("unroll") for (int i = 0; i < W / 2; ++i) h2(r)[i] = __hmul2_rn(cc, h2(a)[i]); \
+      return r;                                                                        \
+    }                                                                                  \
+    static __device__ __forceinline__ P flip(const P& a, uint32_t m) {                 \
+      P r;                                                                             \
+      const uint32_t* s = reinterpret_cast<const uint32_t*>(a.v);                      \
+      uint32_t* d = reinterpret_cast<uint32_t*>(r.v);                                  \
+      uint32_t mm = m ? 0x80008000u : 0u;                                              \
+      _Pragma("unroll") for (int i = 0; i < W / 2; ++i) d[i] = s[i] ^ mm;              \
+      return r;                                                                        \
+    }                                                                                  \
+    static __device__ __forceinline__ P select(bool c, const P& a, const P& b) {       \
+      P r;                                                                             \
+      const uint32_t* x = reinterpret_cast<const uint32_t*>(a.v);                      \
+      const uint32_t* y = reinterpret_cast<const uint32_t*>(b.v);                      \
+      uint32_t* d = reinterpret_cast<uint32_t*>(r.v);                                  \
+      _Pragma("unroll") for (int i = 0; i < W / 2; ++i) d[i] = c ? x[i] : y[i];        \
+      return r;                                                                        \
+    }                                                                                  \
+    static __device__ __forceinline__ bool all_finite(const P& a) {                    \
+      bool ok = true;                                                                  \
+      _Pragma("unroll") for (int i = 0; i < W; ++i) ok = ok && Arith<__half>::finite(a.v[i]); \
+      return ok;                                                                       \
+    }                                                                                  \
+  };
+RBC_HALF2_PACK(2)
+RBC_HALF2_PACK(4)
+RBC_HALF2_PACK(8)
+#undef RBC_HALF2_PACK
+
+// Three-term left fold whose order is a runtime choice: the two elements
+// that come first are added first (addition commutes, so their order does
+// not matter) and the element named by `last` (0, 1 or 2) is added last.
+template <class T, int W>
+__device__ __forceinline__ Pack<T, W> fold3(const Pack<T, W>& a, const Pack<T, W>& b,
+                                            const Pack<T, W>& c, int last) {
+  using O = PackOps<T, W>;
+  Pack<T, W> p = O::select(last == 0, b, a);
+  Pack<T, W> q = O::select(last == 2, b, c);
+  Pack<T, W> r = O::select(last == 0, a, O::select(last == 1, b, c));
+  return O::add(O::add(p, q), r);
+}
+
+// -------------------------------------------------------------- plans ----
+// Per (trial, level) randomization plan, packed for the device
+// (reference RandomizationPlan, randomize.py:58-85).  perm[i][hat] is the
+// base block index that hatted block index `hat` reads (perms[i][j] in the
+// reference); inv[i][base] is its inverse; neg[i][hat] is 1 where
+// signs[i][hat] == -1.
+constexpr int kMaxPlanN = 4;
+struct PlanLevel {
+  int8_t perm[3][kMaxPlanN];
+  int8_t inv[3][kMaxPlanN];
+  int8_t neg[3][kMaxPlanN];
+  int8_t pad[4];
+};
+static_assert(sizeof(PlanLevel) == 40, "PlanLevel layout");
+
+}  // namespace rbc

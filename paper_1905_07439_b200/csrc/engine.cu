@@ -1,0 +1,577 @@
+// Orchestration and C ABI of the B200 BC engine (declared in include/rbc.h).
+//
+// Breadth-first evaluation, as in the reference apply_levels
+// (pkg/src/randbc/_engine.py:117-149): Q level-wide expansions of A, Q of B,
+// one batched exact-order leaf product, Q contractions in reverse, then the
+// non-finite check.  Intermediate levels live in a caller-provided (async
+// API) or pooled (host API) workspace of four equal buffers:
+//
+//   bufX, bufY : deepest expansions of A and B          (L_Q elements/trial)
+//   ping, pong : intermediate levels, leaf product, contractions
+//
+// each sized max_q L_q per trial, L_q = prod_{j<q} R_j * (N / prod_{j<q} n_j)^2.
+// Trials are processed in chunks that fit the workspace; chunking never
+// changes values (every output element's operation chain is per trial).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rbc.h"
+#include "kernels.h"
+
+namespace rbc {
+
+static thread_local std::string g_last_error;
+
+static int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int fail_cuda(cudaError_t e, const char* expr, const char* file, int line) {
+  return set_error(RBC_ERUNTIME, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+                   cudaGetErrorString(e), file, line, expr);
+}
+
+#define CUDA_TRY(expr)                                                      \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) return fail_cuda(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+#define RBC_TRY(expr)          \
+  do {                         \
+    int _rc = (expr);          \
+    if (_rc != RBC_OK) return _rc; \
+  } while (0)
+
+// ------------------------------------------------------------- level plan --
+struct LevelShape {
+  int n;
+  int R;
+};
+
+struct Geometry {
+  int Q = 0;
+  int64_t N = 0;
+  std::vector<LevelShape> lv;
+  int64_t maxL = 0;   // elements per trial of the largest level (q >= 1)
+  int64_t leaves = 1; // prod R
+  int64_t leaf_m = 0; // leaf block side
+};
+
+static int make_geometry(int Q, const int32_t* n, const int32_t* R, int64_t N, Geometry* g) {
+  if (Q < 1) return set_error(RBC_EVALUE, "need at least one level");
+  if (N < 0) return set_error(RBC_EVALUE, "operand size must be >= 0");
+  g->Q = Q;
+  g->N = N;
+  g->lv.resize(Q);
+  int64_t s = N, K = 1;
+  g->maxL = 0;
+  for (int q = 0; q < Q; ++q) {
+    if (n[q] < 1 || R[q] < 1) return set_error(RBC_EVALUE, "level %d: need n >= 1 and R >= 1", q);
+    if (s % n[q]) return set_error(RBC_EVALUE, "operand size not divisible by block grid");
+    g->lv[q] = {n[q], R[q]};
+    s /= n[q];
+    K *= R[q];
+    g->maxL = std::max(g->maxL, K * s * s);
+  }
+  g->leaves = K;
+  g->leaf_m = s;
+  return RBC_OK;
+}
+
+static size_t per_trial_ws(const Geometry& g, int dtype) {
+  return (size_t)4 * (size_t)g.maxL * dtype_size(dtype);
+}
+
+// Workspace the async entry points need for `T` trials in one chunk
+// (4 sub-buffers, each rounded up to 256 bytes).
+static size_t ws_for(const Geometry& g, int dtype, int64_t T) {
+  const size_t sub = (((size_t)T * (size_t)g.maxL * dtype_size(dtype)) + 255) & ~(size_t)255;
+  return 4 * sub;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// RBC_DEBUG_SYNC=1: synchronise after every launch so a fault is attributed
+// to the stage that caused it.
+static bool debug_sync() {
+  static const bool on = [] {
+    const char* v = getenv("RBC_DEBUG_SYNC");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+static cudaError_t stage_done(cudaError_t e, cudaStream_t st) {
+  if (e != cudaSuccess || !debug_sync()) return e;
+  return cudaStreamSynchronize(st);
+}
+
+// One chunked breadth-first pass.  `kind` selects the combination kernels.
+struct PassArgs {
+  int dtype;
+  bool plan;        // plan path (formula kernels) vs dense coefficient tables
+  int formula;      // plan path
+  const PlanLevel* plans;
+  int64_t Tp;
+  std::vector<const void*> u, v, w;  // dense path, device pointers
+  std::vector<int64_t> Tc;           // dense path
+  int64_t T0, T;
+  const void* a;
+  const void* b;
+  void* out;
+  uint8_t* nonfinite;
+};
+
+static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_bytes,
+                    cudaStream_t st) {
+  const int dt = p.dtype;
+  const size_t es = dtype_size(dt);
+  const int64_t N2 = g.N * g.N;
+  const size_t ptw = per_trial_ws(g, dt);
+  if (p.T == 0 || g.N == 0) return RBC_OK;
+  int64_t chunk = ptw ? (int64_t)(ws_bytes / ptw) : p.T;
+  chunk = std::min(chunk, p.T);
+  while (chunk > 0 && ws_for(g, dt, chunk) > ws_bytes) --chunk;
+  if (chunk < 1)
+    return set_error(RBC_EVALUE, "workspace too small: need %zu bytes per trial", ws_for(g, dt, 1));
+  // 4 sub-buffers of chunk * maxL elements each
+  const size_t buf_elems = align_up((size_t)chunk * (size_t)g.maxL * es) / es;
+  char* base = (char*)ws;
+  void* bufX = base;
+  void* bufY = base + buf_elems * es;
+  void* ping = base + 2 * buf_elems * es;
+  void* pong = base + 3 * buf_elems * es;
+  if (p.nonfinite) CUDA_TRY(cudaMemsetAsync(p.nonfinite, 0, (size_t)p.T, st));
+
+  for (int64_t t0 = 0; t0 < p.T; t0 += chunk) {
+    const int64_t nt = std::min(chunk, p.T - t0);
+    // --- expansions of A and B
+    for (int which = 0; which < 2; ++which) {
+      const void* cur = which == 0 ? p.a : p.b;
+      int64_t cur_ts = p.T0 == 1 ? 0 : N2;
+      if (p.T0 != 1) cur = (const char*)cur + (size_t)t0 * N2 * es;
+      int64_t K = 1, s = g.N;
+      for (int q = 0; q < g.Q; ++q) {
+        const int n = g.lv[q].n, R = g.lv[q].R;
+        void* dst = (q == g.Q - 1) ? (which == 0 ? bufX : bufY) : ((q & 1) ? pong : ping);
+        cudaError_t e;
+        if (p.plan) {
+          const int64_t pts = p.Tp == 1 ? 0 : g.Q;
+          const PlanLevel* pl = p.plans + (p.Tp == 1 ? 0 : t0 * g.Q);
+          e = launch_expand_plan(dt, p.formula, which, cur, cur_ts, K, s, dst, pl, pts, q, nt, st);
+        } else {
+          const void* c = which == 0 ? p.u[q] : p.v[q];
+          const int64_t cts = p.Tc[q] == 1 ? 0 : (int64_t)R * n * n;
+          c = (const char*)c + (size_t)(p.Tc[q] == 1 ? 0 : t0 * cts) * es;
+          e = launch_expand_dense(dt, cur, cur_ts, K, s, n, R, c, cts, dst, nt, st);
+        }
+        e = stage_done(e, st);
+        if (e != cudaSuccess) return fail_cuda(e, "expand", __FILE__, __LINE__);
+        const int64_t mb = s / n;
+        cur = dst;
+        cur_ts = K * R * mb * mb;
+        K *= R;
+        s = mb;
+      }
+    }
+    // --- leaves
+    const int64_t m = g.leaf_m;
+    {
+      cudaError_t e = launch_leaf(dt, dt, nt * g.leaves, m, m, m, bufX, m * m, bufY, m * m, ping, st);
+      e = stage_done(e, st);
+      if (e != cudaSuccess) return fail_cuda(e, "leaf", __FILE__, __LINE__);
+    }
+    // --- contractions, innermost level first
+    const void* cur = ping;
+    int64_t K = g.leaves, mb = m;
+    for (int q = g.Q - 1; q >= 0; --q) {
+      const int n = g.lv[q].n, R = g.lv[q].R;
+      K /= R;
+      void* dst = q == 0 ? (char*)p.out + (size_t)t0 * N2 * es : (cur == ping ? pong : ping);
+      uint8_t* nf = (q == 0 && p.nonfinite) ? p.nonfinite + t0 : nullptr;
+      cudaError_t e;
+      if (p.plan) {
+        const int64_t pts = p.Tp == 1 ? 0 : g.Q;
+        const PlanLevel* pl = p.plans + (p.Tp == 1 ? 0 : t0 * g.Q);
+        e = launch_contract_plan(dt, p.formula, cur, K, mb, dst, pl, pts, q, nt, nf, st);
+      } else {
+        const int64_t cts = p.Tc[q] == 1 ? 0 : (int64_t)R * n * n;
+        const void* c = (const char*)p.w[q] + (size_t)(p.Tc[q] == 1 ? 0 : t0 * cts) * es;
+        e = launch_contract_dense(dt, cur, K, mb, n, R, c, cts, dst, nt, nf, st);
+      }
+      e = stage_done(e, st);
+      if (e != cudaSuccess) return fail_cuda(e, "contract", __FILE__, __LINE__);
+      cur = dst;
+      mb *= n;
+    }
+  }
+  return RBC_OK;
+}
+
+// ------------------------------------------------------------ device pool --
+// Host-API calls are synchronous; one growing device arena per process is
+// reused across calls (guarded by a mutex, calls are serialised).
+struct Arena {
+  std::mutex mu;
+  char* ptr = nullptr;
+  size_t cap = 0;
+  size_t off = 0;
+  int reserve(size_t bytes) {
+    if (bytes <= cap) {
+      off = 0;
+      return RBC_OK;
+    }
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc((void**)&ptr, bytes);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(arena)", __FILE__, __LINE__);
+    cap = bytes;
+    off = 0;
+    return RBC_OK;
+  }
+  void* take(size_t bytes) {
+    void* r = ptr + off;
+    off += align_up(bytes);
+    return r;
+  }
+};
+
+static Arena& arena() {
+  static Arena a;
+  return a;
+}
+
+static int check_device() {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return set_error(RBC_ERUNTIME, "no CUDA device available (%s)", cudaGetErrorString(e));
+  return RBC_OK;
+}
+
+// Workspace for a synchronous call: everything not already accounted for,
+// bounded by the free device memory.
+static size_t host_ws_budget(size_t fixed, size_t want) {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return want;
+  const size_t usable = (size_t)((double)(free_b + arena().cap) * 0.85);
+  if (usable <= fixed) return 0;
+  return std::min(want, usable - fixed);
+}
+
+static int validate_trials(int64_t T, int64_t T0) {
+  if (T < 0 || T0 < 0) return set_error(RBC_EVALUE, "negative trial count");
+  if (!(T0 == 1 || T0 == T)) return set_error(RBC_EVALUE, "operand trials %lld do not broadcast to %lld",
+                                              (long long)T0, (long long)T);
+  return RBC_OK;
+}
+
+}  // namespace rbc
+
+using namespace rbc;
+
+extern "C" {
+
+int rbc_abi_version(void) { return RBC_ABI_VERSION; }
+
+const char* rbc_last_error(void) { return g_last_error.c_str(); }
+
+int rbc_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+size_t rbc_levels_workspace_bytes(int dtype, int Q, const int32_t* n, const int32_t* R, int64_t T,
+                                  int64_t N) {
+  Geometry g;
+  if (make_geometry(Q, n, R, N, &g) != RBC_OK) return 0;
+  return ws_for(g, dtype, T);
+}
+
+size_t rbc_plans_workspace_bytes(int dtype, int formula, int Q, int64_t T, int64_t N) {
+  const int n = formula_n(formula), R = formula_R(formula);
+  if (!n || Q < 1) return 0;
+  std::vector<int32_t> nv(Q, n), Rv(Q, R);
+  return rbc_levels_workspace_bytes(dtype, Q, nv.data(), Rv.data(), T, N);
+}
+
+int rbc_apply_levels_async(int dtype, int Q, const int32_t* n, const int32_t* R, const int64_t* Tc,
+                           const void* const* u, const void* const* v, const void* const* w,
+                           int64_t T0, int64_t N, const void* a, const void* b, int64_t T, void* out,
+                           uint8_t* nonfinite, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);
+  Geometry g;
+  RBC_TRY(make_geometry(Q, n, R, N, &g));
+  RBC_TRY(validate_trials(T, T0));
+  PassArgs p;
+  p.dtype = dtype;
+  p.plan = false;
+  p.formula = 0;
+  p.plans = nullptr;
+  p.Tp = 1;
+  for (int q = 0; q < Q; ++q) {
+    if (n[q] > 8) return set_error(RBC_EUNSUPPORTED, "block grids above 8x8 are not supported");
+    if (!(Tc[q] == 1 || Tc[q] == T)) return set_error(RBC_EVALUE, "coefficient trials do not broadcast");
+    p.u.push_back(u[q]);
+    p.v.push_back(v[q]);
+    p.w.push_back(w[q]);
+    p.Tc.push_back(Tc[q]);
+  }
+  p.T0 = T0;
+  p.T = T;
+  p.a = a;
+  p.b = b;
+  p.out = out;
+  p.nonfinite = nonfinite;
+  return run_pass(g, p, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int rbc_apply_plans_async(int dtype, int formula, int Q, int64_t Tp, const void* packed_plans,
+                          int64_t T0, int64_t N, const void* a, const void* b, int64_t T, void* out,
+                          uint8_t* nonfinite, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);
+  const int n = formula_n(formula), R = formula_R(formula);
+  if (!n) return set_error(RBC_EVALUE, "unknown formula id %d", formula);
+  if (Q < 1) return set_error(RBC_EVALUE, "need at least one level");
+  std::vector<int32_t> nv(Q, n), Rv(Q, R);
+  Geometry g;
+  RBC_TRY(make_geometry(Q, nv.data(), Rv.data(), N, &g));
+  RBC_TRY(validate_trials(T, T0));
+  if (!(Tp == 1 || Tp == T)) return set_error(RBC_EVALUE, "plan trials do not broadcast");
+  PassArgs p;
+  p.dtype = dtype;
+  p.plan = true;
+  p.formula = formula;
+  p.plans = (const PlanLevel*)packed_plans;
+  p.Tp = Tp;
+  p.T0 = T0;
+  p.T = T;
+  p.a = a;
+  p.b = b;
+  p.out = out;
+  p.nonfinite = nonfinite;
+  return run_pass(g, p, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int rbc_pack_plans(int n, int64_t count, const int64_t* perms, const double* signs, void* packed) {
+  if (n < 1 || n > kMaxPlanN) return set_error(RBC_EVALUE, "plan grid n=%d unsupported (max %d)", n, kMaxPlanN);
+  PlanLevel* out = (PlanLevel*)packed;
+  for (int64_t c = 0; c < count; ++c) {
+    PlanLevel pl;
+    memset(&pl, 0, sizeof pl);
+    for (int i = 0; i < 3; ++i) {
+      int seen = 0;
+      for (int j = 0; j < n; ++j) {
+        const int64_t pj = perms[(c * 3 + i) * n + j];
+        const double sj = signs[(c * 3 + i) * n + j];
+        if (pj < 0 || pj >= n || (seen >> pj) & 1)
+          return set_error(RBC_EVALUE, "each perms row must be a permutation of 0..n-1");
+        if (!(sj == 1.0 || sj == -1.0)) return set_error(RBC_EVALUE, "signs must be +1 or -1");
+        seen |= 1 << pj;
+        pl.perm[i][j] = (int8_t)pj;
+        pl.inv[i][pj] = (int8_t)j;
+        pl.neg[i][j] = sj < 0 ? 1 : 0;
+      }
+    }
+    out[c] = pl;
+  }
+  return RBC_OK;
+}
+
+int rbc_leaf_matmul_async(int dtype_in, int dtype_out, int64_t batch, int64_t xs, int64_t ys,
+                          int64_t M, int64_t K, int64_t N, const void* x, const void* y, void* out,
+                          void* stream) {
+  if (K == 0) return set_error(RBC_EVALUE, "empty shared dimension is handled by the caller");
+  cudaError_t e = launch_leaf(dtype_in, dtype_out, batch, M, K, N, x, xs, y, ys, out,
+                              (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail_cuda(e, "leaf", __FILE__, __LINE__);
+  return RBC_OK;
+}
+
+int rbc_truth_async(int dtype_in, int64_t T, int64_t N, const void* a, const void* b, double* ref,
+                    void* stream) {
+  if (N == 0 || T == 0) return RBC_OK;
+  cudaError_t e = launch_leaf(dtype_in, kF64, T, N, N, N, a, N * N, b, N * N, ref,
+                              (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail_cuda(e, "truth", __FILE__, __LINE__);
+  return RBC_OK;
+}
+
+size_t rbc_rel_errors_scratch_bytes(int64_t T) { return error_scratch_bytes(T); }
+
+int rbc_rel_errors_async(int dtype, int64_t T, int64_t N, const void* c, const double* ref,
+                         int64_t ref_tstride, double* err, void* scratch, void* stream) {
+  if (T == 0) return RBC_OK;
+  cudaError_t e = launch_rel_errors(dtype, T, N * N, c, ref, ref_tstride, err, scratch,
+                                    (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail_cuda(e, "rel_errors", __FILE__, __LINE__);
+  return RBC_OK;
+}
+
+int rbc_nonfinite_async(int dtype, int64_t T, int64_t N, const void* x, uint8_t* nonfinite,
+                        void* stream) {
+  if (T == 0) return RBC_OK;
+  cudaError_t e = cudaMemsetAsync(nonfinite, 0, (size_t)T, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail_cuda(e, "memset", __FILE__, __LINE__);
+  if (N == 0) return RBC_OK;
+  e = launch_nonfinite(dtype, T, N * N, x, nonfinite, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail_cuda(e, "nonfinite", __FILE__, __LINE__);
+  return RBC_OK;
+}
+
+// ------------------------------------------------------- host-buffer API --
+
+static int finish_sync(int rc) {
+  if (rc != RBC_OK) return rc;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return fail_cuda(e, "cudaDeviceSynchronize", __FILE__, __LINE__);
+  return RBC_OK;
+}
+
+int rbc_apply_levels(int dtype, int Q, const int32_t* n, const int32_t* R, const int64_t* Tc,
+                     const void* const* u, const void* const* v, const void* const* w, int64_t T0,
+                     int64_t N, const void* a, const void* b, int64_t T, void* out,
+                     uint64_t* leaf_multiplies) {
+  if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);
+  Geometry g;
+  RBC_TRY(make_geometry(Q, n, R, N, &g));
+  RBC_TRY(validate_trials(T, T0));
+  for (int q = 0; q < Q; ++q) {
+    if (!(Tc[q] == 1 || Tc[q] == T)) return set_error(RBC_EVALUE, "coefficient trials do not broadcast");
+    if (n[q] > 8) return set_error(RBC_EUNSUPPORTED, "block grids above 8x8 are not supported");
+  }
+  RBC_TRY(check_device());
+  const size_t es = dtype_size(dtype);
+  const int64_t N2 = N * N;
+  std::lock_guard<std::mutex> lock(arena().mu);
+  size_t fixed = align_up(T0 * N2 * es) * 2 + align_up(T * N2 * es) + align_up(T) + 4096;
+  std::vector<size_t> cbytes(Q);
+  for (int q = 0; q < Q; ++q) {
+    cbytes[q] = (size_t)Tc[q] * R[q] * n[q] * n[q] * es;
+    fixed += 3 * align_up(cbytes[q]);
+  }
+  const size_t ptw = per_trial_ws(g, dtype);
+  size_t ws_bytes = host_ws_budget(fixed, ws_for(g, dtype, std::max<int64_t>(T, 1)));
+  if (ptw && ws_bytes < ws_for(g, dtype, 1)) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
+  RBC_TRY(arena().reserve(fixed + ws_bytes + 256));
+  Arena& A = arena();
+  void* da = A.take(T0 * N2 * es);
+  void* db = A.take(T0 * N2 * es);
+  void* dout = A.take(T * N2 * es);
+  uint8_t* dnf = (uint8_t*)A.take((size_t)std::max<int64_t>(T, 1));
+  std::vector<const void*> du(Q), dv(Q), dw(Q);
+  for (int q = 0; q < Q; ++q) {
+    void* pu = A.take(cbytes[q]);
+    void* pv = A.take(cbytes[q]);
+    void* pw = A.take(cbytes[q]);
+    CUDA_TRY(cudaMemcpy(pu, u[q], cbytes[q], cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(pv, v[q], cbytes[q], cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(pw, w[q], cbytes[q], cudaMemcpyHostToDevice));
+    du[q] = pu;
+    dv[q] = pv;
+    dw[q] = pw;
+  }
+  void* dws = A.take(ws_bytes);
+  CUDA_TRY(cudaMemcpy(da, a, T0 * N2 * es, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(db, b, T0 * N2 * es, cudaMemcpyHostToDevice));
+  RBC_TRY(finish_sync(rbc_apply_levels_async(dtype, Q, n, R, Tc, du.data(), dv.data(), dw.data(),
+                                             T0, N, da, db, T, dout, dnf, dws, ws_bytes, nullptr)));
+  if (leaf_multiplies) *leaf_multiplies += (uint64_t)T * (uint64_t)g.leaves;
+  std::vector<uint8_t> nf((size_t)T);
+  if (T) CUDA_TRY(cudaMemcpy(nf.data(), dnf, (size_t)T, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, dout, T * N2 * es, cudaMemcpyDeviceToHost));
+  for (int64_t t = 0; t < T; ++t)
+    if (nf[t]) return set_error(RBC_EOVERFLOW, "non-finite result in trial %lld", (long long)t);
+  return RBC_OK;
+}
+
+int rbc_apply_plans(int dtype, int formula, int Q, int64_t Tp, const void* packed_plans,
+                    int64_t T0, int64_t N, const void* a, const void* b, int64_t T, void* out,
+                    uint8_t* nonfinite, uint64_t* leaf_multiplies) {
+  const int n = formula_n(formula), R = formula_R(formula);
+  if (!n) return set_error(RBC_EVALUE, "unknown formula id %d", formula);
+  if (Q < 1) return set_error(RBC_EVALUE, "need at least one level");
+  std::vector<int32_t> nv(Q, n), Rv(Q, R);
+  Geometry g;
+  RBC_TRY(make_geometry(Q, nv.data(), Rv.data(), N, &g));
+  RBC_TRY(validate_trials(T, T0));
+  if (!(Tp == 1 || Tp == T)) return set_error(RBC_EVALUE, "plan trials do not broadcast");
+  RBC_TRY(check_device());
+  const size_t es = dtype_size(dtype);
+  const int64_t N2 = N * N;
+  std::lock_guard<std::mutex> lock(arena().mu);
+  const size_t pbytes = (size_t)Tp * Q * sizeof(PlanLevel);
+  size_t fixed = align_up(T0 * N2 * es) * 2 + align_up(T * N2 * es) + align_up(T) +
+                 align_up(pbytes) + 4096;
+  const size_t ptw = per_trial_ws(g, dtype);
+  size_t ws_bytes = host_ws_budget(fixed, ws_for(g, dtype, std::max<int64_t>(T, 1)));
+  if (ptw && ws_bytes < ws_for(g, dtype, 1)) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
+  RBC_TRY(arena().reserve(fixed + ws_bytes + 256));
+  Arena& A = arena();
+  void* da = A.take(T0 * N2 * es);
+  void* db = A.take(T0 * N2 * es);
+  void* dout = A.take(T * N2 * es);
+  uint8_t* dnf = (uint8_t*)A.take((size_t)std::max<int64_t>(T, 1));
+  void* dpl = A.take(pbytes);
+  void* dws = A.take(ws_bytes);
+  CUDA_TRY(cudaMemcpy(dpl, packed_plans, pbytes, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(da, a, T0 * N2 * es, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(db, b, T0 * N2 * es, cudaMemcpyHostToDevice));
+  RBC_TRY(finish_sync(rbc_apply_plans_async(dtype, formula, Q, Tp, dpl, T0, N, da, db, T, dout,
+                                            dnf, dws, ws_bytes, nullptr)));
+  if (leaf_multiplies) *leaf_multiplies += (uint64_t)T * (uint64_t)g.leaves;
+  std::vector<uint8_t> nf((size_t)T);
+  if (T) CUDA_TRY(cudaMemcpy(nf.data(), dnf, (size_t)T, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, dout, T * N2 * es, cudaMemcpyDeviceToHost));
+  bool any = false;
+  for (int64_t t = 0; t < T; ++t) {
+    if (nonfinite) nonfinite[t] = nf[t];
+    any = any || nf[t];
+  }
+  if (any) return set_error(RBC_EOVERFLOW, "non-finite result");
+  return RBC_OK;
+}
+
+int rbc_leaf_matmul(int dtype, int64_t batch, int64_t xs, int64_t ys, int64_t M, int64_t K,
+                    int64_t N, const void* x, const void* y, void* out) {
+  if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);
+  if (K == 0) return set_error(RBC_EVALUE, "empty shared dimension is handled by the caller");
+  RBC_TRY(check_device());
+  const size_t es = dtype_size(dtype);
+  const size_t xb = (size_t)(xs ? batch : 1) * M * K * es;
+  const size_t yb = (size_t)(ys ? batch : 1) * K * N * es;
+  const size_t ob = (size_t)batch * M * N * es;
+  std::lock_guard<std::mutex> lock(arena().mu);
+  RBC_TRY(arena().reserve(align_up(xb) + align_up(yb) + align_up(ob) + 1024));
+  Arena& A = arena();
+  void* dx = A.take(xb);
+  void* dy = A.take(yb);
+  void* dout = A.take(ob);
+  CUDA_TRY(cudaMemcpy(dx, x, xb, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dy, y, yb, cudaMemcpyHostToDevice));
+  RBC_TRY(finish_sync(rbc_leaf_matmul_async(dtype, dtype, batch, xs, ys, M, K, N, dx, dy, dout, nullptr)));
+  CUDA_TRY(cudaMemcpy(out, dout, ob, cudaMemcpyDeviceToHost));
+  return RBC_OK;
+}
+
+}  // extern "C"

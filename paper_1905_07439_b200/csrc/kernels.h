@@ -1,0 +1,70 @@
+// Internal host-side launch interface of the B200 BC engine (not part of the
+// C-ABI; see include/rbc.h for that).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace rbc {
+
+enum Dtype : int { kF64 = 0, kF32 = 1, kF16 = 2 };
+
+inline size_t dtype_size(int dt) { return dt == kF64 ? 8 : dt == kF32 ? 4 : 2; }
+
+// Records a CUDA failure as the thread's last error; returns RBC_ERUNTIME.
+int fail_cuda(cudaError_t e, const char* expr, const char* file, int line);
+
+// Largest vector width (elements per thread) that divides the block side.
+int pick_width(int dtype, int64_t mb, int cap_elems);
+
+// ---- plan path: exact +-1 formulas, per-trial signed permutations ---------
+// Expansion of one level for operand A (which == 0: rows by perm 1, cols by
+// perm 2) or B (which == 1: rows by perm 2, cols by perm 3).
+//   x    : (T or 1, K, s, s)   x_tstride = K*s*s or 0 (broadcast)
+//   out  : (T, K*R, s/n, s/n)
+//   plans: PlanLevel[(t * plan_tstride) + level]; plan_tstride = Q or 0
+cudaError_t launch_expand_plan(int dtype, int formula, int which, const void* x,
+                               int64_t x_tstride, int64_t K, int64_t s, void* out,
+                               const PlanLevel* plans, int64_t plan_tstride, int level,
+                               int64_t T, cudaStream_t st);
+
+// Contraction of one level: ch (T, K, R, mb, mb) -> out (T, K, n*mb, n*mb).
+// nonfinite (optional, T bytes) gets 1 for trials with a non-finite output.
+cudaError_t launch_contract_plan(int dtype, int formula, const void* ch, int64_t K, int64_t mb,
+                                 void* out, const PlanLevel* plans, int64_t plan_tstride,
+                                 int level, int64_t T, uint8_t* nonfinite, cudaStream_t st);
+
+int formula_n(int formula);
+int formula_R(int formula);
+
+// ---- dense path: arbitrary coefficient tables (Tc, R, n, n) --------------
+cudaError_t launch_expand_dense(int dtype, const void* x, int64_t x_tstride, int64_t K, int64_t s,
+                                int n, int R, const void* coeff, int64_t c_tstride, void* out,
+                                int64_t T, cudaStream_t st);
+cudaError_t launch_contract_dense(int dtype, const void* ch, int64_t K, int64_t mb, int n, int R,
+                                  const void* w, int64_t w_tstride, void* out, int64_t T,
+                                  uint8_t* nonfinite, cudaStream_t st);
+
+// ---- leaf: exact-order batched product ------------------------------------
+// out[b] = x[b] @ y[b], k ascending, first term initialises, one rounding per
+// multiply and per add.  dtype_out may be wider than dtype_in (f64 truth of
+// f32/f16 operands: inputs are widened exactly).
+cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, int64_t K,
+                        int64_t N, const void* x, int64_t x_bstride, const void* y,
+                        int64_t y_bstride, void* out, cudaStream_t st);
+
+// ---- error check -----------------------------------------------------------
+// err[t] = ||widen(c[t]) - ref[t or 0]||_F / ||ref[t or 0]||_F   (binary64)
+// scratch: at least error_scratch_bytes(T) bytes of device memory.
+size_t error_scratch_bytes(int64_t T);
+cudaError_t launch_rel_errors(int dtype, int64_t T, int64_t N2, const void* c, const double* ref,
+                              int64_t ref_tstride, double* err, void* scratch, cudaStream_t st);
+
+// Set nonfinite[t] = 1 when any element of x[t] (N2 elements) is non-finite.
+cudaError_t launch_nonfinite(int dtype, int64_t T, int64_t N2, const void* x, uint8_t* flags,
+                             cudaStream_t st);
+
+}  // namespace rbc

@@ -1,0 +1,184 @@
+// Dense-coefficient combination kernels: the general engine path for any
+// coefficient tables (approximate / perturbed formulas, arbitrary n and R).
+//
+// Exactly the reference's arithmetic (pkg/src/randbc/_engine.py:64-114):
+// every coefficient -- zeros included -- is multiplied and added, the
+// expansion folds l inside each row k and then folds the row sums over k,
+// the contraction folds r ascending, first term initialising.  The result is
+// therefore bit-identical to the reference, signed zeros and non-finite
+// propagation included.
+//
+// Coefficients are per trial ((Tc, R, n, n), Tc in {1, T}); every thread of a
+// block row reads the same coefficient, so the loads are broadcasts.
+
+#include "kernels.h"
+
+namespace rbc {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxDenseN = 8;
+
+template <class T, int W, int NMAX>
+__global__ void __launch_bounds__(kThreads) expand_dense_kernel(
+    const T* __restrict__ x, int64_t x_tstride, int K, int s, int n, int R,
+    const T* __restrict__ coeff, int64_t c_tstride, T* __restrict__ out, int64_t ntr) {
+  const int mb = s / n;
+  const int P = (mb * mb) / W;
+  const int64_t items = (int64_t)K * P;
+  const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (e >= items) return;
+  const int Kp = (int)(e / P);
+  const int p = (int)(e - (int64_t)Kp * P);
+  const int pos = p * W;
+  const int i = pos / mb;
+  const int j = pos - i * mb;
+  using O = PackOps<T, W>;
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    const T* xb = x + t * x_tstride + (int64_t)Kp * s * s + (int64_t)i * s + j;
+    Pack<T, W> g[NMAX * NMAX];
+#pragma unroll
+    for (int k = 0; k < NMAX; ++k)
+#pragma unroll
+      for (int l = 0; l < NMAX; ++l)
+        if (k < n && l < n) g[k * NMAX + l] = pload<T, W>(xb + (int64_t)k * mb * s + l * mb);
+    const T* ct = coeff + t * c_tstride;
+    T* ob = out + (t * K + Kp) * (int64_t)R * mb * mb + pos;
+    for (int r = 0; r < R; ++r) {
+      const T* cr = ct + (int64_t)r * n * n;
+      Pack<T, W> acc;
+#pragma unroll
+      for (int k = 0; k < NMAX; ++k) {
+        if (k < n) {
+          Pack<T, W> row = O::mul_scalar(cr[k * n], g[k * NMAX]);
+#pragma unroll
+          for (int l = 1; l < NMAX; ++l)
+            if (l < n) row = O::add(row, O::mul_scalar(cr[k * n + l], g[k * NMAX + l]));
+          acc = (k == 0) ? row : O::add(acc, row);
+        }
+      }
+      pstore<T, W>(ob + (int64_t)r * mb * mb, acc);
+    }
+  }
+}
+
+template <class T, int W>
+__global__ void __launch_bounds__(kThreads) contract_dense_kernel(
+    const T* __restrict__ ch, int K, int mb, int n, int R, const T* __restrict__ w,
+    int64_t w_tstride, T* __restrict__ out, int64_t ntr, uint8_t* __restrict__ nonfinite) {
+  const int s = n * mb;
+  const int P = (mb * mb) / W;
+  const int64_t items = (int64_t)K * P;
+  const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (e >= items) return;
+  const int Kp = (int)(e / P);
+  const int p = (int)(e - (int64_t)Kp * P);
+  const int pos = p * W;
+  const int i = pos / mb;
+  const int j = pos - i * mb;
+  using O = PackOps<T, W>;
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    const T* cb = ch + (t * K + Kp) * (int64_t)R * mb * mb + pos;
+    const T* wt = w + t * w_tstride;
+    T* obase = out + (t * K + Kp) * (int64_t)s * s + (int64_t)i * s + j;
+    bool ok = true;
+    for (int I = 0; I < n; ++I) {
+      for (int J = 0; J < n; ++J) {
+        Pack<T, W> acc = O::mul_scalar(wt[I * n + J], pload<T, W>(cb));
+        for (int r = 1; r < R; ++r)
+          acc = O::add(acc, O::mul_scalar(wt[((int64_t)r * n + I) * n + J],
+                                          pload<T, W>(cb + (int64_t)r * mb * mb)));
+        if (nonfinite) ok = ok && O::all_finite(acc);
+        pstore<T, W>(obase + (int64_t)I * mb * s + J * mb, acc);
+      }
+    }
+    if (!ok) nonfinite[t] = 1;
+  }
+}
+
+inline dim3 grid_for(int64_t items, int64_t ntr) {
+  const int64_t bx = (items + kThreads - 1) / kThreads;
+  return dim3((unsigned)bx, (unsigned)(ntr < 65535 ? ntr : 65535), 1);
+}
+
+template <class T, int W>
+cudaError_t expand_dense_w(const void* x, int64_t xs, int64_t K, int64_t s, int n, int R,
+                           const void* c, int64_t cs, void* out, int64_t ntr, cudaStream_t st) {
+  const int64_t mb = s / n;
+  const dim3 grid = grid_for(K * (mb * mb / W), ntr);
+  if (n <= 2)
+    expand_dense_kernel<T, W, 2><<<grid, kThreads, 0, st>>>((const T*)x, xs, (int)K, (int)s, n, R,
+                                                            (const T*)c, cs, (T*)out, ntr);
+  else if (n <= 4)
+    expand_dense_kernel<T, W, 4><<<grid, kThreads, 0, st>>>((const T*)x, xs, (int)K, (int)s, n, R,
+                                                            (const T*)c, cs, (T*)out, ntr);
+  else
+    expand_dense_kernel<T, 1, kMaxDenseN><<<grid_for(K * mb * mb, ntr), kThreads, 0, st>>>(
+        (const T*)x, xs, (int)K, (int)s, n, R, (const T*)c, cs, (T*)out, ntr);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t expand_dense_t(int dtype, const void* x, int64_t xs, int64_t K, int64_t s, int n,
+                           int R, const void* c, int64_t cs, void* out, int64_t ntr,
+                           cudaStream_t st) {
+  const int W = n > 4 ? 1 : pick_width(dtype, s / n, 8 / (int)sizeof(T));
+  switch (W) {
+    case 4: return expand_dense_w<T, (sizeof(T) == 2 ? 4 : 1)>(x, xs, K, s, n, R, c, cs, out, ntr, st);
+    case 2: return expand_dense_w<T, (sizeof(T) <= 4 ? 2 : 1)>(x, xs, K, s, n, R, c, cs, out, ntr, st);
+    default: return expand_dense_w<T, 1>(x, xs, K, s, n, R, c, cs, out, ntr, st);
+  }
+}
+
+template <class T>
+cudaError_t contract_dense_t(int dtype, const void* ch, int64_t K, int64_t mb, int n, int R,
+                             const void* w, int64_t ws, void* out, int64_t ntr, uint8_t* nf,
+                             cudaStream_t st) {
+  const int W = pick_width(dtype, mb, 8 / (int)sizeof(T));
+  if (W >= 2 && sizeof(T) <= 4) {
+    constexpr int W2 = sizeof(T) <= 4 ? 2 : 1;
+    contract_dense_kernel<T, W2><<<grid_for(K * (mb * mb / W2), ntr), kThreads, 0, st>>>(
+        (const T*)ch, (int)K, (int)mb, n, R, (const T*)w, ws, (T*)out, ntr, nf);
+  } else {
+    contract_dense_kernel<T, 1><<<grid_for(K * mb * mb, ntr), kThreads, 0, st>>>(
+        (const T*)ch, (int)K, (int)mb, n, R, (const T*)w, ws, (T*)out, ntr, nf);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int pick_width(int dtype, int64_t mb, int cap_elems) {
+  (void)dtype;
+  int W = 1;
+  for (int c = 2; c <= cap_elems; c *= 2)
+    if (mb % c == 0) W = c;
+  return W;
+}
+
+cudaError_t launch_expand_dense(int dtype, const void* x, int64_t x_tstride, int64_t K, int64_t s,
+                                int n, int R, const void* coeff, int64_t c_tstride, void* out,
+                                int64_t ntr, cudaStream_t st) {
+  if (n > kMaxDenseN) return cudaErrorInvalidValue;
+  switch (dtype) {
+    case kF64: return expand_dense_t<double>(dtype, x, x_tstride, K, s, n, R, coeff, c_tstride, out, ntr, st);
+    case kF32: return expand_dense_t<float>(dtype, x, x_tstride, K, s, n, R, coeff, c_tstride, out, ntr, st);
+    case kF16: return expand_dense_t<__half>(dtype, x, x_tstride, K, s, n, R, coeff, c_tstride, out, ntr, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_contract_dense(int dtype, const void* ch, int64_t K, int64_t mb, int n, int R,
+                                  const void* w, int64_t w_tstride, void* out, int64_t ntr,
+                                  uint8_t* nonfinite, cudaStream_t st) {
+  if (n > kMaxDenseN) return cudaErrorInvalidValue;
+  switch (dtype) {
+    case kF64: return contract_dense_t<double>(dtype, ch, K, mb, n, R, w, w_tstride, out, ntr, nonfinite, st);
+    case kF32: return contract_dense_t<float>(dtype, ch, K, mb, n, R, w, w_tstride, out, ntr, nonfinite, st);
+    case kF16: return contract_dense_t<__half>(dtype, ch, K, mb, n, R, w, w_tstride, out, ntr, nonfinite, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace rbc

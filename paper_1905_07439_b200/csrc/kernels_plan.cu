@@ -1,0 +1,248 @@
+// Plan-path combination kernels for exact +-1 formulas.
+//
+// Reference semantics (pkg/src/randbc/_engine.py:64-114 applied to the
+// hatted tensors of randomize.py:163-178):
+//   child_r(pos)      = sum_kl uh[r,k,l] X[k][l](pos),
+//   uh[r,k,l]         = u[r, p1(k), p2(l)] s1(k) s2(l)
+//   out[i][j](pos)    = sum_r wh[r,i,j] P_r(pos),
+//   wh[r,i,j]         = w[r, p1(i), p3(j)] s1(i) s3(j)      (1/(1-kappa) == 1)
+//
+// Instead of multiplying by hatted coefficients, the expansion gathers the
+// parent grid through the plan (G[k'][l'] = s1(k) s2(l) X[k][l] with
+// k = p1^-1(k'), l = p2^-1(l'): a sign flip is exact) and runs the formula's
+// generated base-coordinate network (formulas_gen.cuh); the contraction runs
+// the base network and scatters base block (I, J) to hatted block
+// (p1^-1(I), p3^-1(J)) with sign s1 s3.  Both are bitwise equal in value to
+// the reference (see tools/gen_formulas.py for the fold-order argument).
+//
+// One thread handles W consecutive columns of one position of one parent
+// block; memory traffic per thread is n*n loads + R stores (expand) or
+// R loads + n*n stores (contract), all coalesced along block rows.
+
+#include "formulas_gen.cuh"
+#include "kernels.h"
+
+namespace rbc {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <class F, class T, int W, int WHICH>
+__global__ void __launch_bounds__(kThreads) expand_plan_kernel(
+    const T* __restrict__ x, int64_t x_tstride, int K, int s, T* __restrict__ out,
+    const PlanLevel* __restrict__ plans, int64_t plan_tstride, int level, int64_t ntr) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  const int mb = s / n;
+  const int P = (mb * mb) / W;             // packs per parent block
+  const int64_t items = (int64_t)K * P;    // packs per trial
+  const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (e >= items) return;
+  const int Kp = (int)(e / P);
+  const int p = (int)(e - (int64_t)Kp * P);
+  const int pos = p * W;
+  const int i = pos / mb;
+  const int j = pos - i * mb;
+  constexpr int ri = WHICH == 0 ? 0 : 1;  // plan index permuting block rows
+  constexpr int ci = WHICH == 0 ? 1 : 2;  // plan index permuting block cols
+  using O = PackOps<T, W>;
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    const PlanLevel pl = plans[t * plan_tstride + level];
+    const T* xb = x + t * x_tstride + (int64_t)Kp * s * s + (int64_t)i * s + j;
+    Pack<T, W> g[n * n];
+#pragma unroll
+    for (int kb = 0; kb < n; ++kb) {
+      const int hk = pl.inv[ri][kb];
+#pragma unroll
+      for (int lb = 0; lb < n; ++lb) {
+        const int hl = pl.inv[ci][lb];
+        const uint32_t m = sign_mask(pl.neg[ri][hk] ^ pl.neg[ci][hl]);
+        g[kb * n + lb] = O::flip(pload<T, W>(xb + (int64_t)hk * mb * s + hl * mb), m);
+      }
+    }
+    Pack<T, W> o[R];
+    if (WHICH == 0)
+      F::template expand_u<T, W>(g, o, pl.perm[ri][n - 1], pl.perm[ci][n - 1]);
+    else
+      F::template expand_v<T, W>(g, o, pl.perm[ri][n - 1], pl.perm[ci][n - 1]);
+    T* ob = out + (t * K + Kp) * (int64_t)R * mb * mb + pos;
+#pragma unroll
+    for (int r = 0; r < R; ++r) pstore<T, W>(ob + (int64_t)r * mb * mb, o[r]);
+  }
+}
+
+template <class F, class T, int W>
+__global__ void __launch_bounds__(kThreads) contract_plan_kernel(
+    const T* __restrict__ ch, int K, int mb, T* __restrict__ out,
+    const PlanLevel* __restrict__ plans, int64_t plan_tstride, int level, int64_t ntr,
+    uint8_t* __restrict__ nonfinite) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  const int s = n * mb;
+  const int P = (mb * mb) / W;
+  const int64_t items = (int64_t)K * P;
+  const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (e >= items) return;
+  const int Kp = (int)(e / P);
+  const int p = (int)(e - (int64_t)Kp * P);
+  const int pos = p * W;
+  const int i = pos / mb;
+  const int j = pos - i * mb;
+  using O = PackOps<T, W>;
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    const PlanLevel pl = plans[t * plan_tstride + level];
+    const T* cb = ch + (t * K + Kp) * (int64_t)R * mb * mb + pos;
+    Pack<T, W> pr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) pr[r] = pload<T, W>(cb + (int64_t)r * mb * mb);
+    Pack<T, W> o[n * n];
+    F::template contract_w<T, W>(pr, o);
+    T* obase = out + (t * K + Kp) * (int64_t)s * s + (int64_t)i * s + j;
+    bool ok = true;
+#pragma unroll
+    for (int I = 0; I < n; ++I) {
+      const int hi = pl.inv[0][I];
+#pragma unroll
+      for (int J = 0; J < n; ++J) {
+        const int hj = pl.inv[2][J];
+        const Pack<T, W> val = O::flip(o[I * n + J], sign_mask(pl.neg[0][hi] ^ pl.neg[2][hj]));
+        if (nonfinite) ok = ok && O::all_finite(val);
+        pstore<T, W>(obase + (int64_t)hi * mb * s + hj * mb, val);
+      }
+    }
+    if (!ok) nonfinite[t] = 1;
+  }
+}
+
+inline dim3 grid_for(int64_t items, int64_t ntr) {
+  const int64_t bx = (items + kThreads - 1) / kThreads;
+  return dim3((unsigned)bx, (unsigned)(ntr < 65535 ? ntr : 65535), 1);
+}
+
+template <class F, class T, int W>
+cudaError_t expand_plan_w(int which, const void* x, int64_t xs, int64_t K, int64_t s, void* out,
+                          const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
+                          cudaStream_t st) {
+  const int64_t mb = s / F::n;
+  const dim3 grid = grid_for(K * (mb * mb / W), ntr);
+  if (which == 0)
+    expand_plan_kernel<F, T, W, 0><<<grid, kThreads, 0, st>>>(
+        (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
+  else
+    expand_plan_kernel<F, T, W, 1><<<grid, kThreads, 0, st>>>(
+        (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
+  return cudaGetLastError();
+}
+
+template <class F, class T, int W>
+cudaError_t contract_plan_w(const void* ch, int64_t K, int64_t mb, void* out,
+                            const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
+                            uint8_t* nonfinite, cudaStream_t st) {
+  const dim3 grid = grid_for(K * (mb * mb / W), ntr);
+  contract_plan_kernel<F, T, W><<<grid, kThreads, 0, st>>>(
+      (const T*)ch, (int)K, (int)mb, (T*)out, plans, pts, level, ntr, nonfinite);
+  return cudaGetLastError();
+}
+
+// Width dispatch.  Large-R formulas (Laderman: 23 live packs) cap the width
+// so the children stay in registers.
+template <class F, class T>
+cudaError_t expand_plan_t(int dtype, int which, const void* x, int64_t xs, int64_t K, int64_t s,
+                          void* out, const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
+                          cudaStream_t st) {
+  const int cap = (F::R > 8 ? 8 : 16) / (int)sizeof(T);
+  const int W = pick_width(dtype, s / F::n, cap);
+  switch (W) {
+    case 8: return expand_plan_w<F, T, (sizeof(T) == 2 ? 8 : 1)>(which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    case 4: return expand_plan_w<F, T, (sizeof(T) <= 4 ? 4 : 1)>(which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    case 2: return expand_plan_w<F, T, 2>(which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    default: return expand_plan_w<F, T, 1>(which, x, xs, K, s, out, plans, pts, level, ntr, st);
+  }
+}
+
+template <class F, class T>
+cudaError_t contract_plan_t(int dtype, const void* ch, int64_t K, int64_t mb, void* out,
+                            const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
+                            uint8_t* nonfinite, cudaStream_t st) {
+  const int cap = (F::R > 8 ? 8 : 16) / (int)sizeof(T);
+  const int W = pick_width(dtype, mb, cap);
+  switch (W) {
+    case 8: return contract_plan_w<F, T, (sizeof(T) == 2 ? 8 : 1)>(ch, K, mb, out, plans, pts, level, ntr, nonfinite, st);
+    case 4: return contract_plan_w<F, T, (sizeof(T) <= 4 ? 4 : 1)>(ch, K, mb, out, plans, pts, level, ntr, nonfinite, st);
+    case 2: return contract_plan_w<F, T, 2>(ch, K, mb, out, plans, pts, level, ntr, nonfinite, st);
+    default: return contract_plan_w<F, T, 1>(ch, K, mb, out, plans, pts, level, ntr, nonfinite, st);
+  }
+}
+
+template <class T>
+cudaError_t expand_plan_f(int dtype, int formula, int which, const void* x, int64_t xs, int64_t K,
+                          int64_t s, void* out, const PlanLevel* plans, int64_t pts, int level,
+                          int64_t ntr, cudaStream_t st) {
+  switch (formula) {
+    case FStrassen::kId: return expand_plan_t<FStrassen, T>(dtype, which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    case FLaderman::kId: return expand_plan_t<FLaderman, T>(dtype, which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    case FStandard2::kId: return expand_plan_t<FStandard2, T>(dtype, which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    case FStandard3::kId: return expand_plan_t<FStandard3, T>(dtype, which, x, xs, K, s, out, plans, pts, level, ntr, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <class T>
+cudaError_t contract_plan_f(int dtype, int formula, const void* ch, int64_t K, int64_t mb,
+                            void* out, const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
+                            uint8_t* nonfinite, cudaStream_t st) {
+  switch (formula) {
+    case FStrassen::kId: return contract_plan_t<FStrassen, T>(dtype, ch, K, mb, out, plans, pts, level, ntr, nonfinite, st);
+    case FLaderman::kId: return contract_plan_t<FLaderman, T>(dtype, ch, K, mb, out, plans, pts, level, ntr, nonfinite, st);
+    case FStandard2::kId: return contract_plan_t<FStandard2, T>(dtype, ch, K, mb, out, plans, pts, level, ntr, nonfinite, st);
+    case FStandard3::kId: return contract_plan_t<FStandard3, T>(dtype, ch, K, mb, out, plans, pts, level, ntr, nonfinite, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int formula_n(int formula) {
+  switch (formula) {
+    case FStrassen::kId: return FStrassen::n;
+    case FLaderman::kId: return FLaderman::n;
+    case FStandard2::kId: return FStandard2::n;
+    case FStandard3::kId: return FStandard3::n;
+  }
+  return 0;
+}
+
+int formula_R(int formula) {
+  switch (formula) {
+    case FStrassen::kId: return FStrassen::R;
+    case FLaderman::kId: return FLaderman::R;
+    case FStandard2::kId: return FStandard2::R;
+    case FStandard3::kId: return FStandard3::R;
+  }
+  return 0;
+}
+
+cudaError_t launch_expand_plan(int dtype, int formula, int which, const void* x, int64_t x_tstride,
+                               int64_t K, int64_t s, void* out, const PlanLevel* plans,
+                               int64_t plan_tstride, int level, int64_t ntr, cudaStream_t st) {
+  switch (dtype) {
+    case kF64: return expand_plan_f<double>(dtype, formula, which, x, x_tstride, K, s, out, plans, plan_tstride, level, ntr, st);
+    case kF32: return expand_plan_f<float>(dtype, formula, which, x, x_tstride, K, s, out, plans, plan_tstride, level, ntr, st);
+    case kF16: return expand_plan_f<__half>(dtype, formula, which, x, x_tstride, K, s, out, plans, plan_tstride, level, ntr, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_contract_plan(int dtype, int formula, const void* ch, int64_t K, int64_t mb,
+                                 void* out, const PlanLevel* plans, int64_t plan_tstride,
+                                 int level, int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
+  switch (dtype) {
+    case kF64: return contract_plan_f<double>(dtype, formula, ch, K, mb, out, plans, plan_tstride, level, ntr, nonfinite, st);
+    case kF32: return contract_plan_f<float>(dtype, formula, ch, K, mb, out, plans, plan_tstride, level, ntr, nonfinite, st);
+    case kF16: return contract_plan_f<__half>(dtype, formula, ch, K, mb, out, plans, plan_tstride, level, ntr, nonfinite, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace rbc

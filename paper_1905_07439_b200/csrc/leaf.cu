@@ -1,0 +1,259 @@
+// Exact-order batched leaf products (reference leaf_matmul,
+// pkg/src/randbc/_engine.py:42-61):
+//
+//   P[i,j] = fl(...fl(fl(x_i0*y_0j) + fl(x_i1*y_1j)) + ...),  k ascending,
+//
+// one rounding per multiply and per add, first term initialising, no FMA and
+// no split-K.  This pins the rounding of every output element to the
+// reference's, so per-trial errors match.  Consequently the
+// kernels run on the CUDA-core FP pipes (FMUL + FADD per multiply-add), not
+// on the tensor cores, whose internal accumulation would change the very
+// rounding error the paper measures.
+//
+// Two kernels:
+//  * leaf_small  -- one thread per output element, for leaves narrower than a
+//                   tile (3x3, 10x10, 27x27 ...).
+//  * leaf_tiled  -- BM x BN x BK register-tiled SGEMM/DGEMM structure:
+//                   operand tiles double-buffered in shared memory (A stored
+//                   k-major), each thread owns TM x TN outputs in VW-wide
+//                   groups so fragments are read with 16-byte LDS, and every
+//                   output keeps its own sequential k chain.
+// Both also serve the binary64 ground truth of binary32/binary16 operands
+// (TIn narrower than TAcc: operands are widened exactly on load).
+
+#include "kernels.h"
+
+namespace rbc {
+
+namespace {
+
+template <class TIn, class TAcc>
+__device__ __forceinline__ TAcc widen_to(TIn v);
+template <> __device__ __forceinline__ float widen_to<float, float>(float v) { return v; }
+template <> __device__ __forceinline__ double widen_to<double, double>(double v) { return v; }
+template <> __device__ __forceinline__ double widen_to<float, double>(float v) { return (double)v; }
+template <> __device__ __forceinline__ __half widen_to<__half, __half>(__half v) { return v; }
+template <> __device__ __forceinline__ double widen_to<__half, double>(__half v) {
+  return (double)__half2float(v);
+}
+template <> __device__ __forceinline__ float widen_to<__half, float>(__half v) {
+  return __half2float(v);
+}
+
+template <class TIn, class TAcc>
+__global__ void __launch_bounds__(256) leaf_small_kernel(int64_t batch, int M, int K, int N,
+                                                         const TIn* __restrict__ x, int64_t xs,
+                                                         const TIn* __restrict__ y, int64_t ys,
+                                                         TAcc* __restrict__ out) {
+  using A = Arith<TAcc>;
+  const int64_t per = (int64_t)M * N;
+  const int64_t total = batch * per;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / per;
+    const int rem = (int)(idx - b * per);
+    const int i = rem / N;
+    const int j = rem - i * N;
+    const TIn* xr = x + b * xs + (int64_t)i * K;
+    const TIn* yc = y + b * ys + j;
+    TAcc acc = A::mul(widen_to<TIn, TAcc>(xr[0]), widen_to<TIn, TAcc>(yc[0]));
+    for (int k = 1; k < K; ++k)
+      acc = A::add(acc, A::mul(widen_to<TIn, TAcc>(xr[k]), widen_to<TIn, TAcc>(yc[(int64_t)k * N])));
+    out[idx] = acc;
+  }
+}
+
+// VW = elements per 16-byte fragment read.
+template <class TIn, class TAcc, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    leaf_tiled_kernel(int M, int K, int N, const TIn* __restrict__ x, int64_t xs,
+                      const TIn* __restrict__ y, int64_t ys, TAcc* __restrict__ out,
+                      int tiles_n) {
+  constexpr int VW = 16 / (int)sizeof(TAcc) < TM ? 16 / (int)sizeof(TAcc) : TM;
+  constexpr int DY = BM / TM;  // threads along M
+  constexpr int DX = BN / TN;  // threads along N
+  constexpr int NT = DY * DX;
+  constexpr int GM = TM / VW;  // fragment groups along M
+  constexpr int GN = TN / VW;
+  constexpr int A_PER = BM * BK / NT;  // A elements loaded per thread per tile
+  constexpr int B_PER = BK * BN / NT;
+  static_assert(BM * BK % NT == 0 && BK * BN % NT == 0, "tile/threads");
+  static_assert(TM % VW == 0 && TN % VW == 0, "fragment width");
+  using A = Arith<TAcc>;
+
+  __shared__ __align__(16) TAcc As[2][BK][BM];
+  __shared__ __align__(16) TAcc Bs[2][BK][BN];
+
+  const int tid = threadIdx.x;
+  const int tx = tid % DX;
+  const int ty = tid / DX;
+  const int64_t b = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  const int tm = blockIdx.x / tiles_n;
+  const int tn = blockIdx.x - tm * tiles_n;
+  const int m0 = tm * BM;
+  const int n0 = tn * BN;
+  const TIn* xb = x + b * xs;
+  const TIn* yb = y + b * ys;
+
+  TAcc ra[A_PER];
+  TAcc rb[B_PER];
+  auto load_tile = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < A_PER; ++q) {
+      const int e = tid + q * NT;
+      const int mm = e / BK, kk = e % BK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      ra[q] = (gm < M && gk < K) ? widen_to<TIn, TAcc>(xb[(int64_t)gm * K + gk]) : TAcc(0);
+    }
+#pragma unroll
+    for (int q = 0; q < B_PER; ++q) {
+      const int e = tid + q * NT;
+      const int kk = e / BN, nn = e % BN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      rb[q] = (gk < K && gn < N) ? widen_to<TIn, TAcc>(yb[(int64_t)gk * N + gn]) : TAcc(0);
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < A_PER; ++q) {
+      const int e = tid + q * NT;
+      As[buf][e % BK][e / BK] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < B_PER; ++q) {
+      const int e = tid + q * NT;
+      Bs[buf][e / BN][e % BN] = rb[q];
+    }
+  };
+
+  TAcc acc[TM][TN];
+  const int ktiles = (K + BK - 1) / BK;
+  load_tile(0);
+  store_tile(0);
+  __syncthreads();
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
+    const int kmax = min(BK, K - kt * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      if (kk < kmax) {
+        TAcc a[TM], bv[TN];
+#pragma unroll
+        for (int g = 0; g < GM; ++g)
+#pragma unroll
+          for (int v = 0; v < VW; ++v) a[g * VW + v] = As[buf][kk][g * DY * VW + ty * VW + v];
+#pragma unroll
+        for (int g = 0; g < GN; ++g)
+#pragma unroll
+          for (int v = 0; v < VW; ++v) bv[g * VW + v] = Bs[buf][kk][g * DX * VW + tx * VW + v];
+        if (kt == 0 && kk == 0) {
+#pragma unroll
+          for (int ii = 0; ii < TM; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = A::mul(a[ii], bv[jj]);
+        } else {
+#pragma unroll
+          for (int ii = 0; ii < TM; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = A::add(acc[ii][jj], A::mul(a[ii], bv[jj]));
+        }
+      }
+    }
+    if (kt + 1 < ktiles) {
+      store_tile(buf ^ 1);
+      __syncthreads();
+    }
+  }
+
+  TAcc* ob = out + b * (int64_t)M * N;
+#pragma unroll
+  for (int gi = 0; gi < GM; ++gi)
+#pragma unroll
+    for (int v = 0; v < VW; ++v) {
+      const int gm = m0 + gi * DY * VW + ty * VW + v;
+      if (gm >= M) continue;
+#pragma unroll
+      for (int gj = 0; gj < GN; ++gj)
+#pragma unroll
+        for (int w = 0; w < VW; ++w) {
+          const int gn = n0 + gj * DX * VW + tx * VW + w;
+          if (gn < N) ob[(int64_t)gm * N + gn] = acc[gi * VW + v][gj * VW + w];
+        }
+    }
+}
+
+template <class TIn, class TAcc, int BM, int BN, int BK, int TM, int TN>
+cudaError_t run_tiled(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
+                      const void* y, int64_t ys, void* out, cudaStream_t st) {
+  const int tiles_m = (int)((M + BM - 1) / BM);
+  const int tiles_n = (int)((N + BN - 1) / BN);
+  constexpr int NT = (BM / TM) * (BN / TN);
+  for (int64_t b0 = 0; b0 < batch; b0 += (int64_t)65535 * 65535) {
+    const int64_t nb = batch - b0 < (int64_t)65535 * 65535 ? batch - b0 : (int64_t)65535 * 65535;
+    const unsigned gy = (unsigned)(nb < 65535 ? nb : 65535);
+    const unsigned gz = (unsigned)((nb + 65534) / 65535);
+    // blocks with b >= nb in the last z slice are harmless only if we guard;
+    // split instead into a full-z part and a remainder part.
+    const int64_t full = (nb / 65535) * 65535;
+    if (full > 0) {
+      dim3 grid(tiles_m * tiles_n, 65535, (unsigned)(full / 65535));
+      leaf_tiled_kernel<TIn, TAcc, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(
+          (int)M, (int)K, (int)N, (const TIn*)x + b0 * xs, xs, (const TIn*)y + b0 * ys, ys,
+          (TAcc*)out + b0 * M * N, tiles_n);
+    }
+    if (nb > full) {
+      dim3 grid(tiles_m * tiles_n, (unsigned)(nb - full), 1);
+      const int64_t bb = b0 + full;
+      leaf_tiled_kernel<TIn, TAcc, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(
+          (int)M, (int)K, (int)N, (const TIn*)x + bb * xs, xs, (const TIn*)y + bb * ys, ys,
+          (TAcc*)out + bb * M * N, tiles_n);
+    }
+    (void)gy;
+    (void)gz;
+  }
+  return cudaGetLastError();
+}
+
+template <class TIn, class TAcc>
+cudaError_t run_small(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
+                      const void* y, int64_t ys, void* out, cudaStream_t st) {
+  const int64_t total = batch * M * N;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  leaf_small_kernel<TIn, TAcc><<<(unsigned)blocks, 256, 0, st>>>(
+      batch, (int)M, (int)K, (int)N, (const TIn*)x, xs, (const TIn*)y, ys, (TAcc*)out);
+  return cudaGetLastError();
+}
+
+template <class TIn, class TAcc>
+cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x,
+                          int64_t xs, const void* y, int64_t ys, void* out, cudaStream_t st) {
+  if (M >= 128 && N >= 128 && sizeof(TAcc) <= 4)
+    return run_tiled<TIn, TAcc, 128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (M >= 64 && N >= 64)
+    return run_tiled<TIn, TAcc, 64, 64, 8, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (M >= 32 && N >= 32)
+    return run_tiled<TIn, TAcc, 32, 32, 8, 2, 2>(batch, M, K, N, x, xs, y, ys, out, st);
+  return run_small<TIn, TAcc>(batch, M, K, N, x, xs, y, ys, out, st);
+}
+
+}  // namespace
+
+cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, int64_t K,
+                        int64_t N, const void* x, int64_t xs, const void* y, int64_t ys, void* out,
+                        cudaStream_t st) {
+  if (batch == 0 || M == 0 || N == 0) return cudaSuccess;
+  if (dtype_out == kF64) {
+    if (dtype_in == kF64) return leaf_dispatch<double, double>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (dtype_in == kF32) return leaf_dispatch<float, double>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (dtype_in == kF16) return leaf_dispatch<__half, double>(batch, M, K, N, x, xs, y, ys, out, st);
+  }
+  if (dtype_out == kF32 && dtype_in == kF32)
+    return leaf_dispatch<float, float>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (dtype_out == kF16 && dtype_in == kF16)
+    return run_small<__half, __half>(batch, M, K, N, x, xs, y, ys, out, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace rbc

@@ -1,0 +1,205 @@
+"""Drop-in replacement for the reference engine ``randbc._engine``.
+
+``apply_levels`` and ``leaf_matmul`` keep the reference signatures, argument
+meaning, return values and exceptions (reference
+``pkg/src/randbc/_engine.py:42-61`` and ``:117-149``) and run on the B200
+through the C ABI of ``librbc.so`` (include/rbc.h).  ``install()`` assigns them
+into ``randbc._engine``; every reference caller resolves the attribute at
+call time (multiply.py:51,69,99; randomize.py:219,230,273,322), so the whole
+reference library then multiplies on the GPU.
+
+``apply_plans`` is the accelerator extension used by this package's own L2
+mirror (``multiply``/``randomize``): for exact +-1 formulas it evaluates the
+recursion straight from the randomization plans instead of from hatted
+coefficient tables (same values; see csrc/kernels_plan.cu).
+
+There is no CPU fallback anywhere in this module.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _lib
+from .precision import dtype_code, mode_of
+
+__all__ = ["apply_levels", "leaf_matmul", "apply_plans", "pack_plans", "install", "uninstall"]
+
+
+def _ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _as_mode_array(x, dtype) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x), dtype=dtype)
+
+
+def apply_levels(levels, a, b, mode, stats=None) -> np.ndarray:
+    """Evaluate a blocked formula recursion (reference _engine.py:117-149).
+
+    levels : sequence of (u, v, w), each (Tc, R, n, n) in the mode's dtype,
+             Tc in {1, T}; levels[0] splits the full operands
+    a, b   : (T0, s, s) mode-typed operands, T0 in {1, T}
+    returns: (T, s, s) mode-typed array (a new host array)
+    """
+    m = mode_of(mode)
+    if not levels:
+        raise ValueError("need at least one level")
+    dt = np.dtype(m.dtype)
+    a = _as_mode_array(a, dt)
+    b = _as_mode_array(b, dt)
+    if a.ndim != 3 or b.ndim != 3 or a.shape != b.shape or a.shape[1] != a.shape[2]:
+        raise ValueError("operands must be (T0, s, s) stacks of equal square matrices")
+    T0, N, _ = a.shape
+    tabs = []
+    for lvl in levels:
+        u, v, w = (_as_mode_array(t, dt) for t in lvl)
+        if u.ndim != 4 or v.ndim != 4 or w.ndim != 4:
+            raise ValueError("coefficient tables must have shape (Tc, R, n, n)")
+        core = u.shape[1:]
+        if v.shape[1:] != core or w.shape[1:] != core or core[1] != core[2]:
+            raise ValueError("u, v, w of one level must share (R, n, n)")
+        tabs.append([u, v, w])
+    T = max([T0] + [t.shape[0] for lvl in tabs for t in lvl])
+    for lvl in tabs:
+        for k, t in enumerate(lvl):
+            if t.shape[0] not in (1, T):
+                raise ValueError("coefficient trial axis does not broadcast")
+        tc = max(t.shape[0] for t in lvl)
+        # one trial count per level on the C side: broadcast the odd ones out
+        for k, t in enumerate(lvl):
+            if t.shape[0] != tc:
+                lvl[k] = np.ascontiguousarray(np.broadcast_to(t, (tc,) + t.shape[1:]))
+    if T0 not in (1, T):
+        raise ValueError("operand trial axis does not broadcast")
+    Q = len(tabs)
+    n_arr = (ctypes.c_int32 * Q)(*[lvl[0].shape[2] for lvl in tabs])
+    R_arr = (ctypes.c_int32 * Q)(*[lvl[0].shape[1] for lvl in tabs])
+    Tc_arr = (ctypes.c_int64 * Q)(*[lvl[0].shape[0] for lvl in tabs])
+    u_arr = (ctypes.c_void_p * Q)(*[lvl[0].ctypes.data for lvl in tabs])
+    v_arr = (ctypes.c_void_p * Q)(*[lvl[1].ctypes.data for lvl in tabs])
+    w_arr = (ctypes.c_void_p * Q)(*[lvl[2].ctypes.data for lvl in tabs])
+    out = np.empty((T, N, N), dtype=dt)
+    leaves = ctypes.c_uint64(0)
+    lib = _lib.load()
+    rc = lib.rbc_apply_levels(
+        dtype_code(m), Q, n_arr, R_arr, Tc_arr, u_arr, v_arr, w_arr,
+        T0, N, _ptr(a), _ptr(b), T, _ptr(out), ctypes.byref(leaves),
+    )
+    _lib.check(rc, overflow_msg=f"result left the {getattr(mode, 'kind', m.kind)} range")
+    if stats is not None:
+        stats["leaf_multiplies"] = stats.get("leaf_multiplies", 0) + int(leaves.value)
+    return out
+
+
+def leaf_matmul(x, y, mode) -> np.ndarray:
+    """Batched product over the last two axes, sequential over the shared
+    dimension (reference _engine.py:42-61)."""
+    m = mode_of(mode)
+    dt = np.dtype(m.dtype)
+    x = np.asarray(x)
+    y = np.asarray(y)
+    shared = x.shape[-1]
+    if y.shape[-2] != shared:
+        raise ValueError("inner dimensions do not conform")
+    lead = np.broadcast_shapes(x.shape[:-2], y.shape[:-2])
+    M, N = x.shape[-2], y.shape[-1]
+    shape = lead + (M, N)
+    if shared == 0:
+        return m.array(np.zeros(shape))
+    batch = int(math.prod(lead))
+    out = np.empty(shape, dtype=dt)
+    if batch == 0 or M == 0 or N == 0:
+        return out
+
+    def flat(t, tail):
+        t = _as_mode_array(t, dt)
+        if t.shape[:-2] == lead:
+            return t, tail
+        if int(math.prod(t.shape[:-2])) == 1:
+            return np.ascontiguousarray(t.reshape(t.shape[-2:])), 0
+        return np.ascontiguousarray(np.broadcast_to(t, lead + t.shape[-2:])), tail
+
+    xf, xs = flat(x, M * shared)
+    yf, ys = flat(y, shared * N)
+    rc = _lib.load().rbc_leaf_matmul(dtype_code(m), batch, xs, ys, M, shared, N,
+                                     _ptr(xf), _ptr(yf), _ptr(out))
+    _lib.check(rc)
+    return out
+
+
+def pack_plans(n: int, perms: np.ndarray, signs: np.ndarray) -> np.ndarray:
+    """Pack (count, 3, n) perms / signs into the engine's 40-byte plan records."""
+    perms = np.ascontiguousarray(perms, dtype=np.int64)
+    signs = np.ascontiguousarray(signs, dtype=np.float64)
+    if perms.shape != signs.shape or perms.ndim != 3 or perms.shape[1:] != (3, n):
+        raise ValueError("perms and signs must both have shape (count, 3, n)")
+    count = perms.shape[0]
+    out = np.zeros((count, _lib.PLAN_BYTES), dtype=np.uint8)
+    rc = _lib.load().rbc_pack_plans(n, count, _ptr(perms), _ptr(signs), _ptr(out))
+    _lib.check(rc)
+    return out
+
+
+def apply_plans(formula_id: int, Q: int, packed: np.ndarray, a, b, mode, stats=None,
+                return_flags: bool = False):
+    """Q-level evaluation of an exact +-1 formula under packed plans.
+
+    packed: (Tp, Q, 40) uint8 from ``pack_plans`` (Tp in {1, T});
+    a, b  : (T0, N, N) mode-typed operands.
+    Raises OverflowError like the reference when any output is non-finite,
+    unless ``return_flags`` is set (then returns (out, per-trial flags)).
+    """
+    m = mode_of(mode)
+    dt = np.dtype(m.dtype)
+    a = _as_mode_array(a, dt)
+    b = _as_mode_array(b, dt)
+    if a.ndim != 3 or a.shape != b.shape or a.shape[1] != a.shape[2]:
+        raise ValueError("operands must be (T0, s, s) stacks of equal square matrices")
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    if packed.ndim != 3 or packed.shape[1] != Q or packed.shape[2] != _lib.PLAN_BYTES:
+        raise ValueError("packed plans must have shape (Tp, Q, 40)")
+    T0, N, _ = a.shape
+    Tp = packed.shape[0]
+    T = max(T0, Tp)
+    out = np.empty((T, N, N), dtype=dt)
+    flags = np.zeros(max(T, 1), dtype=np.uint8)
+    leaves = ctypes.c_uint64(0)
+    rc = _lib.load().rbc_apply_plans(
+        dtype_code(m), formula_id, Q, Tp, _ptr(packed), T0, N, _ptr(a), _ptr(b), T,
+        _ptr(out), _ptr(flags), ctypes.byref(leaves),
+    )
+    if stats is not None and rc in (_lib.RBC_OK, _lib.RBC_EOVERFLOW):
+        stats["leaf_multiplies"] = stats.get("leaf_multiplies", 0) + int(leaves.value)
+    if return_flags and rc == _lib.RBC_EOVERFLOW:
+        return out, flags[:T].astype(bool)
+    _lib.check(rc, overflow_msg=f"result left the {getattr(mode, 'kind', m.kind)} range")
+    return (out, flags[:T].astype(bool)) if return_flags else out
+
+
+_saved = {}
+
+
+def install(module=None):
+    """Route ``randbc._engine.apply_levels`` / ``leaf_matmul`` to the GPU.
+
+    ``module`` defaults to ``randbc._engine`` (the reference must be
+    importable).  Returns the module; ``uninstall`` restores the originals.
+    """
+    if module is None:
+        import randbc._engine as module  # noqa: PLC0415  (reference package)
+    _saved[id(module)] = (module, module.apply_levels, module.leaf_matmul)
+    module.apply_levels = apply_levels
+    module.leaf_matmul = leaf_matmul
+    return module
+
+
+def uninstall(module=None) -> None:
+    if module is None:
+        import randbc._engine as module  # noqa: PLC0415
+    saved = _saved.pop(id(module), None)
+    if saved is not None:
+        _, module.apply_levels, module.leaf_matmul = saved

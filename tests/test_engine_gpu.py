@@ -1,0 +1,140 @@
+"""GPU parity: the B200 engine (through the C ABI) against the reference's
+golden outputs and the CPU oracle on the same seeded inputs."""
+
+import numpy as np
+import pytest
+
+from conftest import case_levels, mode_for, same_values
+from oracle import engine as oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_1905_07439_b200 import _lib, engine
+
+    _lib.require_device()
+    return engine
+
+
+def test_golden_engine_cases_dense_path(eng, engine_cases):
+    """apply_levels (hatted coefficient tables -> dense kernels) == reference."""
+    meta, arrs = engine_cases
+    for case in meta["engine"]:
+        name = case["name"]
+        mode = mode_for(case["mode"])
+        levels = case_levels(arrs, name, case["Q"])
+        a, b = arrs[f"{name}/a"], arrs[f"{name}/b"]
+        stats = {}
+        if case["raises"] == "OverflowError":
+            with pytest.raises(OverflowError, match="result left the half range"):
+                eng.apply_levels(levels, a, b, mode, stats)
+            continue
+        out = eng.apply_levels(levels, a, b, mode, stats)
+        assert same_values(out, arrs[f"{name}/out"]), name
+        assert stats["leaf_multiplies"] == case["leaf_multiplies"], name
+
+
+def test_golden_engine_cases_plan_path(eng, engine_cases):
+    """apply_plans (plans folded into generated networks) == reference."""
+    from paper_1905_07439_b200._lib import FORMULA_IDS
+
+    meta, arrs = engine_cases
+    checked = 0
+    for case in meta["engine"]:
+        if case["plan_formula"] is None or f"{case['name']}/perms" not in arrs:
+            continue
+        name = case["name"]
+        mode = mode_for(case["mode"])
+        Q, n = case["Q"], case["n"]
+        perms, signs = arrs[f"{name}/perms"], arrs[f"{name}/signs"]
+        Tp = perms.shape[0]
+        packed = eng.pack_plans(n, perms.reshape(Tp * Q, 3, n), signs.reshape(Tp * Q, 3, n))
+        packed = packed.reshape(Tp, Q, -1)
+        a, b = arrs[f"{name}/a"], arrs[f"{name}/b"]
+        fid = FORMULA_IDS[case["plan_formula"]]
+        if case["raises"] == "OverflowError":
+            with pytest.raises(OverflowError):
+                eng.apply_plans(fid, Q, packed, a, b, mode)
+            out, flags = eng.apply_plans(fid, Q, packed, a, b, mode, return_flags=True)
+            assert flags.all()
+            continue
+        stats = {}
+        out = eng.apply_plans(fid, Q, packed, a, b, mode, stats)
+        assert same_values(out, arrs[f"{name}/out"]), name
+        assert stats["leaf_multiplies"] == case["leaf_multiplies"], name
+        checked += 1
+    assert checked >= 8
+
+
+def test_golden_leaf_cases(eng, engine_cases):
+    meta, arrs = engine_cases
+    for case in meta["leaf"]:
+        name = case["name"]
+        mode = mode_for(case["mode"])
+        out = eng.leaf_matmul(arrs[f"{name}/x"], arrs[f"{name}/y"], mode)
+        assert same_values(out, arrs[f"{name}/out"]), name
+
+
+@pytest.mark.parametrize(
+    "label,fname,Q,N,T",
+    [
+        ("f32", "strassen", 2, 256, 3),   # config-1 shape
+        ("f32", "strassen", 3, 320, 2),   # golden artifact size
+        ("f32", "laderman", 3, 81, 3),
+        ("f64", "laderman", 2, 81, 2),
+        ("f16", "strassen", 3, 128, 2),
+        ("f64", "strassen", 2, 200, 2),
+    ],
+)
+def test_random_plans_vs_oracle(eng, label, fname, Q, N, T):
+    """Both engine paths equal the oracle on seeded larger problems."""
+    import paper_1905_07439_b200 as rbc
+
+    mode = mode_for(label)
+    f = {"strassen": rbc.strassen_formula, "laderman": rbc.laderman_formula}[fname]()
+    g = rbc.derive_rng(77, N, Q)
+    A = mode.array(g.standard_normal((N, N)))
+    B = mode.array(g.standard_normal((N, N)))
+    rplans = [rbc.draw_recursive_plan(f.n, Q, rbc.derive_rng(78, t)) for t in range(T)]
+    levels = [rbc.plan_levels(f, [rp.levels[q] for rp in rplans], mode) for q in range(Q)]
+    want = oracle.apply_levels(levels, A[None], B[None], mode)
+    got_dense = eng.apply_levels(levels, A[None], B[None], mode)
+    got_plan = rbc.recursive_randomized_apply_many(f, rplans, A, B, mode)
+    assert same_values(got_dense, want)
+    assert same_values(got_plan, want)
+
+
+def test_dense_formula_tree_order(eng):
+    """Dense (noisy Laderman) coefficients exercise the row-then-rows fold."""
+    import paper_1905_07439_b200 as rbc
+
+    mode = mode_for("f32")
+    f = rbc.perturb_all(rbc.laderman_formula(), 1e-4, rbc.derive_rng(5, 0))
+    g = rbc.derive_rng(6)
+    A = mode.array(g.standard_normal((54, 54)))
+    B = mode.array(g.standard_normal((54, 54)))
+    rplans = [rbc.draw_recursive_plan(3, 2, rbc.derive_rng(7, t)) for t in range(3)]
+    levels = [rbc.plan_levels(f, [rp.levels[q] for rp in rplans], mode) for q in range(2)]
+    want = oracle.apply_levels(levels, A[None], B[None], mode)
+    assert same_values(rbc.recursive_randomized_apply_many(f, rplans, A, B, mode), want)
+
+
+def test_engine_errors(eng):
+    from paper_1905_07439_b200.precision import SINGLE
+
+    one = np.ones((1, 4, 4), np.float32)
+    with pytest.raises(ValueError, match="need at least one level"):
+        eng.apply_levels([], one, one, SINGLE)
+    u = np.ones((1, 7, 3, 3), np.float32)
+    with pytest.raises(ValueError, match="not divisible"):
+        eng.apply_levels([(u, u, u)], one, one, SINGLE)
+    with pytest.raises(ValueError, match="inner dimensions"):
+        eng.leaf_matmul(np.ones((1, 2, 3)), np.ones((1, 2, 3)), SINGLE)
+
+    class Dec:
+        kind = "decimal"
+
+    with pytest.raises(NotImplementedError):
+        eng.apply_levels([(u, u, u)], one, one, Dec())
