@@ -76,6 +76,13 @@ int rbc_abi_version(void);
 const char* rbc_last_error(void);
 int rbc_device_count(void);
 
+/* Stage profiler: when enabled, every engine launch is bracketed by CUDA
+ * events on its own stream and tagged with its algorithmic bytes and flops.
+ * rbc_profile_summary synchronises the recorded events and writes a JSON
+ * object {stage: {count, ms, bytes, flops}}; returns the length needed. */
+void rbc_profile_enable(int on);
+int64_t rbc_profile_summary(char* buf, size_t len);
+
 /* ---- reference engine boundary (host buffers, synchronous) --------------- */
 
 /* randbc._engine.apply_levels  (_engine.py:117-149).
@@ -141,6 +148,25 @@ int rbc_rel_errors_async(int dtype, int64_t T, int64_t N, const void* c, const d
 /* nonfinite[t] = 1 if x[t] (N*N elements) holds a non-finite value. */
 int rbc_nonfinite_async(int dtype, int64_t T, int64_t N, const void* x, uint8_t* nonfinite,
                         void* stream);
+
+/* ---- error trials: the per-pair work of the distribution experiments ----
+ * (experiments.py:248-261, 327-379): for each trial t with operands
+ * (a[t], b[t]) in the mode, ref_t = binary64 inner-product truth, then the
+ * randomized product under rand_plans[t] (packed (T, Q)) and/or the
+ * deterministic product (identity plans), each with its relative Frobenius
+ * error against ref_t and a per-trial non-finite flag.
+ * Host variant: host buffers in/out, H2D/D2H inside the call. */
+int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
+                     const void* b, const void* rand_plans, int with_det, double* err_rand,
+                     double* err_det, uint8_t* nonfinite_rand, uint8_t* nonfinite_det);
+
+size_t rbc_error_trials_workspace_bytes(int dtype, int formula, int Q, int64_t T, int64_t N);
+/* Device variant: det_plans is a device (1, Q) identity table or NULL. */
+int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
+                           const void* b, const void* rand_plans, const void* det_plans,
+                           double* err_rand, double* err_det, uint8_t* nonfinite_rand,
+                           uint8_t* nonfinite_det, void* workspace, size_t workspace_bytes,
+                           void* stream);
 
 #ifdef __cplusplus
 }

@@ -29,6 +29,8 @@ EXPORTS = (
     "rbc_abi_version",
     "rbc_last_error",
     "rbc_device_count",
+    "rbc_profile_enable",
+    "rbc_profile_summary",
     "rbc_apply_levels",
     "rbc_leaf_matmul",
     "rbc_pack_plans",
@@ -42,6 +44,9 @@ EXPORTS = (
     "rbc_rel_errors_scratch_bytes",
     "rbc_rel_errors_async",
     "rbc_nonfinite_async",
+    "rbc_error_trials",
+    "rbc_error_trials_workspace_bytes",
+    "rbc_error_trials_async",
 )
 
 _lock = threading.Lock()
@@ -61,6 +66,8 @@ def _declare(lib):
         "rbc_abi_version": (c_int, []),
         "rbc_last_error": (ctypes.c_char_p, []),
         "rbc_device_count": (c_int, []),
+        "rbc_profile_enable": (None, [c_int]),
+        "rbc_profile_summary": (c_i64, [ctypes.c_char_p, c_size]),
         "rbc_apply_levels": (
             c_int,
             [c_int, c_int, P(c_i32), P(c_i32), P(c_i64), P(c_vp), P(c_vp), P(c_vp),
@@ -91,6 +98,16 @@ def _declare(lib):
         "rbc_rel_errors_scratch_bytes": (c_size, [c_i64]),
         "rbc_rel_errors_async": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
         "rbc_nonfinite_async": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp]),
+        "rbc_error_trials": (
+            c_int,
+            [c_int, c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp],
+        ),
+        "rbc_error_trials_workspace_bytes": (c_size, [c_int, c_int, c_int, c_i64, c_i64]),
+        "rbc_error_trials_async": (
+            c_int,
+            [c_int, c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+             c_vp, c_size, c_vp],
+        ),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -131,6 +148,21 @@ def check(rc: int, *, overflow_msg: str | None = None) -> None:
     if rc == RBC_EUNSUPPORTED:
         raise NotImplementedError(msg)
     raise RuntimeError(msg or f"librbc status {rc}")
+
+
+def profile_enable(on: bool = True) -> None:
+    load().rbc_profile_enable(1 if on else 0)
+
+
+def profile_summary() -> dict:
+    """{stage: {count, ms, bytes, flops}} of the launches since profile_enable."""
+    import json
+
+    lib = load()
+    need = lib.rbc_profile_summary(None, 0)
+    buf = ctypes.create_string_buffer(int(need) + 16)
+    lib.rbc_profile_summary(buf, len(buf))
+    return json.loads(buf.value.decode())
 
 
 def require_device() -> None:

@@ -41,6 +41,8 @@ static int set_error(int code, const char* fmt, ...) {
   return code;
 }
 
+int set_error_public(int code, const char* msg) { return set_error(code, "%s", msg); }
+
 int fail_cuda(cudaError_t e, const char* expr, const char* file, int line) {
   return set_error(RBC_ERUNTIME, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
                    cudaGetErrorString(e), file, line, expr);
@@ -107,6 +109,54 @@ static size_t ws_for(const Geometry& g, int dtype, int64_t T) {
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// ---------------------------------------------------------- stage profiler --
+struct ProfRec {
+  std::string name;
+  cudaEvent_t ev0, ev1;
+  double bytes, flops;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_prof_pool;
+
+bool prof_on() { return g_prof_on; }
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_record(cudaStream_t st, const char* name, double bytes, double flops, bool start) {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  if (start) {
+    ProfRec r{name, prof_event(), nullptr, bytes, flops};
+    cudaEventRecord(r.ev0, st);
+    g_prof.push_back(r);
+  } else {
+    for (auto it = g_prof.rbegin(); it != g_prof.rend(); ++it)
+      if (!it->ev1 && it->name == name) {
+        it->ev1 = prof_event();
+        cudaEventRecord(it->ev1, st);
+        break;
+      }
+  }
+}
+
+static void prof_clear() {
+  for (auto& r : g_prof) {
+    if (r.ev0) g_prof_pool.push_back(r.ev0);
+    if (r.ev1) g_prof_pool.push_back(r.ev1);
+  }
+  g_prof.clear();
+}
+
 // RBC_DEBUG_SYNC=1: synchronise after every launch so a fault is attributed
 // to the stage that caused it.
 static bool debug_sync() {
@@ -171,6 +221,10 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
         const int n = g.lv[q].n, R = g.lv[q].R;
         void* dst = (q == g.Q - 1) ? (which == 0 ? bufX : bufY) : ((q & 1) ? pong : ping);
         cudaError_t e;
+        const double mbq = (double)(s / n);
+        Stage stage(st, p.plan ? "expand_plan" : "expand_dense",
+                    ((cur_ts ? (double)nt : 1.0) * K * s * s + (double)nt * K * R * mbq * mbq) * es,
+                    (double)nt * K * R * mbq * mbq * n * n * 2.0);
         if (p.plan) {
           const int64_t pts = p.Tp == 1 ? 0 : g.Q;
           const PlanLevel* pl = p.plans + (p.Tp == 1 ? 0 : t0 * g.Q);
@@ -193,6 +247,8 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
     // --- leaves
     const int64_t m = g.leaf_m;
     {
+      Stage stage(st, dt == kF64 ? "leaf_f64" : dt == kF32 ? "leaf_f32" : "leaf_f16",
+                  3.0 * nt * g.leaves * m * m * es, 2.0 * nt * g.leaves * (double)m * m * m);
       cudaError_t e = launch_leaf(dt, dt, nt * g.leaves, m, m, m, bufX, m * m, bufY, m * m, ping, st);
       e = stage_done(e, st);
       if (e != cudaSuccess) return fail_cuda(e, "leaf", __FILE__, __LINE__);
@@ -206,6 +262,10 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
       void* dst = q == 0 ? (char*)p.out + (size_t)t0 * N2 * es : (cur == ping ? pong : ping);
       uint8_t* nf = (q == 0 && p.nonfinite) ? p.nonfinite + t0 : nullptr;
       cudaError_t e;
+      const double sq = (double)(mb * n);
+      Stage stage(st, p.plan ? "contract_plan" : "contract_dense",
+                  ((double)nt * K * R * mb * mb + (double)nt * K * sq * sq) * es,
+                  (double)nt * K * sq * sq * R * 2.0);
       if (p.plan) {
         const int64_t pts = p.Tp == 1 ? 0 : g.Q;
         const PlanLevel* pl = p.plans + (p.Tp == 1 ? 0 : t0 * g.Q);
@@ -290,6 +350,51 @@ using namespace rbc;
 extern "C" {
 
 int rbc_abi_version(void) { return RBC_ABI_VERSION; }
+
+void rbc_profile_enable(int on) {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  prof_clear();
+  g_prof_on = on != 0;
+}
+
+int64_t rbc_profile_summary(char* buf, size_t len) {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  struct Agg {
+    int64_t count = 0;
+    double ms = 0, bytes = 0, flops = 0;
+  };
+  std::vector<std::pair<std::string, Agg>> aggs;
+  for (auto& r : g_prof) {
+    if (!r.ev1) continue;
+    if (cudaEventSynchronize(r.ev1) != cudaSuccess) continue;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.ev0, r.ev1);
+    auto it = std::find_if(aggs.begin(), aggs.end(), [&](auto& p) { return p.first == r.name; });
+    if (it == aggs.end()) {
+      aggs.push_back({r.name, Agg{}});
+      it = aggs.end() - 1;
+    }
+    it->second.count += 1;
+    it->second.ms += ms;
+    it->second.bytes += r.bytes;
+    it->second.flops += r.flops;
+  }
+  std::string js = "{";
+  char tmp[512];
+  for (size_t i = 0; i < aggs.size(); ++i) {
+    const Agg& a = aggs[i].second;
+    snprintf(tmp, sizeof tmp, "%s\"%s\": {\"count\": %lld, \"ms\": %.6f, \"bytes\": %.6e, \"flops\": %.6e}",
+             i ? ", " : "", aggs[i].first.c_str(), (long long)a.count, a.ms, a.bytes, a.flops);
+    js += tmp;
+  }
+  js += "}";
+  if (buf && len > 0) {
+    const size_t n = std::min(len - 1, js.size());
+    memcpy(buf, js.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)js.size() + 1;
+}
 
 const char* rbc_last_error(void) { return g_last_error.c_str(); }
 
@@ -571,6 +676,80 @@ int rbc_leaf_matmul(int dtype, int64_t batch, int64_t xs, int64_t ys, int64_t M,
   CUDA_TRY(cudaMemcpy(dy, y, yb, cudaMemcpyHostToDevice));
   RBC_TRY(finish_sync(rbc_leaf_matmul_async(dtype, dtype, batch, xs, ys, M, K, N, dx, dy, dout, nullptr)));
   CUDA_TRY(cudaMemcpy(out, dout, ob, cudaMemcpyDeviceToHost));
+  return RBC_OK;
+}
+
+static cudaStream_t host_stream() {
+  static cudaStream_t s = [] {
+    cudaStream_t x = nullptr;
+    cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+    return x;
+  }();
+  return s;
+}
+
+int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
+                     const void* b, const void* rand_plans, int with_det, double* err_rand,
+                     double* err_det, uint8_t* nf_rand, uint8_t* nf_det) {
+  if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);
+  const int n = formula_n(formula);
+  if (!n) return set_error(RBC_EVALUE, "unknown formula id %d", formula);
+  if (Q < 1) return set_error(RBC_EVALUE, "need at least one level");
+  if (T < 0 || N < 0) return set_error(RBC_EVALUE, "negative size");
+  {
+    int64_t s = N;
+    for (int q = 0; q < Q; ++q) {
+      if (s % n) return set_error(RBC_EVALUE, "operand size not divisible by block grid");
+      s /= n;
+    }
+  }
+  if (!rand_plans && !with_det) return set_error(RBC_EVALUE, "no product requested");
+  RBC_TRY(check_device());
+  if (T == 0 || N == 0) return RBC_OK;
+  const size_t es = dtype_size(dtype);
+  const size_t ab = (size_t)T * N * N * es;
+  const size_t pb = rand_plans ? (size_t)T * Q * RBC_PLAN_BYTES : 0;
+  const size_t db = (size_t)Q * RBC_PLAN_BYTES;
+  std::lock_guard<std::mutex> lock(arena().mu);
+  const size_t fixed = 2 * align_up(ab) + align_up(pb) + align_up(db) + 2 * align_up(T * 8) +
+                       2 * align_up(T) + 4096;
+  const size_t one = rbc_error_trials_workspace_bytes(dtype, formula, Q, 1, N);
+  const size_t ws = host_ws_budget(fixed, rbc_error_trials_workspace_bytes(dtype, formula, Q, T, N));
+  if (ws < one) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
+  RBC_TRY(arena().reserve(fixed + ws + 256));
+  Arena& A = arena();
+  void* da = A.take(ab);
+  void* dbb = A.take(ab);
+  void* dpl = A.take(pb);
+  void* ddet = A.take(db);
+  double* derr_r = (double*)A.take(T * 8);
+  double* derr_d = (double*)A.take(T * 8);
+  uint8_t* dnf_r = (uint8_t*)A.take(T);
+  uint8_t* dnf_d = (uint8_t*)A.take(T);
+  void* dws = A.take(ws);
+  cudaStream_t st = host_stream();
+  std::vector<PlanLevel> ident(Q);
+  for (int q = 0; q < Q; ++q) {
+    memset(&ident[q], 0, sizeof(PlanLevel));
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < n; ++j) ident[q].perm[i][j] = ident[q].inv[i][j] = (int8_t)j;
+  }
+  CUDA_TRY(cudaMemcpyAsync(da, a, ab, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dbb, b, ab, cudaMemcpyHostToDevice, st));
+  if (pb) CUDA_TRY(cudaMemcpyAsync(dpl, rand_plans, pb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(ddet, ident.data(), db, cudaMemcpyHostToDevice, st));
+  RBC_TRY(rbc_error_trials_async(dtype, formula, Q, T, N, da, dbb, pb ? dpl : nullptr,
+                                 with_det ? ddet : nullptr, derr_r, derr_d, dnf_r, dnf_d, dws, ws,
+                                 st));
+  if (pb) {
+    CUDA_TRY(cudaMemcpyAsync(err_rand, derr_r, T * 8, cudaMemcpyDeviceToHost, st));
+    if (nf_rand) CUDA_TRY(cudaMemcpyAsync(nf_rand, dnf_r, T, cudaMemcpyDeviceToHost, st));
+  }
+  if (with_det) {
+    CUDA_TRY(cudaMemcpyAsync(err_det, derr_d, T * 8, cudaMemcpyDeviceToHost, st));
+    if (nf_det) CUDA_TRY(cudaMemcpyAsync(nf_det, dnf_d, T, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
   return RBC_OK;
 }
 

@@ -17,6 +17,23 @@ inline size_t dtype_size(int dt) { return dt == kF64 ? 8 : dt == kF32 ? 4 : 2; }
 // Records a CUDA failure as the thread's last error; returns RBC_ERUNTIME.
 int fail_cuda(cudaError_t e, const char* expr, const char* file, int line);
 
+// ---- stage profiler (rbc_profile_enable) ------------------------------------
+// When enabled, Stage records a CUDA event pair around a launch on its stream,
+// tagged with the launch's algorithmic bytes and flops.
+bool prof_on();
+void prof_record(cudaStream_t st, const char* name, double bytes, double flops, bool start);
+struct Stage {
+  cudaStream_t st;
+  const char* name;
+  double bytes, flops;
+  Stage(cudaStream_t s, const char* n, double b, double f) : st(s), name(n), bytes(b), flops(f) {
+    if (prof_on()) prof_record(st, name, bytes, flops, true);
+  }
+  ~Stage() {
+    if (prof_on()) prof_record(st, name, bytes, flops, false);
+  }
+};
+
 // Largest vector width (elements per thread) that divides the block side.
 int pick_width(int dtype, int64_t mb, int cap_elems);
 

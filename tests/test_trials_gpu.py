@@ -1,0 +1,84 @@
+"""GPU: the error-trial pipeline (truth, products, relative errors) against
+the CPU oracle on the config seed layout, host-buffer and device paths."""
+
+import numpy as np
+import pytest
+
+from oracle import engine as oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_errors(cfg, f, A, B, rplans):
+    from paper_1905_07439_b200.multiply import mode_tensors
+    from paper_1905_07439_b200.randomize import plan_levels
+
+    out = {"err_det": [], "err_rand": [], "nf_det": [], "nf_rand": []}
+    for t in range(A.shape[0]):
+        ref = oracle.standard_multiply(A[t].astype(np.float64), B[t].astype(np.float64))
+        for key, levels in (
+            ("det", [mode_tensors(f, cfg.mode)] * cfg.Q),
+            ("rand", [plan_levels(f, [rplans[t].levels[q]], cfg.mode) for q in range(cfg.Q)]),
+        ):
+            with np.errstate(all="ignore"):
+                try:
+                    C = oracle.apply_levels(levels, A[t][None], B[t][None], cfg.mode)
+                    out["err_" + key].append(oracle.rel_errors(C, ref)[0])
+                    out["nf_" + key].append(False)
+                except OverflowError:
+                    out["err_" + key].append(np.nan)
+                    out["nf_" + key].append(True)
+    return {k: np.array(v) for k, v in out.items()}
+
+
+@pytest.mark.parametrize(
+    "name,N,Q,T",
+    [("c1", 64, 2, 5), ("c2", 81, 3, 4), ("c4", 64, 3, 4), ("c5", 128, 3, 2)],
+)
+def test_error_trials_match_oracle(name, N, Q, T):
+    from dataclasses import replace
+
+    from paper_1905_07439_b200.configs import get_config, make_pairs
+    from paper_1905_07439_b200.trials import error_trials
+
+    cfg = replace(get_config(name), N=N, Q=Q)
+    f = cfg.formula_obj()
+    A, B = make_pairs(cfg, 1, T)
+    rplans = [cfg.plan(cfg.plan_key(p)) for p in range(1, T + 1)]
+    got = error_trials(f, Q, A, B, cfg.mode, rplans=rplans)
+    want = _oracle_errors(cfg, f, A, B, rplans)
+    for key in ("det", "rand"):
+        assert np.array_equal(got["nf_" + key], want["nf_" + key])
+        ok = ~want["nf_" + key]
+        np.testing.assert_allclose(got["err_" + key][ok], want["err_" + key][ok], rtol=1e-12, atol=0)
+
+
+def test_device_runner_matches_host_call():
+    import torch
+
+    from paper_1905_07439_b200.configs import get_config, make_pairs
+    from paper_1905_07439_b200.randomize import pack_recursive_plans
+    from paper_1905_07439_b200.trials import DeviceErrorTrials, error_trials
+
+    from dataclasses import replace
+
+    cfg = replace(get_config("c2"), N=81, Q=3)
+    f = cfg.formula_obj()
+    T = 6
+    A, B = make_pairs(cfg, 1, T)
+    packed = pack_recursive_plans([cfg.plan(p) for p in range(1, T + 1)], cfg.Q, cfg.n)
+    host = error_trials(f, cfg.Q, A, B, cfg.mode, packed=packed)
+    dev = torch.device("cuda:0")
+    # a small workspace forces several trial chunks: values must not change
+    r = DeviceErrorTrials(f, cfg.Q, cfg.N, cfg.mode, T, device=dev, workspace_bytes=1)
+    import ctypes  # noqa: F401
+
+    from paper_1905_07439_b200 import _lib
+    from paper_1905_07439_b200.precision import dtype_code
+
+    one = _lib.load().rbc_error_trials_workspace_bytes(dtype_code(cfg.mode), r.fid, cfg.Q, 2, cfg.N)
+    r.ws = torch.empty(one, dtype=torch.uint8, device=dev)
+    r.run(torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), torch.from_numpy(packed).to(dev))
+    torch.cuda.synchronize()
+    assert np.array_equal(r.err_rand.cpu().numpy(), host["err_rand"])
+    assert np.array_equal(r.err_det.cpu().numpy(), host["err_det"])
