@@ -167,6 +167,14 @@ static bool debug_sync() {
   return on;
 }
 
+// RBC_NO_FUSION=1 forces the plain breadth-first schedule (tests compare both).
+static bool fusion_enabled() {
+  const char* v = getenv("RBC_NO_FUSION");
+  return !(v && v[0] == '1');
+}
+
+static constexpr size_t kMaxSubtreeSmem = 200 * 1024;
+
 static cudaError_t stage_done(cudaError_t e, cudaStream_t st) {
   if (e != cudaSuccess || !debug_sync()) return e;
   return cudaStreamSynchronize(st);
@@ -209,6 +217,22 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
   void* pong = base + 3 * buf_elems * es;
   if (p.nonfinite) CUDA_TRY(cudaMemsetAsync(p.nonfinite, 0, (size_t)p.T, st));
 
+  // Fuse the bottom levels into one shared-memory subtree kernel when an
+  // instantiation exists for (formula, depth, leaf side) and fits on chip.
+  int fuseL = 0;
+  if (p.plan && fusion_enabled()) {
+    for (int L = std::min(2, g.Q); L >= 1 && !fuseL; --L) {
+      const size_t sm = subtree_smem_bytes(dt, p.formula, L, (int)g.leaf_m);
+      if (sm && sm <= kMaxSubtreeSmem) fuseL = L;
+    }
+  }
+  const int q0 = g.Q - fuseL;  // levels evaluated breadth-first over HBM
+  int64_t K_q0 = 1, s_q0 = g.N;
+  for (int q = 0; q < q0; ++q) {
+    K_q0 *= g.lv[q].R;
+    s_q0 /= g.lv[q].n;
+  }
+
   for (int64_t t0 = 0; t0 < p.T; t0 += chunk) {
     const int64_t nt = std::min(chunk, p.T - t0);
     // --- expansions of A and B
@@ -217,9 +241,9 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
       int64_t cur_ts = p.T0 == 1 ? 0 : N2;
       if (p.T0 != 1) cur = (const char*)cur + (size_t)t0 * N2 * es;
       int64_t K = 1, s = g.N;
-      for (int q = 0; q < g.Q; ++q) {
+      for (int q = 0; q < q0; ++q) {
         const int n = g.lv[q].n, R = g.lv[q].R;
-        void* dst = (q == g.Q - 1) ? (which == 0 ? bufX : bufY) : ((q & 1) ? pong : ping);
+        void* dst = (q == q0 - 1) ? (which == 0 ? bufX : bufY) : ((q & 1) ? pong : ping);
         cudaError_t e;
         const double mbq = (double)(s / n);
         Stage stage(st, p.plan ? "expand_plan" : "expand_dense",
@@ -244,9 +268,25 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
         s = mb;
       }
     }
-    // --- leaves
+    // --- leaves (or the fused bottom subtree)
     const int64_t m = g.leaf_m;
-    {
+    if (fuseL) {
+      const bool top = q0 == 0;
+      const char* xs = top ? (const char*)p.a + (p.T0 == 1 ? 0 : (size_t)t0 * N2 * es) : (const char*)bufX;
+      const char* ys = top ? (const char*)p.b + (p.T0 == 1 ? 0 : (size_t)t0 * N2 * es) : (const char*)bufY;
+      const int64_t xy_ts = top ? (p.T0 == 1 ? 0 : N2) : K_q0 * s_q0 * s_q0;
+      void* dst = top ? (char*)p.out + (size_t)t0 * N2 * es : ping;
+      const int64_t pts = p.Tp == 1 ? 0 : g.Q;
+      const PlanLevel* pl = p.plans + (p.Tp == 1 ? 0 : t0 * g.Q);
+      Stage stage(st, "subtree_fused",
+                  ((top && p.T0 == 1 ? 2.0 : 2.0 * nt) + nt) * (double)K_q0 * s_q0 * s_q0 * es,
+                  2.0 * nt * g.leaves * (double)m * m * m);
+      cudaError_t e = launch_subtree(dt, p.formula, fuseL, (int)m, xs, ys, xy_ts, K_q0, dst, pl,
+                                     pts, q0, nt, (top && p.nonfinite) ? p.nonfinite + t0 : nullptr,
+                                     st);
+      e = stage_done(e, st);
+      if (e != cudaSuccess) return fail_cuda(e, "subtree", __FILE__, __LINE__);
+    } else {
       Stage stage(st, dt == kF64 ? "leaf_f64" : dt == kF32 ? "leaf_f32" : "leaf_f16",
                   3.0 * nt * g.leaves * m * m * es, 2.0 * nt * g.leaves * (double)m * m * m);
       cudaError_t e = launch_leaf(dt, dt, nt * g.leaves, m, m, m, bufX, m * m, bufY, m * m, ping, st);
@@ -255,8 +295,8 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
     }
     // --- contractions, innermost level first
     const void* cur = ping;
-    int64_t K = g.leaves, mb = m;
-    for (int q = g.Q - 1; q >= 0; --q) {
+    int64_t K = K_q0, mb = s_q0;
+    for (int q = q0 - 1; q >= 0; --q) {
       const int n = g.lv[q].n, R = g.lv[q].R;
       K /= R;
       void* dst = q == 0 ? (char*)p.out + (size_t)t0 * N2 * es : (cur == ping ? pong : ping);

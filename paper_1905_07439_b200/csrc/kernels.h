@@ -57,6 +57,16 @@ cudaError_t launch_contract_plan(int dtype, int formula, const void* ch, int64_t
 int formula_n(int formula);
 int formula_R(int formula);
 
+// Fused bottom subtree (kernels_fused.cu): L levels below q0 for every
+// (trial, level-q0 block) in shared memory.  x, y: (T, K0, s0, s0) blocks
+// (xy_tstride elements per trial, 0 = broadcast), out: (T, K0, s0, s0).
+// subtree_smem_bytes returns 0 when no instantiation covers (formula, L, M).
+size_t subtree_smem_bytes(int dtype, int formula, int L, int M);
+cudaError_t launch_subtree(int dtype, int formula, int L, int M, const void* x, const void* y,
+                           int64_t xy_tstride, int64_t K0, void* out, const PlanLevel* plans,
+                           int64_t plan_tstride, int q0, int64_t ntr, uint8_t* nonfinite,
+                           cudaStream_t st);
+
 // ---- dense path: arbitrary coefficient tables (Tc, R, n, n) --------------
 cudaError_t launch_expand_dense(int dtype, const void* x, int64_t x_tstride, int64_t K, int64_t s,
                                 int n, int R, const void* coeff, int64_t c_tstride, void* out,

@@ -1,0 +1,256 @@
+// Fused subtree kernel: the bottom L levels of the recursion for one
+// (trial, level-q0 block) pair, entirely in shared memory.
+//
+// The reference evaluates every level breadth-first over the whole batch
+// (_engine.py:117-149).  With small leaves (config 2: 3x3, the golden
+// artifact at Q=5: 10x10) the deepest levels are the largest arrays but each
+// subtree is tiny, so breadth-first HBM round trips dominate.  Here one CTA
+// takes the level-q0 operand blocks X, Y (s0 x s0, s0 = M * n^L) of one
+// trial, expands them L levels into shared memory, forms the R^L leaf
+// products there, contracts back to the s0 x s0 product block and writes
+// only that to HBM.  Every output element sees exactly the same operation
+// sequence as in the breadth-first evaluation (the per-element chains are
+// independent of the evaluation schedule), so values are
+// identical.
+//
+// Shared memory: for l = 1..L, X_l and Y_l (R^l blocks of (s0/n^l)^2), plus
+// the leaf products P_L (R^L M^2).  Contractions reuse the dead X_l buffers.
+
+#include "kernels.h"
+#include "plan_ops.cuh"
+
+namespace rbc {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int B, int E>
+struct Pow {
+  static constexpr int v = B * Pow<B, E - 1>::v;
+};
+template <int B>
+struct Pow<B, 0> {
+  static constexpr int v = 1;
+};
+
+template <class F, class T, int L, int M>
+struct Subtree {
+  static constexpr int n = F::n;
+  static constexpr int R = F::R;
+  static constexpr int s0 = M * Pow<n, L>::v;
+  // side of the blocks at depth l below q0
+  static constexpr __host__ __device__ int side(int l) {
+    int s = s0;
+    for (int k = 0; k < l; ++k) s /= n;
+    return s;
+  }
+  static constexpr __host__ __device__ int count(int l) {
+    int c = 1;
+    for (int k = 0; k < l; ++k) c *= R;
+    return c;
+  }
+  static constexpr __host__ __device__ int elems(int l) { return count(l) * side(l) * side(l); }
+  // offsets (elements) of X_l, Y_l (l = 1..L) and P_L in shared memory
+  static constexpr __host__ __device__ int x_off(int l) {
+    int o = 0;
+    for (int k = 1; k < l; ++k) o += 2 * elems(k);
+    return o;
+  }
+  static constexpr __host__ __device__ int y_off(int l) { return x_off(l) + elems(l); }
+  static constexpr __host__ __device__ int p_off() { return x_off(L + 1); }
+  static constexpr __host__ __device__ int total() { return p_off() + elems(L); }
+  static constexpr size_t smem_bytes() { return (size_t)total() * sizeof(T) + 64 * L + 64; }
+};
+
+template <class F, class T, int L, int M>
+__global__ void __launch_bounds__(kThreads) subtree_kernel(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0,
+    T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
+    int64_t ntr, uint8_t* __restrict__ nonfinite) {
+  using S = Subtree<F, T, L, M>;
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  constexpr int s0 = S::s0;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
+  T* sm = reinterpret_cast<T*>(smem_raw + 64 * L + 64);
+  const int k0 = blockIdx.x;
+  using A = Arith<T>;
+
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    __syncthreads();  // previous trial's readers of spl / sm are done
+    if (threadIdx.x < L) spl[threadIdx.x] = plans[t * plan_tstride + q0 + threadIdx.x];
+    __syncthreads();
+    const T* xg = x + t * xy_tstride + (int64_t)k0 * s0 * s0;
+    const T* yg = y + t * xy_tstride + (int64_t)k0 * s0 * s0;
+
+    // ---- expansions: level l -> l + 1, both operands in one sweep
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int sp = S::side(l);
+      const int mb = S::side(l + 1);
+      const int kids = mb * mb;
+      const int items = S::count(l) * kids;
+      const PlanLevel& pl = spl[l];
+      for (int it = threadIdx.x; it < 2 * items; it += kThreads) {
+        const int which = it >= items;
+        const int e = which ? it - items : it;
+        const int Kp = e / kids;
+        const int pos = e - Kp * kids;
+        const int i = pos / mb;
+        const int j = pos - i * mb;
+        const T* par = l == 0 ? (which ? yg : xg) + Kp * sp * sp
+                              : sm + (which ? S::y_off(l) : S::x_off(l)) + Kp * sp * sp;
+        T* dst = sm + (which ? S::y_off(l + 1) : S::x_off(l + 1)) + Kp * R * kids;
+        if (which)
+          expand_at<F, T, 1, 1>(par, sp, dst, kids, pl, i, j);
+        else
+          expand_at<F, T, 1, 0>(par, sp, dst, kids, pl, i, j);
+      }
+      __syncthreads();
+    }
+
+    // ---- leaves: one thread per (leaf, row), k ascending, first term initialises
+    {
+      constexpr int leaves = S::count(L);
+      const T* XL = sm + S::x_off(L);
+      const T* YL = sm + S::y_off(L);
+      T* PL = sm + S::p_off();
+      for (int it = threadIdx.x; it < leaves * M; it += kThreads) {
+        const int leaf = it / M;
+        const int i = it - leaf * M;
+        const T* xr = XL + leaf * M * M + i * M;
+        const T* yb = YL + leaf * M * M;
+        T acc[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) acc[j] = A::mul(xr[0], yb[j]);
+#pragma unroll
+        for (int k = 1; k < M; ++k) {
+          const T xv = xr[k];
+#pragma unroll
+          for (int j = 0; j < M; ++j) acc[j] = A::add(acc[j], A::mul(xv, yb[k * M + j]));
+        }
+        T* pr = PL + leaf * M * M + i * M;
+#pragma unroll
+        for (int j = 0; j < M; ++j) pr[j] = acc[j];
+      }
+      __syncthreads();
+    }
+
+    // ---- contractions: level l + 1 -> l (into the dead X_l, or HBM at l = 0)
+    bool ok = true;
+#pragma unroll
+    for (int l = L - 1; l >= 0; --l) {
+      const int mb = S::side(l + 1);
+      const int sp = S::side(l);
+      const int kids = mb * mb;
+      const int items = S::count(l) * kids;
+      const PlanLevel& pl = spl[l];
+      const T* src = sm + (l == L - 1 ? S::p_off() : S::x_off(l + 1));
+      for (int e = threadIdx.x; e < items; e += kThreads) {
+        const int Kp = e / kids;
+        const int pos = e - Kp * kids;
+        const int i = pos / mb;
+        const int j = pos - i * mb;
+        const T* ks = src + Kp * R * kids;
+        if (l == 0) {
+          T* dst = out + (t * K0 + k0) * (int64_t)s0 * s0;
+          if (nonfinite)
+            ok = contract_at<F, T, 1, true>(ks, kids, mb, dst, pl, i, j) && ok;
+          else
+            contract_at<F, T, 1, false>(ks, kids, mb, dst, pl, i, j);
+        } else {
+          T* dst = sm + S::x_off(l) + Kp * sp * sp;
+          contract_at<F, T, 1, false>(ks, kids, mb, dst, pl, i, j);
+        }
+      }
+      __syncthreads();
+    }
+    if (nonfinite && !ok) nonfinite[t] = 1;
+  }
+}
+
+template <class F, class T, int L, int M>
+cudaError_t launch_subtree_t(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
+                             void* out, const PlanLevel* plans, int64_t pts, int q0, int64_t ntr,
+                             uint8_t* nonfinite, cudaStream_t st) {
+  using S = Subtree<F, T, L, M>;
+  const size_t smem = S::smem_bytes();
+  auto kern = subtree_kernel<F, T, L, M>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)K0, (unsigned)(ntr < 65535 ? ntr : 65535));
+  kern<<<grid, kThreads, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, (T*)out, plans,
+                                     pts, q0, ntr, nonfinite);
+  return cudaGetLastError();
+}
+
+// Table of instantiated (formula, L, M) shapes.
+template <class T>
+cudaError_t dispatch(int formula, int L, int M, const void* x, const void* y, int64_t xs,
+                     int64_t K0, void* out, const PlanLevel* plans, int64_t pts, int q0,
+                     int64_t ntr, uint8_t* nf, cudaStream_t st) {
+#define RBC_SUBTREE(FT, LL, MM)                                                               \
+  if (formula == FT::kId && L == LL && M == MM)                                               \
+    return launch_subtree_t<FT, T, LL, MM>(x, y, xs, K0, out, plans, pts, q0, ntr, nf, st);
+  RBC_SUBTREE(FLaderman, 2, 3)
+  RBC_SUBTREE(FLaderman, 2, 1)
+  RBC_SUBTREE(FLaderman, 1, 3)
+  RBC_SUBTREE(FLaderman, 1, 9)
+  RBC_SUBTREE(FStrassen, 2, 10)
+  RBC_SUBTREE(FStrassen, 2, 5)
+  RBC_SUBTREE(FStrassen, 2, 8)
+  RBC_SUBTREE(FStrassen, 2, 4)
+  RBC_SUBTREE(FStrassen, 2, 2)
+  RBC_SUBTREE(FStrassen, 2, 1)
+  RBC_SUBTREE(FStrassen, 1, 16)
+#undef RBC_SUBTREE
+  return cudaErrorNotSupported;
+}
+
+template <class T>
+size_t smem_of(int formula, int L, int M) {
+#define RBC_SMEM(FT, LL, MM) \
+  if (formula == FT::kId && L == LL && M == MM) return Subtree<FT, T, LL, MM>::smem_bytes();
+  RBC_SMEM(FLaderman, 2, 3)
+  RBC_SMEM(FLaderman, 2, 1)
+  RBC_SMEM(FLaderman, 1, 3)
+  RBC_SMEM(FLaderman, 1, 9)
+  RBC_SMEM(FStrassen, 2, 10)
+  RBC_SMEM(FStrassen, 2, 5)
+  RBC_SMEM(FStrassen, 2, 8)
+  RBC_SMEM(FStrassen, 2, 4)
+  RBC_SMEM(FStrassen, 2, 2)
+  RBC_SMEM(FStrassen, 2, 1)
+  RBC_SMEM(FStrassen, 1, 16)
+#undef RBC_SMEM
+  return 0;
+}
+
+}  // namespace
+
+size_t subtree_smem_bytes(int dtype, int formula, int L, int M) {
+  switch (dtype) {
+    case kF64: return smem_of<double>(formula, L, M);
+    case kF32: return smem_of<float>(formula, L, M);
+    case kF16: return smem_of<__half>(formula, L, M);
+  }
+  return 0;
+}
+
+cudaError_t launch_subtree(int dtype, int formula, int L, int M, const void* x, const void* y,
+                           int64_t xy_tstride, int64_t K0, void* out, const PlanLevel* plans,
+                           int64_t plan_tstride, int q0, int64_t ntr, uint8_t* nonfinite,
+                           cudaStream_t st) {
+  switch (dtype) {
+    case kF64: return dispatch<double>(formula, L, M, x, y, xy_tstride, K0, out, plans, plan_tstride, q0, ntr, nonfinite, st);
+    case kF32: return dispatch<float>(formula, L, M, x, y, xy_tstride, K0, out, plans, plan_tstride, q0, ntr, nonfinite, st);
+    case kF16: return dispatch<__half>(formula, L, M, x, y, xy_tstride, K0, out, plans, plan_tstride, q0, ntr, nonfinite, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace rbc

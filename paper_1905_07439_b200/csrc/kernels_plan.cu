@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kThreads) expand_plan_kernel(
   constexpr int ci = WHICH == 0 ? 1 : 2;  // plan index permuting block cols
   using O = PackOps<T, W>;
   for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
-    const PlanLevel pl = plans[t * plan_tstride + level];
+    const PlanLevel& pl = plans[t * plan_tstride + level];
     const T* xb = x + t * x_tstride + (int64_t)Kp * s * s + (int64_t)i * s + j;
     Pack<T, W> g[n * n];
 #pragma unroll
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kThreads) contract_plan_kernel(
   const int j = pos - i * mb;
   using O = PackOps<T, W>;
   for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
-    const PlanLevel pl = plans[t * plan_tstride + level];
+    const PlanLevel& pl = plans[t * plan_tstride + level];
     const T* cb = ch + (t * K + Kp) * (int64_t)R * mb * mb + pos;
     Pack<T, W> pr[R];
 #pragma unroll

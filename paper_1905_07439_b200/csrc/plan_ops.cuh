@@ -1,0 +1,81 @@
+// Per-position plan-path operations shared by the breadth-first kernels
+// (kernels_plan.cu) and the fused subtree kernel (kernels_fused.cu).
+//
+// expand_at  : W consecutive columns at position (i, j) of one parent block
+//              -> the R children at the same position (reference _expand,
+//              _engine.py:64-90, on hatted tensors, randomize.py:163-178)
+// contract_at: the R children at one position -> the n*n parent blocks
+//              at that position (reference _contract, _engine.py:93-114)
+// Pointers may address global or shared memory.
+#pragma once
+
+#include "formulas_gen.cuh"
+
+namespace rbc {
+
+// WHICH = 0: operand A (rows permuted by plan 1, cols by plan 2, network U)
+// WHICH = 1: operand B (rows by plan 2, cols by plan 3, network V)
+template <class F, class T, int W, int WHICH>
+__device__ __forceinline__ void expand_at(const T* __restrict__ parent, int s,
+                                          T* __restrict__ kids, int kid_stride,
+                                          const PlanLevel& pl, int i, int j) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  constexpr int ri = WHICH == 0 ? 0 : 1;
+  constexpr int ci = WHICH == 0 ? 1 : 2;
+  using O = PackOps<T, W>;
+  const int mb = s / n;
+  const T* base = parent + i * s + j;
+  Pack<T, W> g[n * n];
+#pragma unroll
+  for (int kb = 0; kb < n; ++kb) {
+    const int hk = pl.inv[ri][kb];
+#pragma unroll
+    for (int lb = 0; lb < n; ++lb) {
+      const int hl = pl.inv[ci][lb];
+      const uint32_t m = sign_mask(pl.neg[ri][hk] ^ pl.neg[ci][hl]);
+      g[kb * n + lb] = O::flip(pload<T, W>(base + (hk * mb) * s + hl * mb), m);
+    }
+  }
+  Pack<T, W> o[R];
+  if (WHICH == 0)
+    F::template expand_u<T, W>(g, o, pl.perm[ri][n - 1], pl.perm[ci][n - 1]);
+  else
+    F::template expand_v<T, W>(g, o, pl.perm[ri][n - 1], pl.perm[ci][n - 1]);
+  T* kb0 = kids + i * mb + j;
+#pragma unroll
+  for (int r = 0; r < R; ++r) pstore<T, W>(kb0 + r * kid_stride, o[r]);
+}
+
+// Returns false when any written value is non-finite (only checked if asked).
+template <class F, class T, int W, bool CHECK>
+__device__ __forceinline__ bool contract_at(const T* __restrict__ kids, int kid_stride, int mb,
+                                            T* __restrict__ parent, const PlanLevel& pl, int i,
+                                            int j) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  using O = PackOps<T, W>;
+  const int s = n * mb;
+  const T* kb0 = kids + i * mb + j;
+  Pack<T, W> pr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) pr[r] = pload<T, W>(kb0 + r * kid_stride);
+  Pack<T, W> o[n * n];
+  F::template contract_w<T, W>(pr, o);
+  T* base = parent + i * s + j;
+  bool ok = true;
+#pragma unroll
+  for (int I = 0; I < n; ++I) {
+    const int hi = pl.inv[0][I];
+#pragma unroll
+    for (int J = 0; J < n; ++J) {
+      const int hj = pl.inv[2][J];
+      const Pack<T, W> val = O::flip(o[I * n + J], sign_mask(pl.neg[0][hi] ^ pl.neg[2][hj]));
+      if (CHECK) ok = ok && O::all_finite(val);
+      pstore<T, W>(base + (hi * mb) * s + hj * mb, val);
+    }
+  }
+  return ok;
+}
+
+}  // namespace rbc

@@ -106,6 +106,60 @@ def test_random_plans_vs_oracle(eng, label, fname, Q, N, T):
     assert same_values(got_plan, want)
 
 
+@pytest.mark.parametrize(
+    "label,fname,Q,N,T,T0",
+    [
+        ("f32", "laderman", 4, 243, 2, 2),   # config-2 shape: fused bottom 2 levels, 3x3 leaves
+        ("f32", "strassen", 5, 320, 2, 1),   # golden artifact shape: 10x10 leaves
+        ("f32", "laderman", 2, 9, 3, 3),     # whole recursion fused (q0 = 0), per-trial operands
+        ("f64", "laderman", 2, 27, 2, 1),
+        ("f16", "laderman", 2, 27, 2, 2),
+        ("f16", "strassen", 3, 32, 3, 1),
+    ],
+)
+def test_fused_subtree_vs_breadth_first_and_oracle(eng, monkeypatch, label, fname, Q, N, T, T0):
+    import paper_1905_07439_b200 as rbc
+    from paper_1905_07439_b200.randomize import pack_recursive_plans, plan_formula_id
+
+    mode = mode_for(label)
+    f = {"strassen": rbc.strassen_formula, "laderman": rbc.laderman_formula}[fname]()
+    g = rbc.derive_rng(91, N, Q)
+    a = mode.array(g.standard_normal((T0, N, N)))
+    b = mode.array(g.standard_normal((T0, N, N)))
+    rplans = [rbc.draw_recursive_plan(f.n, Q, rbc.derive_rng(92, t)) for t in range(T)]
+    packed = pack_recursive_plans(rplans, Q, f.n)
+    fid = plan_formula_id(f)
+    fused = eng.apply_plans(fid, Q, packed, a, b, mode)
+    monkeypatch.setenv("RBC_NO_FUSION", "1")
+    plain = eng.apply_plans(fid, Q, packed, a, b, mode)
+    monkeypatch.delenv("RBC_NO_FUSION")
+    levels = [rbc.plan_levels(f, [rp.levels[q] for rp in rplans], mode) for q in range(Q)]
+    want = oracle.apply_levels(levels, a, b, mode)
+    assert same_values(plain, want)
+    assert same_values(fused, want)
+
+
+def test_fused_overflow_flags(eng):
+    """fp16 overflow inside a fused subtree is flagged per trial."""
+    import paper_1905_07439_b200 as rbc
+    from paper_1905_07439_b200.randomize import pack_recursive_plans
+
+    mode = mode_for("f16")
+    f = rbc.laderman_formula()
+    g = rbc.derive_rng(93)
+    a = g.standard_normal((2, 27, 27))
+    b = g.standard_normal((2, 27, 27))
+    a[1] *= 300.0
+    b[1] *= 300.0
+    a, b = mode.array(a), mode.array(b)
+    rplans = [rbc.draw_recursive_plan(3, 2, rbc.derive_rng(94, t)) for t in range(2)]
+    packed = pack_recursive_plans(rplans, 2, 3)
+    out, flags = eng.apply_plans(2, 2, packed, a, b, mode, return_flags=True)
+    assert flags.tolist() == [False, True]
+    with pytest.raises(OverflowError):
+        eng.apply_plans(2, 2, packed, a, b, mode)
+
+
 def test_dense_formula_tree_order(eng):
     """Dense (noisy Laderman) coefficients exercise the row-then-rows fold."""
     import paper_1905_07439_b200 as rbc
