@@ -719,15 +719,32 @@ int rbc_leaf_matmul(int dtype, int64_t batch, int64_t xs, int64_t ys, int64_t M,
   return RBC_OK;
 }
 
+static cudaStream_t make_stream() {
+  cudaStream_t x = nullptr;
+  cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+  return x;
+}
+
 static cudaStream_t host_stream() {
-  static cudaStream_t s = [] {
-    cudaStream_t x = nullptr;
-    cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
-    return x;
-  }();
+  static cudaStream_t s = make_stream();
   return s;
 }
 
+static cudaStream_t copy_stream() {
+  static cudaStream_t s = make_stream();
+  return s;
+}
+
+static cudaEvent_t pipe_event(int i) {
+  static cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (!ev[i]) cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+  return ev[i];
+}
+
+// Host-buffer error trials, pipelined: trials are cut into chunks; chunk k+1
+// is copied host->device on a copy stream (into the other of two input
+// slots) while chunk k is computed on the compute stream.  With pinned host
+// buffers the PCIe transfer hides behind the kernels.
 int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
                      const void* b, const void* rand_plans, int with_det, double* err_rand,
                      double* err_det, uint8_t* nf_rand, uint8_t* nf_det) {
@@ -747,49 +764,76 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   RBC_TRY(check_device());
   if (T == 0 || N == 0) return RBC_OK;
   const size_t es = dtype_size(dtype);
-  const size_t ab = (size_t)T * N * N * es;
-  const size_t pb = rand_plans ? (size_t)T * Q * RBC_PLAN_BYTES : 0;
+  const size_t N2 = (size_t)N * N;
   const size_t db = (size_t)Q * RBC_PLAN_BYTES;
   std::lock_guard<std::mutex> lock(arena().mu);
-  const size_t fixed = 2 * align_up(ab) + align_up(pb) + align_up(db) + 2 * align_up(T * 8) +
-                       2 * align_up(T) + 4096;
-  const size_t one = rbc_error_trials_workspace_bytes(dtype, formula, Q, 1, N);
-  const size_t ws = host_ws_budget(fixed, rbc_error_trials_workspace_bytes(dtype, formula, Q, T, N));
-  if (ws < one) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
-  RBC_TRY(arena().reserve(fixed + ws + 256));
+  // chunk size: ~8 chunks, shrunk until two input slots + workspace fit
+  int64_t C = std::max<int64_t>(1, (T + 7) / 8);
+  auto need = [&](int64_t c) {
+    const size_t slot = 2 * align_up(c * N2 * es) + align_up(c * Q * RBC_PLAN_BYTES);
+    return 2 * slot + align_up(db) + 2 * align_up(T * 8) + 2 * align_up(T) + 4096 +
+           rbc_error_trials_workspace_bytes(dtype, formula, Q, c, N);
+  };
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t budget = (size_t)((double)(free_b + arena().cap) * 0.85);
+  while (C > 1 && need(C) > budget) C = (C + 1) / 2;
+  if (need(C) > budget) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
+  RBC_TRY(arena().reserve(need(C) + 256));
   Arena& A = arena();
-  void* da = A.take(ab);
-  void* dbb = A.take(ab);
-  void* dpl = A.take(pb);
+  void* da[2];
+  void* dbb[2];
+  void* dpl[2];
+  for (int k = 0; k < 2; ++k) {
+    da[k] = A.take(C * N2 * es);
+    dbb[k] = A.take(C * N2 * es);
+    dpl[k] = A.take(C * Q * RBC_PLAN_BYTES);
+  }
   void* ddet = A.take(db);
   double* derr_r = (double*)A.take(T * 8);
   double* derr_d = (double*)A.take(T * 8);
   uint8_t* dnf_r = (uint8_t*)A.take(T);
   uint8_t* dnf_d = (uint8_t*)A.take(T);
+  const size_t ws = rbc_error_trials_workspace_bytes(dtype, formula, Q, C, N);
   void* dws = A.take(ws);
-  cudaStream_t st = host_stream();
+  cudaStream_t sc = host_stream();
+  cudaStream_t sx = copy_stream();
   std::vector<PlanLevel> ident(Q);
   for (int q = 0; q < Q; ++q) {
     memset(&ident[q], 0, sizeof(PlanLevel));
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < n; ++j) ident[q].perm[i][j] = ident[q].inv[i][j] = (int8_t)j;
   }
-  CUDA_TRY(cudaMemcpyAsync(da, a, ab, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(dbb, b, ab, cudaMemcpyHostToDevice, st));
-  if (pb) CUDA_TRY(cudaMemcpyAsync(dpl, rand_plans, pb, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(ddet, ident.data(), db, cudaMemcpyHostToDevice, st));
-  RBC_TRY(rbc_error_trials_async(dtype, formula, Q, T, N, da, dbb, pb ? dpl : nullptr,
-                                 with_det ? ddet : nullptr, derr_r, derr_d, dnf_r, dnf_d, dws, ws,
-                                 st));
-  if (pb) {
-    CUDA_TRY(cudaMemcpyAsync(err_rand, derr_r, T * 8, cudaMemcpyDeviceToHost, st));
-    if (nf_rand) CUDA_TRY(cudaMemcpyAsync(nf_rand, dnf_r, T, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ddet, ident.data(), db, cudaMemcpyHostToDevice, sc));
+  int64_t k = 0;
+  for (int64_t t0 = 0; t0 < T; t0 += C, ++k) {
+    const int64_t nt = std::min(C, T - t0);
+    const int slot = (int)(k & 1);
+    cudaEvent_t copied = pipe_event(slot), computed = pipe_event(2 + slot);
+    if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(sx, computed, 0));  // slot free again
+    CUDA_TRY(cudaMemcpyAsync(da[slot], (const char*)a + t0 * N2 * es, nt * N2 * es,
+                             cudaMemcpyHostToDevice, sx));
+    CUDA_TRY(cudaMemcpyAsync(dbb[slot], (const char*)b + t0 * N2 * es, nt * N2 * es,
+                             cudaMemcpyHostToDevice, sx));
+    if (rand_plans)
+      CUDA_TRY(cudaMemcpyAsync(dpl[slot], (const char*)rand_plans + t0 * Q * RBC_PLAN_BYTES,
+                               nt * Q * RBC_PLAN_BYTES, cudaMemcpyHostToDevice, sx));
+    CUDA_TRY(cudaEventRecord(copied, sx));
+    CUDA_TRY(cudaStreamWaitEvent(sc, copied, 0));
+    RBC_TRY(rbc_error_trials_async(dtype, formula, Q, nt, N, da[slot], dbb[slot],
+                                   rand_plans ? dpl[slot] : nullptr, with_det ? ddet : nullptr,
+                                   derr_r + t0, derr_d + t0, dnf_r + t0, dnf_d + t0, dws, ws, sc));
+    CUDA_TRY(cudaEventRecord(computed, sc));
+  }
+  if (rand_plans) {
+    CUDA_TRY(cudaMemcpyAsync(err_rand, derr_r, T * 8, cudaMemcpyDeviceToHost, sc));
+    if (nf_rand) CUDA_TRY(cudaMemcpyAsync(nf_rand, dnf_r, T, cudaMemcpyDeviceToHost, sc));
   }
   if (with_det) {
-    CUDA_TRY(cudaMemcpyAsync(err_det, derr_d, T * 8, cudaMemcpyDeviceToHost, st));
-    if (nf_det) CUDA_TRY(cudaMemcpyAsync(nf_det, dnf_d, T, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(err_det, derr_d, T * 8, cudaMemcpyDeviceToHost, sc));
+    if (nf_det) CUDA_TRY(cudaMemcpyAsync(nf_det, dnf_d, T, cudaMemcpyDeviceToHost, sc));
   }
-  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaStreamSynchronize(sc));
   return RBC_OK;
 }
 

@@ -58,10 +58,43 @@ struct Subtree {
     return o;
   }
   static constexpr __host__ __device__ int y_off(int l) { return x_off(l) + elems(l); }
-  static constexpr __host__ __device__ int p_off() { return x_off(L + 1); }
-  static constexpr __host__ __device__ int total() { return p_off() + elems(L); }
-  static constexpr size_t smem_bytes() { return (size_t)total() * sizeof(T) + 64 * L + 64; }
+  // leaves of side <= 4 are multiplied by one thread each, in place over X_L
+  static constexpr bool kInPlace = M <= 4;
+  static constexpr __host__ __device__ int p_off() { return kInPlace ? x_off(L) : x_off(L + 1); }
+  static constexpr __host__ __device__ int total() {
+    return kInPlace ? x_off(L + 1) : x_off(L + 1) + elems(L);
+  }
+  // header: L plan records, then 3 gather/scatter tables per level
+  static constexpr size_t kTabBytes = sizeof(GatherTab<n>);
+  static constexpr size_t header() {
+    return ((sizeof(PlanLevel) * L + 15) / 16) * 16 + 3 * L * kTabBytes;
+  }
+  static constexpr size_t smem_bytes() { return (size_t)total() * sizeof(T) + header(); }
 };
+
+// Expansion of one (level, operand) over all positions of the stage, the
+// plan's gather table hoisted out of the position loop.
+template <class F, class T, int WHICH>
+__device__ __forceinline__ void expand_stage(const GatherTab<F::n>& gt_sm, const T* par0, int sp,
+                                             T* dst0, int parents, int lt, int nthreads) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  const int mb = sp / n;
+  const int kids = mb * mb;
+  const GatherTab<n> gt = gt_sm;  // registers
+  const int items = parents * kids;
+  // parent-minor order: neighbouring threads take the same position in
+  // neighbouring parents, whose odd strides (R * kids, sp * sp) spread over
+  // all shared-memory banks
+  for (int e = lt; e < items; e += nthreads) {
+    const int pos = e / parents;
+    const int Kp = e - pos * parents;
+    const int i = pos / mb;
+    const int j = pos - i * mb;
+    expand_tab<F, T, 1, WHICH>(par0 + Kp * sp * sp + i * sp + j, gt,
+                               dst0 + Kp * R * kids + i * mb + j, kids);
+  }
+}
 
 template <class F, class T, int L, int M>
 __global__ void __launch_bounds__(kThreads) subtree_kernel(
@@ -72,70 +105,98 @@ __global__ void __launch_bounds__(kThreads) subtree_kernel(
   constexpr int n = F::n;
   constexpr int R = F::R;
   constexpr int s0 = S::s0;
+  constexpr int kHalf = kThreads / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
-  T* sm = reinterpret_cast<T*>(smem_raw + 64 * L + 64);
+  GatherTab<n>* tabs = reinterpret_cast<GatherTab<n>*>(
+      smem_raw + ((sizeof(PlanLevel) * L + 15) / 16) * 16);
+  T* sm = reinterpret_cast<T*>(smem_raw + S::header());
   const int k0 = blockIdx.x;
   using A = Arith<T>;
+  // operand A on the first half of the warps, B on the second (warp-uniform)
+  const int which = threadIdx.x >= kHalf;
+  const int lt = threadIdx.x - which * kHalf;
 
   for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
     __syncthreads();  // previous trial's readers of spl / sm are done
     if (threadIdx.x < L) spl[threadIdx.x] = plans[t * plan_tstride + q0 + threadIdx.x];
     __syncthreads();
-    const T* xg = x + t * xy_tstride + (int64_t)k0 * s0 * s0;
-    const T* yg = y + t * xy_tstride + (int64_t)k0 * s0 * s0;
+    // one thread per (level, table): X gather, Y gather, contraction scatter
+    if (threadIdx.x < 3 * L) {
+      const int l = threadIdx.x / 3, kind = threadIdx.x - 3 * (threadIdx.x / 3);
+      int sp = s0;
+      for (int k = 0; k < l; ++k) sp /= n;
+      GatherTab<n> tab;
+      if (kind == 0)
+        make_gather<n, 0>(spl[l], sp, tab);
+      else if (kind == 1)
+        make_gather<n, 1>(spl[l], sp, tab);
+      else
+        make_scatter<n>(spl[l], sp / n, tab);
+      tabs[threadIdx.x] = tab;
+    }
+    __syncthreads();
+    const T* src = (which ? y : x) + t * xy_tstride + (int64_t)k0 * s0 * s0;
 
-    // ---- expansions: level l -> l + 1, both operands in one sweep
+    // ---- expansions: level l -> l + 1
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      constexpr int dummy = 0;
-      (void)dummy;
       const int sp = S::side(l);
-      const int mb = S::side(l + 1);
-      const int kids = mb * mb;
-      const int items = S::count(l) * kids;
-      const PlanLevel& pl = spl[l];
-      for (int it = threadIdx.x; it < 2 * items; it += kThreads) {
-        const int which = it >= items;
-        const int e = which ? it - items : it;
-        const int Kp = e / kids;
-        const int pos = e - Kp * kids;
-        const int i = pos / mb;
-        const int j = pos - i * mb;
-        const T* par = l == 0 ? (which ? yg : xg) + Kp * sp * sp
-                              : sm + (which ? S::y_off(l) : S::x_off(l)) + Kp * sp * sp;
-        T* dst = sm + (which ? S::y_off(l + 1) : S::x_off(l + 1)) + Kp * R * kids;
-        if (which)
-          expand_at<F, T, 1, 1>(par, sp, dst, kids, pl, i, j);
-        else
-          expand_at<F, T, 1, 0>(par, sp, dst, kids, pl, i, j);
-      }
+      const T* par0 = l == 0 ? src : sm + (which ? S::y_off(l) : S::x_off(l));
+      T* dst0 = sm + (which ? S::y_off(l + 1) : S::x_off(l + 1));
+      if (which)
+        expand_stage<F, T, 1>(tabs[3 * l + 1], par0, sp, dst0, S::count(l), lt, kHalf);
+      else
+        expand_stage<F, T, 0>(tabs[3 * l + 0], par0, sp, dst0, S::count(l), lt, kHalf);
       __syncthreads();
     }
 
-    // ---- leaves: one thread per (leaf, row), k ascending, first term initialises
+    // ---- leaves: k ascending, first term initialises
     {
       constexpr int leaves = S::count(L);
       const T* XL = sm + S::x_off(L);
       const T* YL = sm + S::y_off(L);
       T* PL = sm + S::p_off();
-      for (int it = threadIdx.x; it < leaves * M; it += kThreads) {
-        const int leaf = it / M;
-        const int i = it - leaf * M;
-        const T* xr = XL + leaf * M * M + i * M;
-        const T* yb = YL + leaf * M * M;
-        T acc[M];
+      if (S::kInPlace) {
+        // one thread per leaf product, operands in registers, result written
+        // over the thread's own X leaf (PL == XL)
+        for (int leaf = threadIdx.x; leaf < leaves; leaf += kThreads) {
+          T xa[M * M], yb[M * M];
 #pragma unroll
-        for (int j = 0; j < M; ++j) acc[j] = A::mul(xr[0], yb[j]);
+          for (int q = 0; q < M * M; ++q) {
+            xa[q] = XL[leaf * M * M + q];
+            yb[q] = YL[leaf * M * M + q];
+          }
 #pragma unroll
-        for (int k = 1; k < M; ++k) {
-          const T xv = xr[k];
+          for (int i = 0; i < M; ++i)
 #pragma unroll
-          for (int j = 0; j < M; ++j) acc[j] = A::add(acc[j], A::mul(xv, yb[k * M + j]));
+            for (int j = 0; j < M; ++j) {
+              T acc = A::mul(xa[i * M], yb[j]);
+#pragma unroll
+              for (int k = 1; k < M; ++k) acc = A::add(acc, A::mul(xa[i * M + k], yb[k * M + j]));
+              PL[leaf * M * M + i * M + j] = acc;
+            }
         }
-        T* pr = PL + leaf * M * M + i * M;
+      } else {
+        // one thread per (leaf, row)
+        for (int it = threadIdx.x; it < leaves * M; it += kThreads) {
+          const int leaf = it / M;
+          const int i = it - leaf * M;
+          const T* xr = XL + leaf * M * M + i * M;
+          const T* yl = YL + leaf * M * M;
+          T acc[M];
 #pragma unroll
-        for (int j = 0; j < M; ++j) pr[j] = acc[j];
+          for (int j = 0; j < M; ++j) acc[j] = A::mul(xr[0], yl[j]);
+#pragma unroll
+          for (int k = 1; k < M; ++k) {
+            const T xv = xr[k];
+#pragma unroll
+            for (int j = 0; j < M; ++j) acc[j] = A::add(acc[j], A::mul(xv, yl[k * M + j]));
+          }
+          T* pr = PL + leaf * M * M + i * M;
+#pragma unroll
+          for (int j = 0; j < M; ++j) pr[j] = acc[j];
+        }
       }
       __syncthreads();
     }
@@ -148,24 +209,21 @@ __global__ void __launch_bounds__(kThreads) subtree_kernel(
       const int sp = S::side(l);
       const int kids = mb * mb;
       const int items = S::count(l) * kids;
-      const PlanLevel& pl = spl[l];
-      const T* src = sm + (l == L - 1 ? S::p_off() : S::x_off(l + 1));
+      const GatherTab<n> st = tabs[3 * l + 2];
+      const T* ksrc = sm + (l == L - 1 ? S::p_off() : S::x_off(l + 1));
+      T* dbase = l == 0 ? out + (t * K0 + k0) * (int64_t)s0 * s0 : sm + S::x_off(l);
+      const int parents = S::count(l);
       for (int e = threadIdx.x; e < items; e += kThreads) {
-        const int Kp = e / kids;
-        const int pos = e - Kp * kids;
+        const int pos = e / parents;
+        const int Kp = e - pos * parents;
         const int i = pos / mb;
         const int j = pos - i * mb;
-        const T* ks = src + Kp * R * kids;
-        if (l == 0) {
-          T* dst = out + (t * K0 + k0) * (int64_t)s0 * s0;
-          if (nonfinite)
-            ok = contract_at<F, T, 1, true>(ks, kids, mb, dst, pl, i, j) && ok;
-          else
-            contract_at<F, T, 1, false>(ks, kids, mb, dst, pl, i, j);
-        } else {
-          T* dst = sm + S::x_off(l) + Kp * sp * sp;
-          contract_at<F, T, 1, false>(ks, kids, mb, dst, pl, i, j);
-        }
+        const T* ks = ksrc + Kp * R * kids + i * mb + j;
+        T* dst = dbase + Kp * sp * sp + i * sp + j;
+        if (l == 0 && nonfinite)
+          ok = contract_tab<F, T, 1, true>(ks, kids, dst, st) && ok;
+        else
+          contract_tab<F, T, 1, false>(ks, kids, dst, st);
       }
       __syncthreads();
     }

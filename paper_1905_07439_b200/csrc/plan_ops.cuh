@@ -78,4 +78,88 @@ __device__ __forceinline__ bool contract_at(const T* __restrict__ kids, int kid_
   return ok;
 }
 
+// ---- precomputed variants: the plan-dependent gather/scatter offsets of one
+// (level, operand) are computed once per thread and reused for every position.
+template <int n>
+struct alignas(16) GatherTab {
+  int off[n * n];        // element offset of base block (kb, lb) in the parent
+  uint32_t msk[n * n];   // sign flip of that block
+  int lastrow, lastcol;  // base index added last in 3-term folds
+};
+
+template <int n, int WHICH>
+__device__ __forceinline__ void make_gather(const PlanLevel& pl, int s, GatherTab<n>& gt) {
+  constexpr int ri = WHICH == 0 ? 0 : 1;
+  constexpr int ci = WHICH == 0 ? 1 : 2;
+  const int mb = s / n;
+#pragma unroll
+  for (int kb = 0; kb < n; ++kb) {
+    const int hk = pl.inv[ri][kb];
+#pragma unroll
+    for (int lb = 0; lb < n; ++lb) {
+      const int hl = pl.inv[ci][lb];
+      gt.off[kb * n + lb] = hk * mb * s + hl * mb;
+      gt.msk[kb * n + lb] = sign_mask(pl.neg[ri][hk] ^ pl.neg[ci][hl]);
+    }
+  }
+  gt.lastrow = pl.perm[ri][n - 1];
+  gt.lastcol = pl.perm[ci][n - 1];
+}
+
+// Scatter table of a contraction: base block (I, J) -> hatted position.
+template <int n>
+__device__ __forceinline__ void make_scatter(const PlanLevel& pl, int mb, GatherTab<n>& gt) {
+  const int s = n * mb;
+#pragma unroll
+  for (int I = 0; I < n; ++I) {
+    const int hi = pl.inv[0][I];
+#pragma unroll
+    for (int J = 0; J < n; ++J) {
+      const int hj = pl.inv[2][J];
+      gt.off[I * n + J] = hi * mb * s + hj * mb;
+      gt.msk[I * n + J] = sign_mask(pl.neg[0][hi] ^ pl.neg[2][hj]);
+    }
+  }
+  gt.lastrow = gt.lastcol = 0;
+}
+
+template <class F, class T, int W, int WHICH>
+__device__ __forceinline__ void expand_tab(const T* __restrict__ base, const GatherTab<F::n>& gt,
+                                           T* __restrict__ kid0, int kid_stride) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  using O = PackOps<T, W>;
+  Pack<T, W> g[n * n];
+#pragma unroll
+  for (int k = 0; k < n * n; ++k) g[k] = O::flip(pload<T, W>(base + gt.off[k]), gt.msk[k]);
+  Pack<T, W> o[R];
+  if (WHICH == 0)
+    F::template expand_u<T, W>(g, o, gt.lastrow, gt.lastcol);
+  else
+    F::template expand_v<T, W>(g, o, gt.lastrow, gt.lastcol);
+#pragma unroll
+  for (int r = 0; r < R; ++r) pstore<T, W>(kid0 + r * kid_stride, o[r]);
+}
+
+template <class F, class T, int W, bool CHECK>
+__device__ __forceinline__ bool contract_tab(const T* __restrict__ kid0, int kid_stride,
+                                             T* __restrict__ base, const GatherTab<F::n>& st) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  using O = PackOps<T, W>;
+  Pack<T, W> pr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) pr[r] = pload<T, W>(kid0 + r * kid_stride);
+  Pack<T, W> o[n * n];
+  F::template contract_w<T, W>(pr, o);
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < n * n; ++k) {
+    const Pack<T, W> val = O::flip(o[k], st.msk[k]);
+    if (CHECK) ok = ok && O::all_finite(val);
+    pstore<T, W>(base + st.off[k], val);
+  }
+  return ok;
+}
+
 }  // namespace rbc
