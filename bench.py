@@ -283,11 +283,13 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     _lib.require_device()
 
+    from paper_1905_07439_b200 import distributed
+
     cfg = get_config(args.config)
     T = args.trials or cfg.trials
     f = cfg.formula_obj()
-    first = rank * T + 1
-    pair_ids = list(range(first, first + T))
+    first, _ = distributed.shard(rank, world, T)
+    pair_ids = distributed.pair_ids(rank, world, T)
     workers = min(32, max(1, (os.cpu_count() or 2) // max(1, world)))
     A, B = make_pairs(cfg, first, T, workers=workers)
     packed = pack_recursive_plans([cfg.plan(cfg.plan_key(p)) for p in pair_ids], cfg.Q, cfg.n)
@@ -350,17 +352,12 @@ def run_ours(args):
         e2e_ms = (time.perf_counter() - t0) / args.steps * 1e3
 
     # ---- max over ranks + gather of per-trial statistics
-    if dist is not None:
-        t = torch.tensor([dev_ms, e2e_ms or 0.0], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms, e2e_ms = float(t[0]), (float(t[1]) if e2e_ms is not None else None)
-        stats = torch.from_numpy(np.stack([err_r, err_d])).to(dev)
-        gathered = [torch.empty_like(stats) for _ in range(world)]
-        dist.all_gather(gathered, stats)
-        allerr = torch.cat(gathered, dim=1).cpu().numpy()
-        err_r_all, err_d_all = allerr[0], allerr[1]
-    else:
-        err_r_all, err_d_all = err_r, err_d
+    tmax = distributed.max_over_ranks([dev_ms, e2e_ms or 0.0], device=dev)
+    dev_ms, e2e_ms = float(tmax[0]), (float(tmax[1]) if e2e_ms is not None else None)
+    allerr = distributed.gather_trials(
+        np.stack([err_r, err_d, nf_r.astype(np.float64), nf_d.astype(np.float64)]), device=dev)
+    err_r_all, err_d_all = allerr[0], allerr[1]
+    nf_r_all, nf_d_all = allerr[2] > 0, allerr[3] > 0
 
     flops_step = 2 * cfg.effective_flops() * T * world
     value = flops_step / (dev_ms / 1e3) / 1e9
@@ -381,11 +378,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
         "roofline": roofline(prof, cfg.name),
-        "errors": {
-            "rand_mean": float(np.nanmean(err_r_all)), "rand_std": float(np.nanstd(err_r_all)),
-            "det_mean": float(np.nanmean(err_d_all)), "det_std": float(np.nanstd(err_d_all)),
-            "rand_nonfinite": int(nf_r.sum()), "det_nonfinite": int(nf_d.sum()),
-        },
+        "errors": distributed.trial_stats(err_r_all, err_d_all, nf_r_all, nf_d_all),
     }
     if e2e_ms is not None:
         line["e2e"] = {"value": round(flops_step / (e2e_ms / 1e3) / 1e9, 3), "unit": "GFLOP/s",

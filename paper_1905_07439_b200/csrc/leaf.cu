@@ -21,6 +21,9 @@
 // Both also serve the binary64 ground truth of binary32/binary16 operands
 // (TIn narrower than TAcc: operands are widened exactly on load).
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace rbc {
@@ -183,6 +186,143 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     }
 }
 
+// binary16 leaves: the same tiling with half2 SIMD along N.  Each HMUL2 /
+// HADD2 lane rounds exactly like the scalar __hmul_rn / __hadd_rn, so every
+// output keeps its own sequential k chain (two adjacent outputs per op).
+template <int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    leaf_tiled_h2_kernel(int M, int K, int N, const __half* __restrict__ x, int64_t xs,
+                         const __half* __restrict__ y, int64_t ys, __half* __restrict__ out,
+                         int tiles_n) {
+  constexpr int DY = BM / TM;
+  constexpr int DX = BN / TN;
+  constexpr int NT = DY * DX;
+  constexpr int A_PER = BM * BK / NT;
+  constexpr int B_PER = BK * BN / NT;
+  constexpr int TN2 = TN / 2;
+  static_assert(TN % 2 == 0 && BM * BK % NT == 0 && BK * BN % NT == 0, "tile/threads");
+  __shared__ __align__(16) __half As[2][BK][BM];
+  __shared__ __align__(16) __half Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid % DX;
+  const int ty = tid / DX;
+  const int64_t b = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  const int tm = blockIdx.x / tiles_n;
+  const int tn = blockIdx.x - tm * tiles_n;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const __half* xb = x + b * xs;
+  const __half* yb = y + b * ys;
+  const __half zero = __float2half(0.f);
+  __half ra[A_PER], rb[B_PER];
+  auto load_tile = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < A_PER; ++q) {
+      const int e = tid + q * NT;
+      const int mm = e / BK, kk = e % BK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      ra[q] = (gm < M && gk < K) ? xb[(int64_t)gm * K + gk] : zero;
+    }
+#pragma unroll
+    for (int q = 0; q < B_PER; ++q) {
+      const int e = tid + q * NT;
+      const int kk = e / BN, nn = e % BN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      rb[q] = (gk < K && gn < N) ? yb[(int64_t)gk * N + gn] : zero;
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < A_PER; ++q) {
+      const int e = tid + q * NT;
+      As[buf][e % BK][e / BK] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < B_PER; ++q) {
+      const int e = tid + q * NT;
+      Bs[buf][e / BN][e % BN] = rb[q];
+    }
+  };
+  // thread owns rows ty*TM .. +TM and column pairs tx*TN .. +TN
+  __half2 acc[TM][TN2];
+  const int ktiles = (K + BK - 1) / BK;
+  load_tile(0);
+  store_tile(0);
+  __syncthreads();
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
+    const int kmax = min(BK, K - kt * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      if (kk < kmax) {
+        __half2 a2[TM], b2[TN2];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a2[i] = __half2half2(As[buf][kk][ty * TM + i]);
+#pragma unroll
+        for (int j = 0; j < TN2; ++j)
+          b2[j] = *reinterpret_cast<const __half2*>(&Bs[buf][kk][tx * TN + 2 * j]);
+        if (kt == 0 && kk == 0) {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN2; ++j) acc[i][j] = __hmul2_rn(a2[i], b2[j]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN2; ++j) acc[i][j] = __hadd2_rn(acc[i][j], __hmul2_rn(a2[i], b2[j]));
+        }
+      }
+    }
+    if (kt + 1 < ktiles) {
+      store_tile(buf ^ 1);
+      __syncthreads();
+    }
+  }
+  __half* ob = out + b * (int64_t)M * N;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int gm = m0 + ty * TM + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN2; ++j) {
+      const int gn = n0 + tx * TN + 2 * j;
+      if (gn + 1 < N) {
+        *reinterpret_cast<__half2*>(&ob[(int64_t)gm * N + gn]) = acc[i][j];
+      } else if (gn < N) {
+        ob[(int64_t)gm * N + gn] = __low2half(acc[i][j]);
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int BK, int TM, int TN>
+cudaError_t run_tiled_h2(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
+                         const void* y, int64_t ys, void* out, cudaStream_t st) {
+  const int tiles_m = (int)((M + BM - 1) / BM);
+  const int tiles_n = (int)((N + BN - 1) / BN);
+  constexpr int NT = (BM / TM) * (BN / TN);
+  for (int64_t b0 = 0; b0 < batch;) {
+    const int64_t nb = std::min<int64_t>(batch - b0, (int64_t)65535 * 65535);
+    const int64_t full = (nb / 65535) * 65535;
+    if (full > 0) {
+      dim3 grid(tiles_m * tiles_n, 65535, (unsigned)(full / 65535));
+      leaf_tiled_h2_kernel<BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(
+          (int)M, (int)K, (int)N, (const __half*)x + b0 * xs, xs, (const __half*)y + b0 * ys, ys,
+          (__half*)out + b0 * M * N, tiles_n);
+    }
+    if (nb > full) {
+      dim3 grid(tiles_m * tiles_n, (unsigned)(nb - full), 1);
+      const int64_t bb = b0 + full;
+      leaf_tiled_h2_kernel<BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(
+          (int)M, (int)K, (int)N, (const __half*)x + bb * xs, xs, (const __half*)y + bb * ys, ys,
+          (__half*)out + bb * M * N, tiles_n);
+    }
+    b0 += nb;
+  }
+  return cudaGetLastError();
+}
+
 template <class TIn, class TAcc, int BM, int BN, int BK, int TM, int TN>
 cudaError_t run_tiled(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
                       const void* y, int64_t ys, void* out, cudaStream_t st) {
@@ -226,9 +366,23 @@ cudaError_t run_small(int64_t batch, int64_t M, int64_t K, int64_t N, const void
   return cudaGetLastError();
 }
 
+// RBC_LEAF_TILE=<128|64|32|1> overrides the tile choice (tuning aid).
+inline int tile_override() {
+  const char* v = getenv("RBC_LEAF_TILE");
+  return v ? atoi(v) : 0;
+}
+
 template <class TIn, class TAcc>
 cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x,
                           int64_t xs, const void* y, int64_t ys, void* out, cudaStream_t st) {
+  const int forced = tile_override();
+  if (forced == 128 && M >= 128 && N >= 128)
+    return run_tiled<TIn, TAcc, 128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (forced == 64 && M >= 64 && N >= 64)
+    return run_tiled<TIn, TAcc, 64, 64, 8, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (forced == 32 && M >= 32 && N >= 32)
+    return run_tiled<TIn, TAcc, 32, 32, 8, 2, 2>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (forced == 1) return run_small<TIn, TAcc>(batch, M, K, N, x, xs, y, ys, out, st);
   if (M >= 128 && N >= 128 && sizeof(TAcc) <= 4)
     return run_tiled<TIn, TAcc, 128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
   if (M >= 64 && N >= 64)
@@ -251,8 +405,15 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
   }
   if (dtype_out == kF32 && dtype_in == kF32)
     return leaf_dispatch<float, float>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (dtype_out == kF16 && dtype_in == kF16)
+  if (dtype_out == kF16 && dtype_in == kF16) {
+    if (M >= 128 && N >= 128)
+      return run_tiled_h2<128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (M >= 64 && N >= 64)
+      return run_tiled_h2<64, 64, 8, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (M >= 32 && N >= 32)
+      return run_tiled_h2<32, 32, 8, 2, 2>(batch, M, K, N, x, xs, y, ys, out, st);
     return run_small<__half, __half>(batch, M, K, N, x, xs, y, ys, out, st);
+  }
   return cudaErrorInvalidValue;
 }
 

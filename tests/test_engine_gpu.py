@@ -85,7 +85,10 @@ def test_golden_leaf_cases(eng, engine_cases):
         ("f32", "laderman", 3, 81, 3),
         ("f64", "laderman", 2, 81, 2),
         ("f16", "strassen", 3, 128, 2),
+        ("f16", "strassen", 1, 256, 2),   # 128x128 half2 tiled leaves
+        ("f16", "strassen", 2, 280, 1),   # 70x70 leaves, half2 64-tile with edges
         ("f64", "strassen", 2, 200, 2),
+        ("f64", "strassen", 1, 260, 1),   # 130x130 binary64 leaves
     ],
 )
 def test_random_plans_vs_oracle(eng, label, fname, Q, N, T):
