@@ -3,30 +3,39 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
 
-A *step* is one pass of the hot path over one batch of synthetic input: for
-each of the rank's T operand pairs (config's seed layout) the
-binary64 truth, the deterministic BC product and its error, and the
-randomized BC product (fresh per-level signed permutations) and its error.
-Default workload: BASELINE.json configs[1] ("c2": Laderman <3,3,3;23>,
-Q=4, n=243, f32, Uniform[-1,1], 1000 pairs per rank).
+A *step* is one pass of the hot path over one batch of synthetic input (the
+config's seed layout), on every rank:
 
-value  : effective GFLOP/s = 2 n^3 x (2 BC products per pair) x T x ranks
-         / step time, inputs resident in HBM, CUDA events on the launch
-         stream, max over ranks
-e2e    : the same through the public host-buffer C-ABI call
-         (rbc_error_trials): pinned host operands + plans copied H2D and
+* error-trial configs (c1, c2, c4, c5): for each of the rank's T operand
+  pairs, the binary64 truth, the deterministic BC product and its error, and
+  the randomized BC product (fresh per-level signed permutations) and its
+  error -- 2 BC products per pair;
+* averaging config (c3): for each of the rank's P pairs, the truth, the
+  deterministic product, G = 32 randomized products, their errors and the
+  running-mean errors (reference experiments.py:264-296) -- G + 1 products
+  per pair.
+
+Default workload: BASELINE.json configs[1] ("c2": Laderman <3,3,3;23>, Q=4,
+n=243, f32, Uniform[-1,1], 1000 pairs per rank).
+
+value  : effective GFLOP/s = 2 n^3 x (BC products per step, all ranks) /
+         step time; inputs resident in HBM; CUDA events on the launch stream;
+         max over ranks
+e2e    : the same through the public host-buffer API (error_trials /
+         average_trials): pinned host operands + plans copied H2D and the
          per-trial errors copied D2H inside the timed region
 roofline: the stage with the largest share of the timed region, from the
          engine's CUDA-event stage profiler (algorithmic bytes or flops per
-         launch / average launch duration) against MEASURED_PEAKS.json
+         launch / average launch duration) against MEASURED_PEAKS.json (HBM)
+         or profiles/fp_peaks.json (exact-order CUDA-core rates)
 cpu_baseline: the CPU oracle (numpy restatement of the reference engine,
-         oracle/) on a bounded sample of the same pairs, rank 0, 1 core
---impl reference: the CPU oracle arm with all host cores (the reference is
-         pure Python/numpy and cannot be compiled into oracle/_ref)
+         oracle/) on a bounded sample of the same workload, rank 0, 1 core
+--impl reference: the CPU oracle arm on all host cores (the reference is pure
+         Python/numpy and cannot be compiled into oracle/_ref)
 
-Multi-GPU: one process per GPU (torchrun), each rank takes its own block of
-pairs (weak scaling); the only collective is the MAX of the step times and
-an all-gather of the per-trial error statistics (tiny, NCCL).
+Multi-GPU: one process per GPU (torchrun), each rank owns its own block of
+pairs (weak scaling); the only collectives are the MAX of the step times and
+an all-gather of per-trial error statistics (a few KB, NCCL).
 """
 
 from __future__ import annotations
@@ -47,6 +56,18 @@ if str(ROOT) not in sys.path:
 
 HBM_FALLBACK_GBS = 6650.0
 FP32_NOMINAL_TFLOPS = 148 * 128 * 1.965e9 / 1e12  # FMUL+FADD per MAC: 1 flop/lane/clk
+METRIC = "effective GFLOP/s (2n^3/time) of randomized BC matmul error trials"
+
+# per config: pairs per rank per step (GPU), CPU sample (pairs, products per
+# pair, subtree depth) -- depth d evaluates branch 0 of the top d levels only,
+# i.e. 1/R^d of every product (used where one full CPU product takes minutes)
+DEFAULTS = {
+    "c1": dict(pairs=100, cpu=(100, 2, 0)),
+    "c2": dict(pairs=1000, cpu=(20, 2, 0)),
+    "c3": dict(pairs=4, cpu=(1, 3, 0)),
+    "c4": dict(pairs=16, cpu=(1, 1, 1)),
+    "c5": dict(pairs=2, cpu=(1, 1, 2)),
+}
 
 
 def parse():
@@ -55,9 +76,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--trials", type=int, default=0, help="pairs per rank (default: config)")
+    ap.add_argument("--trials", type=int, default=0, help="pairs per rank per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=0, help="pairs in the CPU baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -121,16 +141,16 @@ def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return d.get("hbm_gbs", HBM_FALLBACK_GBS), "measured"
-    return HBM_FALLBACK_GBS, "fallback"
+        return d.get("hbm_gbs", HBM_FALLBACK_GBS), "measured (MEASURED_PEAKS.json)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
 def fp_peaks():
-    """Exact-order (FMUL+FADD) CUDA-core peaks measured by tools/fp_peak.py."""
+    """Exact-order (FMUL+FADD, DMUL+DADD, HMUL2+HADD2) CUDA-core rates
+    measured by tools/fp_peak.cu (profiles/fp_peaks.json)."""
     p = ROOT / "profiles" / "fp_peaks.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return d, "measured (profiles/fp_peaks.json)"
+        return json.loads(p.read_text()), "measured (profiles/fp_peaks.json)"
     return {"f32_tflops": FP32_NOMINAL_TFLOPS, "f64_tflops": FP32_NOMINAL_TFLOPS / 2,
             "f16_tflops": FP32_NOMINAL_TFLOPS * 2}, "nominal"
 
@@ -156,7 +176,7 @@ def roofline(prof: dict, config: str):
         key = {"leaf_f32": "f32_tflops", "leaf_f16": "f16_tflops"}.get(stage, "f64_tflops")
         achieved = per_launch_flops / avg_s / 1e12
         peak = peaks[key]
-        bound, unit = ("cuda-core-" + key.split("_")[0]), "TFLOP/s"
+        bound, unit = ("cuda-core-" + key.split("_")[0] + "-exact-order"), "TFLOP/s"
     else:
         peak, how = measured_peaks()
         achieved = per_launch_bytes / avg_s / 1e9
@@ -173,10 +193,21 @@ def roofline(prof: dict, config: str):
 
 
 # ------------------------------------------------------------ CPU oracle ----
-def _cpu_pair_work(args):
-    """One pair through the CPU oracle: truth, deterministic and randomized
-    products, both errors (the same step definition as the GPU arm)."""
-    cfg_name, p = args
+def _descend(x, coeff_level, depth_levels):
+    """Branch 0 of the top levels: combine, keep child 0 only."""
+    from oracle import engine as oracle
+
+    for c in depth_levels:
+        x = oracle.combine(x, c[:, :1])[:, :1]
+    return x
+
+
+def _cpu_job(job):
+    """One CPU work unit through the oracle: pair p, products js (0 = the
+    deterministic product, j >= 1 = randomized plan j), evaluated on branch 0
+    of the top `depth` levels (depth 0 = the whole product).  Returns
+    (effective flops, errors) -- errors only for depth 0."""
+    cfg_name, p, js, depth = job
     import numpy as np
 
     from oracle import engine as oracle
@@ -187,38 +218,59 @@ def _cpu_pair_work(args):
     cfg = get_config(cfg_name)
     f = cfg.formula_obj()
     A, B = cfg.pair(p)
-    ref = oracle.standard_multiply(A.astype(np.float64), B.astype(np.float64))
-    det_levels = [mode_tensors(f, cfg.mode)] * cfg.Q
-    rp = cfg.plan(cfg.plan_key(p))
-    rand_levels = [plan_levels(f, [rp.levels[q]], cfg.mode) for q in range(cfg.Q)]
-    out = []
+    ref = oracle.standard_multiply(A.astype(np.float64), B.astype(np.float64)) if depth == 0 else None
+    errs = []
     with np.errstate(all="ignore"):
-        for levels in (det_levels, rand_levels):
+        for j in js:
+            if j == 0:
+                levels = [mode_tensors(f, cfg.mode)] * cfg.Q
+            else:
+                rp = cfg.plan(cfg.plan_key(p, j) if cfg.plans_per_pair > 1 else cfg.plan_key(p))
+                levels = [plan_levels(f, [rp.levels[q]], cfg.mode) for q in range(cfg.Q)]
+            x = A[None, None]
+            y = B[None, None]
+            for q in range(depth):
+                u, v, _ = levels[q]
+                x = oracle.combine(x, u)[:, :1]
+                y = oracle.combine(y, v)[:, :1]
             try:
-                C = oracle.apply_levels(levels, A[None], B[None], cfg.mode)
-                out.append(float(oracle.rel_errors(C, ref)[0]))
+                C = oracle.apply_levels(levels[depth:], x[:, 0], y[:, 0], cfg.mode)
+                errs.append(float(oracle.rel_errors(C, ref)[0]) if ref is not None else None)
             except OverflowError:
-                out.append(float("nan"))
-    return out
+                errs.append(float("nan"))
+    flops = 2.0 * cfg.N ** 3 * len(js) / float(cfg.rank) ** depth
+    return flops, errs
 
 
-def cpu_oracle_rate(cfg, pairs, workers: int):
+def run_cpu_jobs(jobs, workers: int):
     import concurrent.futures as cf
 
-    jobs = [(cfg.name, p) for p in pairs]
     t0 = time.perf_counter()
     if workers > 1:
         with cf.ProcessPoolExecutor(max_workers=workers) as ex:
-            res = list(ex.map(_cpu_pair_work, jobs))
+            res = list(ex.map(_cpu_job, jobs))
     else:
-        res = [_cpu_pair_work(j) for j in jobs]
-    dt = time.perf_counter() - t0
-    return dt, res
+        res = [_cpu_job(j) for j in jobs]
+    return time.perf_counter() - t0, res
 
 
-def default_cpu_sample(cfg) -> int:
-    # about 10-30 s of single-core oracle work
-    return {"c1": 40, "c2": 8, "c3": 1, "c4": 1, "c5": 1}.get(cfg.name, 2)
+def cpu_sample_jobs(cfg, first_pair: int, count: int, per_pair: int, depth: int):
+    if cfg.plans_per_pair > 1:
+        js = list(range(per_pair))  # det + plans 1..per_pair-1
+    else:
+        js = [0, 1][:per_pair] if per_pair <= 2 else [0, 1]
+        if per_pair == 1:
+            js = [1]
+    return [(cfg.name, p, js, depth) for p in range(first_pair, first_pair + count)]
+
+
+def describe_sample(cfg, count, per_pair, depth, seconds, cores):
+    what = f"{count} pair(s) x {per_pair} product(s)"
+    if depth:
+        what += (f", each product evaluated on branch 0 of its top {depth} level(s) "
+                 f"(1/{cfg.rank}^{depth} of the work, credited as 2n^3/{cfg.rank}^{depth})")
+    return (f"{what} through oracle/engine.py (numpy restatement of randbc._engine), "
+            f"{cores} process(es), {seconds:.1f} s")
 
 
 # ------------------------------------------------------------ reference ----
@@ -230,31 +282,30 @@ def run_reference(args):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    per_step = max(cores, 1)
-    flops_per_pair = 2 * cfg.effective_flops()
+    _, per_pair, depth = DEFAULTS[cfg.name]["cpu"]
     p = 1
     for _ in range(args.warmup):
-        cpu_oracle_rate(cfg, range(p, p + per_step), cores)
-        p += per_step
-    total = 0.0
+        run_cpu_jobs(cpu_sample_jobs(cfg, p, cores, per_pair, depth), cores)
+        p += cores
+    total_s, total_flops = 0.0, 0.0
     for _ in range(args.steps):
-        dt, _ = cpu_oracle_rate(cfg, range(p, p + per_step), cores)
-        total += dt
-        p += per_step
-    ms = total / args.steps * 1e3
-    value = flops_per_pair * per_step / (ms / 1e3) / 1e9
+        dt, res = run_cpu_jobs(cpu_sample_jobs(cfg, p, cores, per_pair, depth), cores)
+        total_s += dt
+        total_flops += sum(r[0] for r in res)
+        p += cores
+    ms = total_s / args.steps * 1e3
+    value = total_flops / total_s / 1e9
     line = {
-        "metric": "effective GFLOP/s (2n^3/time) of randomized BC matmul error trials",
-        "impl": "reference", "value": round(value, 4), "unit": "GFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "metric": METRIC, "impl": "reference", "value": round(value, 5), "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.mode.label,
         "data": "synthetic (seeded, reference seed layout)",
-        "trials_per_s": round(per_step / (ms / 1e3), 4),
-        "config": {"workload": cfg.name, "desc": cfg.note, "pairs_per_step": per_step},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"{per_step} pairs per step through oracle/engine.py "
-                                   f"(numpy restatement of randbc._engine), one process per core"},
-        "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+        "config": {"workload": cfg.name, "desc": cfg.note, "jobs_per_step": cores},
+        "cpu_baseline": {
+            "value": round(value, 5), "unit": "GFLOP/s", "cores": cores, "kind": "port",
+            "sample": describe_sample(cfg, cores, per_pair, depth, ms / 1e3, cores) + " per step",
+        },
+        "e2e": {"value": round(value, 5), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -262,14 +313,117 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ ours ----
+class ErrorTrialWorkload:
+    """c1, c2, c4, c5: 2 products per pair (plan path, packed plans)."""
+
+    def __init__(self, cfg, pair_ids, A, B, dev, torch):
+        from paper_1905_07439_b200.randomize import pack_recursive_plans
+        from paper_1905_07439_b200.trials import DeviceErrorTrials
+
+        self.cfg, self.torch = cfg, torch
+        self.f = cfg.formula_obj()
+        self.A, self.B = A, B
+        self.packed = pack_recursive_plans([cfg.plan(cfg.plan_key(p)) for p in pair_ids], cfg.Q, cfg.n)
+        self.a = torch.from_numpy(A).to(dev)
+        self.b = torch.from_numpy(B).to(dev)
+        self.pl = torch.from_numpy(self.packed).to(dev)
+        self.runner = DeviceErrorTrials(self.f, cfg.Q, cfg.N, cfg.mode, len(pair_ids), device=dev)
+        self.products = 2 * len(pair_ids)
+
+    def run(self, stream):
+        self.runner.run(self.a, self.b, self.pl, stream=stream)
+
+    def results(self):
+        r = self.runner
+        return (r.err_rand.cpu().numpy(), r.err_det.cpu().numpy(),
+                r.nf_rand.cpu().numpy().astype(bool), r.nf_det.cpu().numpy().astype(bool))
+
+    def e2e(self, steps):
+        """Public host-buffer call (rbc_error_trials) on pinned buffers."""
+        import numpy as np
+
+        from paper_1905_07439_b200.trials import error_trials
+
+        torch = self.torch
+        A_pin = torch.from_numpy(self.A).pin_memory()
+        B_pin = torch.from_numpy(self.B).pin_memory()
+        P_pin = torch.from_numpy(self.packed).pin_memory()
+        args = (self.f, self.cfg.Q, A_pin.numpy(), B_pin.numpy(), self.cfg.mode)
+        res = error_trials(*args, packed=P_pin.numpy())
+        err_r, err_d, _, _ = self.results()
+        if not (np.array_equal(res["err_rand"], err_r, equal_nan=True)
+                and np.array_equal(res["err_det"], err_d, equal_nan=True)):
+            raise SystemExit("e2e errors differ from the device-resident run")
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            error_trials(*args, packed=P_pin.numpy())
+        ms = (time.perf_counter() - t0) / steps * 1e3
+        h2d = self.A.nbytes + self.B.nbytes + self.packed.nbytes
+        d2h = 2 * len(err_r) * 9
+        return ms, h2d, d2h
+
+
+class AverageWorkload:
+    """c3: per pair truth + deterministic + G randomized products + running mean."""
+
+    def __init__(self, cfg, pair_ids, A, B, dev, torch):
+        from paper_1905_07439_b200.trials import DeviceAverageTrials
+
+        self.cfg, self.torch = cfg, torch
+        self.f = cfg.formula_obj()
+        self.A, self.B = A, B
+        G = cfg.plans_per_pair
+        self.G = G
+        self.rplans = [cfg.plan(cfg.plan_key(p, j)) for p in pair_ids for j in range(1, G + 1)]
+        self.runner = DeviceAverageTrials(self.f, cfg.Q, cfg.N, cfg.mode, len(pair_ids), G, device=dev)
+        self.tables = self.runner.tables(self.rplans)
+        self.a = torch.from_numpy(A).to(dev)
+        self.b = torch.from_numpy(B).to(dev)
+        self.products = (G + 1) * len(pair_ids)
+
+    def run(self, stream):
+        self.runner.run(self.a, self.b, self.tables, stream=stream)
+
+    def results(self):
+        r = self.runner.results()
+        nf_d = self.runner.nf_det.cpu().numpy().astype(bool)
+        return (r["err_rand"].ravel(), r["err_det"], r["nf_rand"].ravel(), nf_d)
+
+    def mean_errors(self):
+        return self.runner.results()["err_mean"]
+
+    def e2e(self, steps):
+        """Public host-buffer call (average_trials): hatted tables built from the
+        plans, operands and tables copied H2D, errors copied back, per step."""
+        import numpy as np
+
+        from paper_1905_07439_b200.trials import average_trials
+
+        torch = self.torch
+        A_pin = torch.from_numpy(self.A).pin_memory().numpy()
+        B_pin = torch.from_numpy(self.B).pin_memory().numpy()
+        args = (self.f, self.cfg.Q, A_pin, B_pin, self.cfg.mode, self.rplans, self.G)
+        res = average_trials(*args)
+        err_r, err_d, _, _ = self.results()
+        if not np.array_equal(res["err_rand"].ravel(), err_r, equal_nan=True):
+            raise SystemExit("e2e errors differ from the device-resident run")
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            average_trials(*args)
+        ms = (time.perf_counter() - t0) / steps * 1e3
+        es = np.dtype(self.cfg.mode.dtype).itemsize
+        h2d = self.A.nbytes + self.B.nbytes + sum(
+            3 * len(self.rplans) * self.cfg.rank * self.cfg.n ** 2 * es for _ in range(self.cfg.Q))
+        d2h = (len(self.rplans) + len(self.runner.cps) * len(self.A) + len(self.A)) * 8
+        return ms, h2d, d2h
+
+
 def run_ours(args):
     import numpy as np
     import torch
 
-    from paper_1905_07439_b200 import _lib
+    from paper_1905_07439_b200 import _lib, distributed
     from paper_1905_07439_b200.configs import get_config, make_pairs
-    from paper_1905_07439_b200.randomize import pack_recursive_plans
-    from paper_1905_07439_b200.trials import DeviceErrorTrials, error_trials
 
     world, rank, local = dist_env()
     if world > 1:
@@ -283,21 +437,14 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     _lib.require_device()
 
-    from paper_1905_07439_b200 import distributed
-
     cfg = get_config(args.config)
-    T = args.trials or cfg.trials
-    f = cfg.formula_obj()
+    T = args.trials or DEFAULTS[cfg.name]["pairs"]
     first, _ = distributed.shard(rank, world, T)
     pair_ids = distributed.pair_ids(rank, world, T)
     workers = min(32, max(1, (os.cpu_count() or 2) // max(1, world)))
     A, B = make_pairs(cfg, first, T, workers=workers)
-    packed = pack_recursive_plans([cfg.plan(cfg.plan_key(p)) for p in pair_ids], cfg.Q, cfg.n)
-
-    a_d = torch.from_numpy(A).to(dev)
-    b_d = torch.from_numpy(B).to(dev)
-    pl_d = torch.from_numpy(packed).to(dev)
-    runner = DeviceErrorTrials(f, cfg.Q, cfg.N, cfg.mode, T, device=dev)
+    kind = AverageWorkload if cfg.plans_per_pair > 1 else ErrorTrialWorkload
+    wl = kind(cfg, pair_ids, A, B, dev, torch)
     stream = torch.cuda.Stream(device=dev)
 
     def barrier():
@@ -307,7 +454,7 @@ def run_ours(args):
     clocks = Clocks(local)
     clocks.start()
     for _ in range(args.warmup):
-        runner.run(a_d, b_d, pl_d, stream=stream)
+        wl.run(stream)
     torch.cuda.synchronize()
     barrier()
     _lib.profile_enable(True)
@@ -316,7 +463,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(args.steps):
-        runner.run(a_d, b_d, pl_d, stream=stream)
+        wl.run(stream)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -325,78 +472,66 @@ def run_ours(args):
     _lib.profile_enable(False)
     launches = sum(v["count"] for v in prof.values())
     dev_ms = ev0.elapsed_time(ev1) / args.steps
+    err_r, err_d, nf_r, nf_d = wl.results()
 
-    err_r = runner.err_rand.cpu().numpy()
-    err_d = runner.err_det.cpu().numpy()
-    nf_r = runner.nf_rand.cpu().numpy().astype(bool)
-    nf_d = runner.nf_det.cpu().numpy().astype(bool)
-
-    # ---- e2e through the public host-buffer call
-    e2e_ms = None
-    h2d = A.nbytes + B.nbytes + packed.nbytes
-    d2h = 2 * T * 8 + 2 * T
+    e2e = None
     if not args.no_e2e:
-        A_pin = torch.from_numpy(A).pin_memory().numpy()
-        B_pin = torch.from_numpy(B).pin_memory().numpy()
-        P_pin = torch.from_numpy(packed).pin_memory().numpy()
-        res = error_trials(f, cfg.Q, A_pin, B_pin, cfg.mode, packed=P_pin)
-        same = (np.array_equal(res["err_rand"], err_r, equal_nan=True)
-                and np.array_equal(res["err_det"], err_d, equal_nan=True))
-        if not same:
-            raise SystemExit("e2e errors differ from the device-resident run")
         barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            error_trials(f, cfg.Q, A_pin, B_pin, cfg.mode, packed=P_pin)
-        torch.cuda.synchronize()
-        e2e_ms = (time.perf_counter() - t0) / args.steps * 1e3
+        e2e = wl.e2e(args.steps)
 
-    # ---- max over ranks + gather of per-trial statistics
-    tmax = distributed.max_over_ranks([dev_ms, e2e_ms or 0.0], device=dev)
-    dev_ms, e2e_ms = float(tmax[0]), (float(tmax[1]) if e2e_ms is not None else None)
+    tmax = distributed.max_over_ranks([dev_ms, e2e[0] if e2e else 0.0], device=dev)
+    dev_ms = float(tmax[0])
     allerr = distributed.gather_trials(
-        np.stack([err_r, err_d, nf_r.astype(np.float64), nf_d.astype(np.float64)]), device=dev)
-    err_r_all, err_d_all = allerr[0], allerr[1]
-    nf_r_all, nf_d_all = allerr[2] > 0, allerr[3] > 0
+        np.stack([err_r, nf_r.astype(np.float64)]), device=dev)
+    alldet = distributed.gather_trials(np.stack([err_d, nf_d.astype(np.float64)]), device=dev)
 
-    flops_step = 2 * cfg.effective_flops() * T * world
+    flops_step = 2.0 * cfg.N ** 3 * wl.products * world
     value = flops_step / (dev_ms / 1e3) / 1e9
     line = {
-        "metric": "effective GFLOP/s (2n^3/time) of randomized BC matmul error trials",
-        "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(dev_ms, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": cfg.mode.label,
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.mode.label,
         "data": "synthetic (seeded pairs and plans, reference seed layout; no dataset)",
-        "trials_per_s": round(T * world / (dev_ms / 1e3), 2),
+        "trials_per_s": round(T * world / (dev_ms / 1e3), 3),
+        "products_per_s": round(wl.products * world / (dev_ms / 1e3), 3),
         "config": {
             "workload": cfg.name, "desc": cfg.note, "formula": cfg.formula, "Q": cfg.Q,
-            "n": cfg.N, "pairs_per_rank": T, "products_per_pair": 2,
+            "n": cfg.N, "pairs_per_rank": T, "products_per_step_per_rank": wl.products,
             "parallelism": f"trial-sharded x{world}",
-            "l2": f"inputs {A.nbytes * 2 / 1e6:.0f} MB + truth {T * cfg.N ** 2 * 8 / 1e6:.0f} MB "
-                  "per step exceed the 126 MB L2 (no flush needed)",
+            "l2": f"per-step operands {A.nbytes * 2 / 1e6:.0f} MB + binary64 truth "
+                  f"{min(T, 1 if cfg.plans_per_pair > 1 else T) * cfg.N ** 2 * 8 / 1e6:.0f} MB and "
+                  "BC intermediates stream through HBM; the level working sets exceed the 126 MB L2 "
+                  "at these batch sizes, so no explicit flush is used",
         },
         "gpu_launches": launches,
         "clocks": clk,
         "roofline": roofline(prof, cfg.name),
-        "errors": distributed.trial_stats(err_r_all, err_d_all, nf_r_all, nf_d_all),
+        "errors": distributed.trial_stats(allerr[0], alldet[0], allerr[1] > 0, alldet[1] > 0),
     }
-    if e2e_ms is not None:
+    if hasattr(wl, "mean_errors"):
+        me = wl.mean_errors()
+        line["errors"]["running_mean_at_G"] = {
+            "mean": float(np.nanmean(me[:, -1])), "checkpoints": wl.runner.cps}
+    if e2e is not None:
+        e2e_ms = float(tmax[1])
         line["e2e"] = {"value": round(flops_step / (e2e_ms / 1e3) / 1e9, 3), "unit": "GFLOP/s",
-                       "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h2d),
-                       "d2h_bytes_per_step": int(d2h)}
+                       "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(e2e[1]),
+                       "d2h_bytes_per_step": int(e2e[2])}
 
-    # ---- CPU baseline (rank 0, N = 1)
     if rank == 0 and world == 1 and not args.no_cpu:
-        S = args.cpu_sample or default_cpu_sample(cfg)
-        dt, res = cpu_oracle_rate(cfg, pair_ids[:S], 1)
-        cpu_val = 2 * cfg.effective_flops() * S / dt / 1e9
-        got = np.stack([err_d[:S], err_r[:S]], axis=1)
-        want = np.array(res)
-        agree = bool(np.allclose(got, want, rtol=1e-10, atol=0, equal_nan=True))
+        count, per_pair, depth = DEFAULTS[cfg.name]["cpu"]
+        jobs = cpu_sample_jobs(cfg, first, count, per_pair, depth)
+        dt, res = run_cpu_jobs(jobs, 1)
+        cpu_val = sum(r[0] for r in res) / dt / 1e9
+        agree = None
+        if depth == 0 and cfg.plans_per_pair == 1 and per_pair == 2:
+            got = np.stack([err_d[:count], err_r[:count]], axis=1)
+            want = np.array([r[1] for r in res], dtype=np.float64)
+            agree = bool(np.allclose(got, want, rtol=1e-10, atol=0, equal_nan=True))
         line["cpu_baseline"] = {
-            "value": round(cpu_val, 5), "unit": "GFLOP/s", "cores": 1, "kind": "port",
-            "sample": f"first {S} pairs of the step through oracle/engine.py (numpy restatement "
-                      f"of randbc._engine), {dt:.1f} s", "errors_agree_with_gpu": agree,
+            "value": round(cpu_val, 6), "unit": "GFLOP/s", "cores": 1, "kind": "port",
+            "sample": describe_sample(cfg, count, per_pair, depth, dt, 1),
+            "errors_agree_with_gpu": agree,
         }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -161,6 +161,25 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
                      double* err_det, uint8_t* nonfinite_rand, uint8_t* nonfinite_det);
 
 size_t rbc_error_trials_workspace_bytes(int dtype, int formula, int Q, int64_t T, int64_t N);
+
+/* ---- averaging trials (experiments.py:264-296; BASELINE config 3) --------
+ * For each of P operand pairs (a[p], b[p]): the binary64 truth, optionally
+ * the deterministic product from det_u/v/w (Tc = 1 tables per level), and G
+ * randomized products from u/v/w (per level (P*G, R, n, n) hatted tables; pair
+ * p owns trials p*G .. p*G+G-1).  Outputs: per-plan errors err_rand (P*G),
+ * running binary64 mean errors err_mean (P * ncheck) at the ascending
+ * checkpoints (1..G; total_i = fl(total_{i-1} + C_i), error of fl(total_i / i)),
+ * deterministic errors err_det (P).  Device pointers, stream ordered. */
+size_t rbc_average_trials_workspace_bytes(int dtype, int Q, const int32_t* n, const int32_t* R,
+                                          int64_t G, int64_t N);
+int rbc_average_trials_async(int dtype, int Q, const int32_t* n, const int32_t* R, int64_t P,
+                             int64_t G, int64_t N, const void* a, const void* b,
+                             const void* const* u, const void* const* v, const void* const* w,
+                             const void* const* det_u, const void* const* det_v,
+                             const void* const* det_w, int ncheck, const int32_t* checkpoints,
+                             double* err_rand, double* err_mean, double* err_det,
+                             uint8_t* nonfinite_rand, uint8_t* nonfinite_det, void* workspace,
+                             size_t workspace_bytes, void* stream);
 /* Device variant: det_plans is a device (1, Q) identity table or NULL. */
 int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
                            const void* b, const void* rand_plans, const void* det_plans,

@@ -47,6 +47,8 @@ EXPORTS = (
     "rbc_error_trials",
     "rbc_error_trials_workspace_bytes",
     "rbc_error_trials_async",
+    "rbc_average_trials_workspace_bytes",
+    "rbc_average_trials_async",
 )
 
 _lock = threading.Lock()
@@ -103,6 +105,13 @@ def _declare(lib):
             [c_int, c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp],
         ),
         "rbc_error_trials_workspace_bytes": (c_size, [c_int, c_int, c_int, c_i64, c_i64]),
+        "rbc_average_trials_workspace_bytes": (c_size, [c_int, c_int, P(c_i32), P(c_i32), c_i64, c_i64]),
+        "rbc_average_trials_async": (
+            c_int,
+            [c_int, c_int, P(c_i32), P(c_i32), c_i64, c_i64, c_i64, c_vp, c_vp,
+             P(c_vp), P(c_vp), P(c_vp), P(c_vp), P(c_vp), P(c_vp), c_int, P(c_i32),
+             c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp],
+        ),
         "rbc_error_trials_async": (
             c_int,
             [c_int, c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,

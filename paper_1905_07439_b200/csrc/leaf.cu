@@ -186,6 +186,84 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     }
 }
 
+// Small square leaves (M x M, M below a tile): one CTA stages LPB whole
+// leaves of X and Y in shared memory with coalesced loads (leaves are
+// contiguous), then each thread computes a TR x TR register tile of one leaf
+// with the sequential k chain.  Serves config 3's 27x27 binary64 leaves.
+template <class TIn, class TAcc, int M, int TR>
+__global__ void __launch_bounds__(256) leaf_smem_kernel(int64_t batch, const TIn* __restrict__ x,
+                                                        int64_t xs, const TIn* __restrict__ y,
+                                                        int64_t ys, TAcc* __restrict__ out) {
+  constexpr int TPL = (M / TR) * (M / TR);  // threads per leaf
+  constexpr int LPB = 256 / TPL;            // leaves per block
+  static_assert(M % TR == 0 && LPB >= 1, "leaf tiling");
+  using A = Arith<TAcc>;
+  __shared__ TAcc Xs[LPB][M * M];
+  __shared__ TAcc Ys[LPB][M * M];
+  const int64_t b0 = (int64_t)blockIdx.x * LPB;
+  const int nl = batch - b0 < LPB ? (int)(batch - b0) : LPB;
+  for (int e = threadIdx.x; e < nl * M * M; e += blockDim.x) {
+    const int l = e / (M * M), q = e - l * (M * M);
+    Xs[l][q] = widen_to<TIn, TAcc>(x[(b0 + l) * xs + q]);
+    Ys[l][q] = widen_to<TIn, TAcc>(y[(b0 + l) * ys + q]);
+  }
+  __syncthreads();
+  const int l = threadIdx.x / TPL;
+  if (l >= nl) return;
+  const int r = threadIdx.x - l * TPL;
+  const int ti = (r / (M / TR)) * TR, tj = (r % (M / TR)) * TR;
+  TAcc acc[TR][TR];
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TR; ++j) acc[i][j] = A::mul(Xs[l][(ti + i) * M], Ys[l][tj + j]);
+#pragma unroll 3
+  for (int k = 1; k < M; ++k) {
+    TAcc a[TR], bb[TR];
+#pragma unroll
+    for (int i = 0; i < TR; ++i) a[i] = Xs[l][(ti + i) * M + k];
+#pragma unroll
+    for (int j = 0; j < TR; ++j) bb[j] = Ys[l][k * M + tj + j];
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < TR; ++j) acc[i][j] = A::add(acc[i][j], A::mul(a[i], bb[j]));
+  }
+  TAcc* o = out + (b0 + l) * (int64_t)M * M;
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TR; ++j) o[(ti + i) * M + tj + j] = acc[i][j];
+}
+
+template <class TIn, class TAcc, int M, int TR>
+cudaError_t run_smem(int64_t batch, const void* x, int64_t xs, const void* y, int64_t ys,
+                     void* out, cudaStream_t st) {
+  constexpr int LPB = 256 / ((M / TR) * (M / TR));
+  const int64_t blocks = (batch + LPB - 1) / LPB;
+  leaf_smem_kernel<TIn, TAcc, M, TR><<<(unsigned)blocks, 256, 0, st>>>(
+      batch, (const TIn*)x, xs, (const TIn*)y, ys, (TAcc*)out);
+  return cudaGetLastError();
+}
+
+// Square small leaves with a shared-memory kernel instantiation; returns
+// cudaErrorNotSupported when none applies.
+template <class TIn, class TAcc>
+cudaError_t small_square(int64_t batch, int64_t M, const void* x, int64_t xs, const void* y,
+                         int64_t ys, void* out, cudaStream_t st) {
+  switch (M) {
+    case 27: return run_smem<TIn, TAcc, 27, 3>(batch, x, xs, y, ys, out, st);
+    case 24: return run_smem<TIn, TAcc, 24, 3>(batch, x, xs, y, ys, out, st);
+    case 18: return run_smem<TIn, TAcc, 18, 3>(batch, x, xs, y, ys, out, st);
+    case 16: return run_smem<TIn, TAcc, 16, 2>(batch, x, xs, y, ys, out, st);
+    case 12: return run_smem<TIn, TAcc, 12, 2>(batch, x, xs, y, ys, out, st);
+    case 10: return run_smem<TIn, TAcc, 10, 2>(batch, x, xs, y, ys, out, st);
+    case 9: return run_smem<TIn, TAcc, 9, 3>(batch, x, xs, y, ys, out, st);
+    case 8: return run_smem<TIn, TAcc, 8, 2>(batch, x, xs, y, ys, out, st);
+  }
+  return cudaErrorNotSupported;
+}
+
 // binary16 leaves: the same tiling with half2 SIMD along N.  Each HMUL2 /
 // HADD2 lane rounds exactly like the scalar __hmul_rn / __hadd_rn, so every
 // output keeps its own sequential k chain (two adjacent outputs per op).
@@ -389,6 +467,10 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
     return run_tiled<TIn, TAcc, 64, 64, 8, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
   if (M >= 32 && N >= 32)
     return run_tiled<TIn, TAcc, 32, 32, 8, 2, 2>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (M == N && M == K && forced != 2) {
+    cudaError_t e = small_square<TIn, TAcc>(batch, M, x, xs, y, ys, out, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   return run_small<TIn, TAcc>(batch, M, K, N, x, xs, y, ys, out, st);
 }
 

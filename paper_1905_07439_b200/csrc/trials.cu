@@ -19,9 +19,6 @@
 #include "../../include/rbc.h"
 #include "kernels.h"
 
-extern "C" int rbc_apply_plans_async(int, int, int, int64_t, const void*, int64_t, int64_t,
-                                     const void*, const void*, int64_t, void*, uint8_t*, void*,
-                                     size_t, void*);
 
 namespace rbc {
 int set_error_public(int code, const char* msg);
@@ -47,6 +44,74 @@ Layout layout_for(int dtype, int formula, int Q, int64_t chunk, int64_t N) {
 }
 
 }  // namespace
+
+// ---- running mean (reference experiments.py:279-289) ----------------------
+// total_i = fl(total_{i-1} + C_i) in binary64 from total_0 = 0, plan order;
+// at each checkpoint i: sum over elements of (fl(total_i / i) - ref)^2.
+constexpr int kMaxCheckpoints = 32;
+struct Checkpoints {
+  int n;
+  int at[kMaxCheckpoints];
+};
+
+constexpr int kMeanThreads = 256;
+constexpr int kMeanBlocks = 64;
+
+template <class T>
+__global__ void __launch_bounds__(kMeanThreads) running_mean_kernel(
+    int G, int64_t N2, const T* __restrict__ C, const double* __restrict__ ref, Checkpoints cp,
+    double* __restrict__ part /* (cp.n + 1) x gridDim.x */) {
+  __shared__ double sh[kMeanThreads / 32];
+  double s[kMaxCheckpoints + 1];
+#pragma unroll
+  for (int c = 0; c <= kMaxCheckpoints; ++c) s[c] = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * kMeanThreads + threadIdx.x; e < N2;
+       e += (int64_t)gridDim.x * kMeanThreads) {
+    const double r = ref[e];
+    double total = 0.0;
+    int c = 0;
+    for (int t = 0; t < G; ++t) {
+      total = __dadd_rn(total, rbc::Arith<T>::widen(C[(int64_t)t * N2 + e]));
+      if (c < cp.n && t + 1 == cp.at[c]) {
+        const double d = __dsub_rn(__ddiv_rn(total, (double)(t + 1)), r);
+#pragma unroll
+        for (int k = 0; k < kMaxCheckpoints; ++k)
+          if (k == c) s[k] += d * d;
+        ++c;
+      }
+    }
+    s[kMaxCheckpoints] += r * r;
+  }
+  for (int c = 0; c <= cp.n; ++c) {
+    double v = c == cp.n ? s[kMaxCheckpoints] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kMaxCheckpoints; ++k)
+      if (k == c && c < cp.n) v = s[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < kMeanThreads / 32; ++w) tot += sh[w];
+      part[c * gridDim.x + blockIdx.x] = tot;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void running_mean_finish(int ncp, int nb, const double* __restrict__ part,
+                                    double* __restrict__ err) {
+  const int c = threadIdx.x;
+  if (c >= ncp) return;
+  double num = 0.0, den = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    num += part[c * nb + b];
+    den += part[ncp * nb + b];
+  }
+  err[c] = sqrt(num) / sqrt(den);
+}
 
 extern "C" {
 
@@ -103,6 +168,113 @@ int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, 
         e = launch_rel_errors(dtype, nt, N2, prod, ref, N2, err + t0, scratch, st);
         if (e != cudaSuccess) return fail_cuda(e, "rel_errors", __FILE__, __LINE__);
       }
+    }
+  }
+  return RBC_OK;
+}
+
+// ---- averaging trials (config 3; reference _run_average, experiments.py:264-296)
+// For each of P pairs: binary64 truth, optional deterministic product
+// (coefficient tables det_u/v/w, Tc = 1), G randomized products (tables
+// u/v/w with P*G trials, pair p owning trials p*G .. p*G+G-1), their
+// per-plan errors, and the running-mean error at each checkpoint.
+size_t rbc_average_trials_workspace_bytes(int dtype, int Q, const int32_t* n, const int32_t* R,
+                                          int64_t G, int64_t N) {
+  using namespace rbc;
+  const size_t N2 = (size_t)N * N;
+  return a256(N2 * 8) + a256((size_t)G * N2 * dtype_size(dtype)) +
+         a256(error_scratch_bytes(G)) + a256((size_t)(kMaxCheckpoints + 1) * kMeanBlocks * 8) +
+         a256(rbc_levels_workspace_bytes(dtype, Q, n, R, G, N));
+}
+
+int rbc_average_trials_async(int dtype, int Q, const int32_t* n, const int32_t* R, int64_t P,
+                             int64_t G, int64_t N, const void* a, const void* b,
+                             const void* const* u, const void* const* v, const void* const* w,
+                             const void* const* det_u, const void* const* det_v,
+                             const void* const* det_w, int ncheck, const int32_t* checkpoints,
+                             double* err_rand, double* err_mean, double* err_det,
+                             uint8_t* nf_rand, uint8_t* nf_det, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  using namespace rbc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (P == 0 || G == 0 || N == 0) return RBC_OK;
+  if (ncheck < 0 || ncheck > kMaxCheckpoints)
+    return set_error_public(RBC_EVALUE, "at most 32 checkpoints");
+  Checkpoints cp;
+  cp.n = ncheck;
+  for (int c = 0; c < ncheck; ++c) {
+    cp.at[c] = checkpoints[c];
+    if (cp.at[c] < 1 || cp.at[c] > G || (c && cp.at[c] <= cp.at[c - 1]))
+      return set_error_public(RBC_EVALUE, "checkpoints must ascend within 1..G");
+  }
+  const size_t need = rbc_average_trials_workspace_bytes(dtype, Q, n, R, G, N);
+  if (workspace_bytes < need) return set_error_public(RBC_EVALUE, "workspace too small");
+  const size_t es = dtype_size(dtype);
+  const int64_t N2 = N * N;
+  char* base = (char*)workspace;
+  double* ref = (double*)base;
+  base += a256(N2 * 8);
+  void* prod = base;
+  base += a256((size_t)G * N2 * es);
+  void* scratch = base;
+  base += a256(error_scratch_bytes(G));
+  double* part = (double*)base;
+  base += a256((size_t)(kMaxCheckpoints + 1) * kMeanBlocks * 8);
+  void* eng = base;
+  const size_t eng_bytes = rbc_levels_workspace_bytes(dtype, Q, n, R, G, N);
+  std::vector<const void*> pu(Q), pv(Q), pw(Q);
+  std::vector<int64_t> tcG(Q, G), tc1(Q, 1);
+  for (int64_t p = 0; p < P; ++p) {
+    const char* ap = (const char*)a + (size_t)p * N2 * es;
+    const char* bp = (const char*)b + (size_t)p * N2 * es;
+    cudaError_t e;
+    {
+      Stage stage(st, "truth_f64", (double)N2 * (2.0 * es + 8.0), 2.0 * (double)N2 * N);
+      e = launch_leaf(dtype, kF64, 1, N, N, N, ap, N2, bp, N2, ref, st);
+    }
+    if (e != cudaSuccess) return fail_cuda(e, "truth", __FILE__, __LINE__);
+    if (det_u && err_det) {
+      int rc = rbc_apply_levels_async(dtype, Q, n, R, tc1.data(), det_u, det_v, det_w, 1, N, ap,
+                                      bp, 1, prod, nf_det ? nf_det + p : nullptr, eng, eng_bytes,
+                                      stream);
+      if (rc != RBC_OK) return rc;
+      Stage stage(st, "rel_errors", (double)N2 * (es + 8.0), 3.0 * (double)N2);
+      e = launch_rel_errors(dtype, 1, N2, prod, ref, 0, err_det + p, scratch, st);
+      if (e != cudaSuccess) return fail_cuda(e, "rel_errors", __FILE__, __LINE__);
+    }
+    for (int q = 0; q < Q; ++q) {
+      const size_t off = (size_t)p * G * R[q] * n[q] * n[q] * es;
+      pu[q] = (const char*)u[q] + off;
+      pv[q] = (const char*)v[q] + off;
+      pw[q] = (const char*)w[q] + off;
+    }
+    int rc = rbc_apply_levels_async(dtype, Q, n, R, tcG.data(), pu.data(), pv.data(), pw.data(), 1,
+                                    N, ap, bp, G, prod, nf_rand ? nf_rand + p * G : nullptr, eng,
+                                    eng_bytes, stream);
+    if (rc != RBC_OK) return rc;
+    {
+      Stage stage(st, "rel_errors", (double)G * N2 * (es + 8.0), 3.0 * (double)G * N2);
+      e = launch_rel_errors(dtype, G, N2, prod, ref, 0, err_rand + p * G, scratch, st);
+    }
+    if (e != cudaSuccess) return fail_cuda(e, "rel_errors", __FILE__, __LINE__);
+    if (ncheck && err_mean) {
+      Stage stage(st, "running_mean", (double)G * N2 * es + N2 * 8.0, 2.0 * (double)G * N2);
+      switch (dtype) {
+        case kF64:
+          running_mean_kernel<double><<<kMeanBlocks, kMeanThreads, 0, st>>>(
+              (int)G, N2, (const double*)prod, ref, cp, part);
+          break;
+        case kF32:
+          running_mean_kernel<float><<<kMeanBlocks, kMeanThreads, 0, st>>>(
+              (int)G, N2, (const float*)prod, ref, cp, part);
+          break;
+        default:
+          running_mean_kernel<__half><<<kMeanBlocks, kMeanThreads, 0, st>>>(
+              (int)G, N2, (const __half*)prod, ref, cp, part);
+      }
+      running_mean_finish<<<1, 32, 0, st>>>(ncheck, kMeanBlocks, part, err_mean + p * ncheck);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return fail_cuda(e, "running_mean", __FILE__, __LINE__);
     }
   }
   return RBC_OK;

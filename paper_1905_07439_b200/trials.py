@@ -71,6 +71,113 @@ def error_trials(f, Q: int, A, B, mode, rplans=None, packed=None, with_det: bool
     return out
 
 
+def checkpoint_grid(total: int):
+    """Running-average checkpoints 1..9, 10..90, ..., plus total
+    (reference experiments.py:304-316)."""
+    if total < 1:
+        raise ValueError("total must be >= 1")
+    pts = set()
+    decade = 1
+    while decade <= total:
+        pts.update(k * decade for k in range(1, 10) if k * decade <= total)
+        decade *= 10
+    pts.add(total)
+    return sorted(pts)
+
+
+class DeviceAverageTrials:
+    """Averaging trials on the device (config 3): per pair the binary64 truth,
+    the deterministic product, G randomized products with per-plan errors and
+    running-mean errors at ``checkpoint_grid(G)`` (reference
+    experiments.py:264-296).  Any formula (dense coefficient tables)."""
+
+    def __init__(self, f, Q: int, N: int, mode, P: int, G: int, device="cuda:0", checkpoints=None):
+        import torch
+
+        from .multiply import mode_tensors
+
+        self.torch = torch
+        self.f, self.Q, self.N, self.P, self.G = f, Q, N, P, G
+        self.m = mode_of(mode)
+        self.device = torch.device(device)
+        self.cps = list(checkpoints) if checkpoints is not None else checkpoint_grid(G)
+        self.n_arr = (ctypes.c_int32 * Q)(*([f.n] * Q))
+        self.R_arr = (ctypes.c_int32 * Q)(*([f.rank] * Q))
+        lib = _lib.load()
+        need = lib.rbc_average_trials_workspace_bytes(dtype_code(self.m), Q, self.n_arr, self.R_arr, G, N)
+        self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        det = mode_tensors(f, self.m)
+        self.det = [torch.from_numpy(np.ascontiguousarray(t)).to(self.device) for t in det]
+        self.err_rand = torch.empty(P * G, dtype=torch.float64, device=self.device)
+        self.err_mean = torch.empty(P * len(self.cps), dtype=torch.float64, device=self.device)
+        self.err_det = torch.empty(P, dtype=torch.float64, device=self.device)
+        self.nf_rand = torch.empty(P * G, dtype=torch.uint8, device=self.device)
+        self.nf_det = torch.empty(P, dtype=torch.uint8, device=self.device)
+
+    def tables(self, rplans):
+        """Per-level (P*G, R, n, n) hatted tables on the device."""
+        from .randomize import plan_levels
+
+        if len(rplans) != self.P * self.G:
+            raise ValueError("need P*G recursive plans")
+        out = []
+        for q in range(self.Q):
+            u, v, w = plan_levels(self.f, [rp.levels[q] for rp in rplans], self.m)
+            out.append(tuple(self.torch.from_numpy(t).to(self.device) for t in (u, v, w)))
+        return out
+
+    def run(self, a, b, tables, with_det: bool = True, stream=None):
+        torch = self.torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        Q = self.Q
+        vp = lambda ts: (ctypes.c_void_p * Q)(*[t.data_ptr() for t in ts])  # noqa: E731
+        u = vp([tb[0] for tb in tables])
+        v = vp([tb[1] for tb in tables])
+        w = vp([tb[2] for tb in tables])
+        du = vp([self.det[0]] * Q) if with_det else None
+        dv = vp([self.det[1]] * Q) if with_det else None
+        dw = vp([self.det[2]] * Q) if with_det else None
+        cps = (ctypes.c_int32 * len(self.cps))(*self.cps)
+        rc = _lib.load().rbc_average_trials_async(
+            dtype_code(self.m), Q, self.n_arr, self.R_arr, self.P, self.G, self.N,
+            ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()), u, v, w, du, dv, dw,
+            len(self.cps), cps, ctypes.c_void_p(self.err_rand.data_ptr()),
+            ctypes.c_void_p(self.err_mean.data_ptr()),
+            ctypes.c_void_p(self.err_det.data_ptr()) if with_det else None,
+            ctypes.c_void_p(self.nf_rand.data_ptr()),
+            ctypes.c_void_p(self.nf_det.data_ptr()) if with_det else None,
+            ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(), ctypes.c_void_p(st.cuda_stream),
+        )
+        _lib.check(rc)
+
+    def results(self):
+        return {
+            "err_rand": self.err_rand.cpu().numpy().reshape(self.P, self.G),
+            "err_mean": self.err_mean.cpu().numpy().reshape(self.P, len(self.cps)),
+            "err_det": self.err_det.cpu().numpy(),
+            "nf_rand": self.nf_rand.cpu().numpy().reshape(self.P, self.G).astype(bool),
+            "checkpoints": list(self.cps),
+        }
+
+
+def average_trials(f, Q: int, A, B, mode, rplans, G: int, checkpoints=None, device="cuda:0"):
+    """Host-buffer entry point for averaging trials: (P, N, N) operands and
+    P*G recursive plans in; per-plan, running-mean and deterministic errors out."""
+    import torch
+
+    m = mode_of(mode)
+    A = np.ascontiguousarray(A, dtype=m.dtype)
+    B = np.ascontiguousarray(B, dtype=m.dtype)
+    P, N, _ = A.shape
+    runner = DeviceAverageTrials(f, Q, N, m, P, G, device=device, checkpoints=checkpoints)
+    tables = runner.tables(list(rplans))
+    a = torch.from_numpy(A).to(runner.device, non_blocking=True)
+    b = torch.from_numpy(B).to(runner.device, non_blocking=True)
+    runner.run(a, b, tables)
+    torch.cuda.synchronize(runner.device)
+    return runner.results()
+
+
 class DeviceErrorTrials:
     """Device-resident pipeline over torch CUDA tensors (throughput path)."""
 

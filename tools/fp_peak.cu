@@ -9,6 +9,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false tools/fp_peak.cu -o tools/fp_peak
 //   ./tools/fp_peak > profiles/fp_peaks.json
 #include <cuda_fp16.h>
+#include <cstdint>
 #include <cstdio>
 
 constexpr int kChains = 16;
@@ -28,8 +29,18 @@ template <> struct Ops<double> {
   static constexpr double flops_per_op = 2.0;
 };
 template <> struct Ops<__half2> {
-  static __device__ __half2 mul(__half2 a, __half2 b) { return __hmul2_rn(a, b); }
-  static __device__ __half2 add(__half2 a, __half2 b) { return __hadd2_rn(a, b); }
+  // inline PTX so the chain is issued exactly as written (one HMUL2 and one
+  // HADD2 per step)
+  static __device__ __half2 mul(__half2 a, __half2 b) {
+    uint32_t r, x = *reinterpret_cast<uint32_t*>(&a), y = *reinterpret_cast<uint32_t*>(&b);
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+    return *reinterpret_cast<__half2*>(&r);
+  }
+  static __device__ __half2 add(__half2 a, __half2 b) {
+    uint32_t r, x = *reinterpret_cast<uint32_t*>(&a), y = *reinterpret_cast<uint32_t*>(&b);
+    asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+    return *reinterpret_cast<__half2*>(&r);
+  }
   static __device__ __half2 from(float x) { return __float2half2_rn(x); }
   static constexpr double flops_per_op = 4.0;
 };
