@@ -97,6 +97,182 @@ __global__ void __launch_bounds__(kThreads) contract_dense_kernel(
   }
 }
 
+// ---- staged variants: one CTA per (trial, 256*PPT positions); the trial's
+// coefficient table lives in shared memory (broadcast reads) and each thread
+// carries PPT positions so one coefficient read feeds PPT multiply-adds.
+constexpr int kPPT = 4;
+
+template <class T, int N>
+__global__ void __launch_bounds__(kThreads) expand_dense_staged(
+    const T* __restrict__ x, int64_t x_tstride, int K, int s, int R, const T* __restrict__ coeff,
+    int64_t c_tstride, T* __restrict__ out, int64_t ntr) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  T* sc = reinterpret_cast<T*>(sraw);
+  using A = Arith<T>;
+  const int mb = s / N;
+  const int P = mb * mb;
+  const int64_t items = (int64_t)K * P;
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < R * N * N; q += kThreads) sc[q] = coeff[t * c_tstride + q];
+    __syncthreads();
+    const T* xt = x + t * x_tstride;
+    T g[kPPT][N * N];
+    int64_t obase[kPPT];
+    bool live[kPPT];
+#pragma unroll
+    for (int p = 0; p < kPPT; ++p) {
+      const int64_t e = ((int64_t)blockIdx.x * kPPT + p) * kThreads + threadIdx.x;
+      live[p] = e < items;
+      const int64_t ee = live[p] ? e : 0;
+      const int Kp = (int)(ee / P);
+      const int pos = (int)(ee - (int64_t)Kp * P);
+      const int i = pos / mb, j = pos - (pos / mb) * mb;
+      const T* xb = xt + (int64_t)Kp * s * s + (int64_t)i * s + j;
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+#pragma unroll
+        for (int l = 0; l < N; ++l) g[p][k * N + l] = live[p] ? xb[(int64_t)k * mb * s + l * mb] : T(0);
+      obase[p] = (t * K + Kp) * (int64_t)R * P + pos;
+    }
+    for (int r = 0; r < R; ++r) {
+      const T* cr = sc + r * N * N;
+      T acc[kPPT];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        T row[kPPT];
+#pragma unroll
+        for (int p = 0; p < kPPT; ++p) row[p] = A::mul(cr[k * N], g[p][k * N]);
+#pragma unroll
+        for (int l = 1; l < N; ++l) {
+          const T c = cr[k * N + l];
+#pragma unroll
+          for (int p = 0; p < kPPT; ++p) row[p] = A::add(row[p], A::mul(c, g[p][k * N + l]));
+        }
+#pragma unroll
+        for (int p = 0; p < kPPT; ++p) acc[p] = (k == 0) ? row[p] : A::add(acc[p], row[p]);
+      }
+#pragma unroll
+      for (int p = 0; p < kPPT; ++p)
+        if (live[p]) out[obase[p] + (int64_t)r * P] = acc[p];
+    }
+  }
+}
+
+template <class T, int N>
+__global__ void __launch_bounds__(kThreads) contract_dense_staged(
+    const T* __restrict__ ch, int K, int mb, int R, const T* __restrict__ w, int64_t w_tstride,
+    T* __restrict__ out, int64_t ntr, uint8_t* __restrict__ nonfinite) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  T* sw = reinterpret_cast<T*>(sraw);
+  using A = Arith<T>;
+  const int s = N * mb;
+  const int P = mb * mb;
+  const int64_t items = (int64_t)K * P;
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < R * N * N; q += kThreads) sw[q] = w[t * w_tstride + q];
+    __syncthreads();
+    int64_t cbase[kPPT], obase[kPPT];
+    bool live[kPPT];
+#pragma unroll
+    for (int p = 0; p < kPPT; ++p) {
+      const int64_t e = ((int64_t)blockIdx.x * kPPT + p) * kThreads + threadIdx.x;
+      live[p] = e < items;
+      const int64_t ee = live[p] ? e : 0;
+      const int Kp = (int)(ee / P);
+      const int pos = (int)(ee - (int64_t)Kp * P);
+      const int i = pos / mb, j = pos - (pos / mb) * mb;
+      cbase[p] = (t * K + Kp) * (int64_t)R * P + pos;
+      obase[p] = (t * K + Kp) * (int64_t)s * s + (int64_t)i * s + j;
+    }
+    T acc[N * N][kPPT];
+    for (int r = 0; r < R; ++r) {
+      T pr[kPPT];
+#pragma unroll
+      for (int p = 0; p < kPPT; ++p) pr[p] = live[p] ? ch[cbase[p] + (int64_t)r * P] : T(0);
+      const T* wr = sw + r * N * N;
+#pragma unroll
+      for (int ij = 0; ij < N * N; ++ij) {
+        const T c = wr[ij];
+#pragma unroll
+        for (int p = 0; p < kPPT; ++p)
+          acc[ij][p] = (r == 0) ? A::mul(c, pr[p]) : A::add(acc[ij][p], A::mul(c, pr[p]));
+      }
+    }
+    bool ok = true;
+#pragma unroll
+    for (int p = 0; p < kPPT; ++p) {
+      if (!live[p]) continue;
+#pragma unroll
+      for (int I = 0; I < N; ++I)
+#pragma unroll
+        for (int J = 0; J < N; ++J) {
+          const T v = acc[I * N + J][p];
+          if (nonfinite) ok = ok && Arith<T>::finite(v);
+          out[obase[p] + (int64_t)I * mb * s + J * mb] = v;
+        }
+    }
+    if (!ok) nonfinite[t] = 1;
+  }
+}
+
+template <class T, int N>
+cudaError_t staged_expand_n(const void* x, int64_t xs, int64_t K, int64_t s, int R, const void* c,
+                            int64_t cs, void* out, int64_t ntr, cudaStream_t st) {
+  const int64_t items = K * (s / N) * (s / N);
+  const size_t smem = (size_t)R * N * N * sizeof(T);
+  auto kern = expand_dense_staged<T, N>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((unsigned)((items + kThreads * kPPT - 1) / (kThreads * kPPT)),
+            (unsigned)(ntr < 65535 ? ntr : 65535));
+  kern<<<grid, kThreads, smem, st>>>((const T*)x, xs, (int)K, (int)s, R, (const T*)c, cs, (T*)out, ntr);
+  return cudaGetLastError();
+}
+
+template <class T, int N>
+cudaError_t staged_contract_n(const void* ch, int64_t K, int64_t mb, int R, const void* w,
+                              int64_t ws, void* out, int64_t ntr, uint8_t* nf, cudaStream_t st) {
+  const int64_t items = K * mb * mb;
+  const size_t smem = (size_t)R * N * N * sizeof(T);
+  auto kern = contract_dense_staged<T, N>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((unsigned)((items + kThreads * kPPT - 1) / (kThreads * kPPT)),
+            (unsigned)(ntr < 65535 ? ntr : 65535));
+  kern<<<grid, kThreads, smem, st>>>((const T*)ch, (int)K, (int)mb, R, (const T*)w, ws, (T*)out, ntr, nf);
+  return cudaGetLastError();
+}
+
+// Returns cudaErrorNotSupported when no staged instantiation applies.
+template <class T>
+cudaError_t staged_expand(int n, const void* x, int64_t xs, int64_t K, int64_t s, int R,
+                          const void* c, int64_t cs, void* out, int64_t ntr, cudaStream_t st) {
+  if ((size_t)R * n * n * sizeof(T) > 160 * 1024) return cudaErrorNotSupported;
+  switch (n) {
+    case 2: return staged_expand_n<T, 2>(x, xs, K, s, R, c, cs, out, ntr, st);
+    case 3: return staged_expand_n<T, 3>(x, xs, K, s, R, c, cs, out, ntr, st);
+    case 4: return staged_expand_n<T, 4>(x, xs, K, s, R, c, cs, out, ntr, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <class T>
+cudaError_t staged_contract(int n, const void* ch, int64_t K, int64_t mb, int R, const void* w,
+                            int64_t ws, void* out, int64_t ntr, uint8_t* nf, cudaStream_t st) {
+  if ((size_t)R * n * n * sizeof(T) > 160 * 1024) return cudaErrorNotSupported;
+  switch (n) {
+    case 2: return staged_contract_n<T, 2>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+    case 3: return staged_contract_n<T, 3>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+  }
+  return cudaErrorNotSupported;
+}
+
 inline dim3 grid_for(int64_t items, int64_t ntr) {
   const int64_t bx = (items + kThreads - 1) / kThreads;
   return dim3((unsigned)bx, (unsigned)(ntr < 65535 ? ntr : 65535), 1);
@@ -123,6 +299,10 @@ template <class T>
 cudaError_t expand_dense_t(int dtype, const void* x, int64_t xs, int64_t K, int64_t s, int n,
                            int R, const void* c, int64_t cs, void* out, int64_t ntr,
                            cudaStream_t st) {
+  {
+    cudaError_t e = staged_expand<T>(n, x, xs, K, s, R, c, cs, out, ntr, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const int W = n > 4 ? 1 : pick_width(dtype, s / n, 8 / (int)sizeof(T));
   switch (W) {
     case 4: return expand_dense_w<T, (sizeof(T) == 2 ? 4 : 1)>(x, xs, K, s, n, R, c, cs, out, ntr, st);
@@ -135,6 +315,10 @@ template <class T>
 cudaError_t contract_dense_t(int dtype, const void* ch, int64_t K, int64_t mb, int n, int R,
                              const void* w, int64_t ws, void* out, int64_t ntr, uint8_t* nf,
                              cudaStream_t st) {
+  {
+    cudaError_t e = staged_contract<T>(n, ch, K, mb, R, w, ws, out, ntr, nf, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const int W = pick_width(dtype, mb, 8 / (int)sizeof(T));
   if (W >= 2 && sizeof(T) <= 4) {
     constexpr int W2 = sizeof(T) <= 4 ? 2 : 1;

@@ -454,6 +454,17 @@ template <class TIn, class TAcc>
 cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x,
                           int64_t xs, const void* y, int64_t ys, void* out, cudaStream_t st) {
   const int forced = tile_override();
+  // tuning variants (RBC_LEAF_TILE=2xx)
+  if (forced == 201 && M >= 64 && N >= 128)
+    return run_tiled<TIn, TAcc, 64, 128, 8, 4, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (forced == 202 && M >= 128 && N >= 64)
+    return run_tiled<TIn, TAcc, 128, 64, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (forced == 203 && M >= 64 && N >= 64)
+    return run_tiled<TIn, TAcc, 64, 64, 16, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (forced == 204 && M >= 64 && N >= 64)
+    return run_tiled<TIn, TAcc, 64, 64, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (forced == 206 && M >= 64 && N >= 64)
+    return run_tiled<TIn, TAcc, 64, 64, 4, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
   if (forced == 128 && M >= 128 && N >= 128)
     return run_tiled<TIn, TAcc, 128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
   if (forced == 64 && M >= 64 && N >= 64)
@@ -461,6 +472,9 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
   if (forced == 32 && M >= 32 && N >= 32)
     return run_tiled<TIn, TAcc, 32, 32, 8, 2, 2>(batch, M, K, N, x, xs, y, ys, out, st);
   if (forced == 1) return run_small<TIn, TAcc>(batch, M, K, N, x, xs, y, ys, out, st);
+  // binary64: 64x128 tiles of 4x8 outputs per thread (ncu: DP pipe ~72% busy)
+  if (sizeof(TAcc) == 8 && M >= 64 && N >= 128)
+    return run_tiled<TIn, TAcc, 64, 128, 8, 4, 8>(batch, M, K, N, x, xs, y, ys, out, st);
   if (M >= 128 && N >= 128 && sizeof(TAcc) <= 4)
     return run_tiled<TIn, TAcc, 128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
   if (M >= 64 && N >= 64)

@@ -55,7 +55,7 @@ struct Checkpoints {
 };
 
 constexpr int kMeanThreads = 256;
-constexpr int kMeanBlocks = 64;
+constexpr int kMeanBlocks = 148 * 4;  // enough CTAs to stream G*N^2 elements at HBM rate
 
 template <class T>
 __global__ void __launch_bounds__(kMeanThreads) running_mean_kernel(

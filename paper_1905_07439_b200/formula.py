@@ -173,11 +173,29 @@ def perturb_all(f: BilinearFormula, sigma: float, rng) -> BilinearFormula:
     return BilinearFormula(f.u + noise[0], f.v + noise[1], f.w + noise[2])
 
 
+_KAPPA_CACHE: dict = {}
+
+
 def kappa(f: BilinearFormula) -> float:
     """n^-3 * sum_(i,j,l) (1 - sum_r u[r,i,l] v[r,l,j] w[r,i,j]), accumulated
     sequentially in binary64, (i, j, l) lexicographic, r innermost
     (formula.py:176-194).  The order is part of the contract: the rescale
-    factor 1/(1-kappa) must round exactly as the reference's does."""
+    factor 1/(1-kappa) must round exactly as the reference's does.
+
+    Formulas are immutable, so the value is memoised by coefficient bytes
+    (the reference recomputes it for every hatted table)."""
+    key = (f.u.shape, f.u.tobytes(), f.v.tobytes(), f.w.tobytes())
+    hit = _KAPPA_CACHE.get(key)
+    if hit is not None:
+        return hit
+    val = _kappa_sequential(f)
+    if len(_KAPPA_CACHE) > 256:
+        _KAPPA_CACHE.clear()
+    _KAPPA_CACHE[key] = val
+    return val
+
+
+def _kappa_sequential(f: BilinearFormula) -> float:
     u = f.u.tolist()
     v = f.v.tolist()
     w = f.w.tolist()

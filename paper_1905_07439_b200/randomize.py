@@ -164,8 +164,22 @@ def plan_levels(f: BilinearFormula, plans, mode):
     """(T, R, n, n) coefficient triple for one recursion level of T plans,
     rounded into the mode (randomize.py:199-209)."""
     m = mode_of(mode)
-    triples = [hatted_tensors(f, p) for p in plans]
-    return tuple(np.stack([m.array(t[k]) for t in triples]) for k in range(3))
+    plans = list(plans)
+    if any(p.n != f.n for p in plans):
+        raise ValueError("plan and formula grid sizes differ")
+    # batched form of hatted_tensors (same operations: exact sign flips and
+    # index gathers, then one binary64 multiply of wh by 1/(1-kappa))
+    S = np.stack([p.signs for p in plans])            # (T, 3, n)
+    P = np.stack([p.perms for p in plans])            # (T, 3, n)
+    c = _rescale_factor(f)
+
+    def hat(t, a, b):
+        g = t[:, P[:, a][:, :, None], P[:, b][:, None, :]]  # (R, T, n, n)
+        g = np.moveaxis(g, 0, 1)                             # (T, R, n, n)
+        return g * (S[:, a][:, :, None] * S[:, b][:, None, :])[:, None]
+
+    uh, vh, wh = hat(f.u, 0, 1), hat(f.v, 1, 2), hat(f.w, 0, 2) * c
+    return m.array(uh), m.array(vh), m.array(wh)
 
 
 _plan_level_alias = plan_levels  # reference name: _plan_levels

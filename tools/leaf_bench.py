@@ -27,7 +27,10 @@ TORCH = {0: torch.float64, 1: torch.float32, 2: torch.float16}
 def main():
     lib = _lib.load()
     tiles = (sys.argv[sys.argv.index("--tiles") + 1].split(",") if "--tiles" in sys.argv else ["0"])
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     for label, di, do, batch, m in CASES:
+        if only and only not in label:
+            continue
         x = torch.randn(batch, m, m, device="cuda").to(TORCH[di])
         y = torch.randn(batch, m, m, device="cuda").to(TORCH[di])
         out = torch.empty(batch, m, m, device="cuda", dtype=TORCH[do])
