@@ -145,6 +145,12 @@ size_t rbc_rel_errors_scratch_bytes(int64_t T);
 int rbc_rel_errors_async(int dtype, int64_t T, int64_t N, const void* c, const double* ref,
                          int64_t ref_tstride, double* err, void* scratch, void* stream);
 
+/* total[e] = fl(...fl(total[e] + x[0][e]) ... + x[T-1][e]) in binary64, trials in
+ * order: the sequential average accumulation of enumerate_expectation
+ * (randomize.py:317-326) and the averaging experiments (experiments.py:382-383). */
+int rbc_sum_trials_async(int dtype, int64_t T, int64_t N, const void* x, double* total,
+                         void* stream);
+
 /* nonfinite[t] = 1 if x[t] (N*N elements) holds a non-finite value. */
 int rbc_nonfinite_async(int dtype, int64_t T, int64_t N, const void* x, uint8_t* nonfinite,
                         void* stream);

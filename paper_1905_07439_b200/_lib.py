@@ -49,6 +49,7 @@ EXPORTS = (
     "rbc_error_trials_async",
     "rbc_average_trials_workspace_bytes",
     "rbc_average_trials_async",
+    "rbc_sum_trials_async",
 )
 
 _lock = threading.Lock()
@@ -100,6 +101,7 @@ def _declare(lib):
         "rbc_rel_errors_scratch_bytes": (c_size, [c_i64]),
         "rbc_rel_errors_async": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
         "rbc_nonfinite_async": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp]),
+        "rbc_sum_trials_async": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp]),
         "rbc_error_trials": (
             c_int,
             [c_int, c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp],

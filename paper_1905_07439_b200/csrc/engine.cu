@@ -573,6 +573,14 @@ int rbc_rel_errors_async(int dtype, int64_t T, int64_t N, const void* c, const d
   return RBC_OK;
 }
 
+int rbc_sum_trials_async(int dtype, int64_t T, int64_t N, const void* x, double* total,
+                         void* stream) {
+  if (T == 0 || N == 0) return RBC_OK;
+  cudaError_t e = launch_sum_trials(dtype, T, N * N, x, total, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail_cuda(e, "sum_trials", __FILE__, __LINE__);
+  return RBC_OK;
+}
+
 int rbc_nonfinite_async(int dtype, int64_t T, int64_t N, const void* x, uint8_t* nonfinite,
                         void* stream) {
   if (T == 0) return RBC_OK;

@@ -108,7 +108,35 @@ cudaError_t nonfinite_t(int64_t ntr, int64_t N2, const void* x, uint8_t* flags, 
   return cudaGetLastError();
 }
 
+// total[e] = fl(...fl(total[e] + widen(x[0][e])) + ... + widen(x[T-1][e])):
+// the sequential binary64 accumulation of enumerate_expectation
+// (reference randomize.py:317-326) / _run_average (experiments.py:382-383).
+template <class T>
+__global__ void __launch_bounds__(kThreads) sum_trials_kernel(int64_t ntr, int64_t N2,
+                                                              const T* __restrict__ x,
+                                                              double* __restrict__ total) {
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < N2;
+       e += (int64_t)gridDim.x * kThreads) {
+    double acc = total[e];
+    for (int64_t t = 0; t < ntr; ++t) acc = __dadd_rn(acc, Arith<T>::widen(x[t * N2 + e]));
+    total[e] = acc;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_sum_trials(int dtype, int64_t ntr, int64_t N2, const void* x, double* total,
+                              cudaStream_t st) {
+  int64_t blocks = (N2 + kThreads - 1) / kThreads;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  switch (dtype) {
+    case kF64: sum_trials_kernel<double><<<(unsigned)blocks, kThreads, 0, st>>>(ntr, N2, (const double*)x, total); break;
+    case kF32: sum_trials_kernel<float><<<(unsigned)blocks, kThreads, 0, st>>>(ntr, N2, (const float*)x, total); break;
+    case kF16: sum_trials_kernel<__half><<<(unsigned)blocks, kThreads, 0, st>>>(ntr, N2, (const __half*)x, total); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 
 size_t error_scratch_bytes(int64_t ntr) { return (size_t)ntr * kBlocksPerTrial * 2 * sizeof(double); }
 

@@ -90,6 +90,10 @@ size_t error_scratch_bytes(int64_t T);
 cudaError_t launch_rel_errors(int dtype, int64_t T, int64_t N2, const void* c, const double* ref,
                               int64_t ref_tstride, double* err, void* scratch, cudaStream_t st);
 
+// total[e] += x[0][e] + ... + x[ntr-1][e], sequentially in binary64.
+cudaError_t launch_sum_trials(int dtype, int64_t ntr, int64_t N2, const void* x, double* total,
+                              cudaStream_t st);
+
 // Set nonfinite[t] = 1 when any element of x[t] (N2 elements) is non-finite.
 cudaError_t launch_nonfinite(int dtype, int64_t T, int64_t N2, const void* x, uint8_t* flags,
                              cudaStream_t st);

@@ -24,12 +24,21 @@ namespace rbc {
 int set_error_public(int code, const char* msg);
 }
 
+#define CUDA_TRY(expr)                                                             \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) return ::rbc::fail_cuda(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+
 namespace {
 
 size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// Per chunk: the binary64 truth, then one "lane" per product (deterministic,
+// randomized) with its own product buffer, error scratch and engine
+// workspace, so the three can run concurrently on forked streams.
 struct Layout {
-  size_t ref, prod, scratch, engine, total;
+  size_t ref, prod, scratch, engine, lane, total;
 };
 
 Layout layout_for(int dtype, int formula, int Q, int64_t chunk, int64_t N) {
@@ -39,8 +48,36 @@ Layout layout_for(int dtype, int formula, int Q, int64_t chunk, int64_t N) {
   L.prod = a256((size_t)chunk * N2 * rbc::dtype_size(dtype));
   L.scratch = a256(rbc::error_scratch_bytes(chunk));
   L.engine = a256(rbc_plans_workspace_bytes(dtype, formula, Q, chunk, N));
-  L.total = L.ref + L.prod + L.scratch + L.engine;
+  L.lane = L.prod + L.scratch + L.engine;
+  L.total = L.ref + 2 * L.lane;
   return L;
+}
+
+// Auxiliary streams (truth, deterministic lane, randomized lane) of the
+// current device, created once.  Work is forked from and joined back into
+// the caller's stream with events, so the whole pass stays stream ordered
+// (and graph capturable).
+struct AuxStreams {
+  cudaStream_t s[3];
+  cudaEvent_t fork, join[3], truth_done, lane_done[2];
+};
+
+AuxStreams* aux_streams() {
+  static AuxStreams* per_dev[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!per_dev[dev]) {
+    AuxStreams* a = new AuxStreams;
+    for (int i = 0; i < 3; ++i) {
+      cudaStreamCreateWithFlags(&a->s[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&a->join[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&a->fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&a->truth_done, cudaEventDisableTiming);
+    for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&a->lane_done[i], cudaEventDisableTiming);
+    per_dev[dev] = a;
+  }
+  return per_dev[dev];
 }
 
 }  // namespace
@@ -138,37 +175,55 @@ int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, 
     return set_error_public(RBC_EVALUE, "workspace too small for one trial");
   char* base = (char*)workspace;
   double* ref = (double*)base;
-  void* prod = base + L.ref;
-  void* scratch = base + L.ref + L.prod;
-  void* eng = base + L.ref + L.prod + L.scratch;
   const size_t es = dtype_size(dtype);
   const int64_t N2 = N * N;
+  AuxStreams* ax = aux_streams();
+  cudaStream_t s_truth = ax->s[0];
+  CUDA_TRY(cudaEventRecord(ax->fork, st));
+  for (int i = 0; i < 3; ++i) CUDA_TRY(cudaStreamWaitEvent(ax->s[i], ax->fork, 0));
   for (int64_t t0 = 0; t0 < T; t0 += chunk) {
     const int64_t nt = std::min(chunk, T - t0);
     const char* at = (const char*)a + (size_t)t0 * N2 * es;
     const char* bt = (const char*)b + (size_t)t0 * N2 * es;
     cudaError_t e;
+    if (t0 > 0)  // ref is reused: the previous chunk's error kernels must be done
+      for (int w = 0; w < 2; ++w) CUDA_TRY(cudaStreamWaitEvent(s_truth, ax->lane_done[w], 0));
     {
-      Stage stage(st, "truth_f64", (double)nt * N2 * (2.0 * es + 8.0), 2.0 * nt * (double)N2 * N);
-      e = launch_leaf(dtype, kF64, nt, N, N, N, at, N2, bt, N2, ref, st);
+      Stage stage(s_truth, "truth_f64", (double)nt * N2 * (2.0 * es + 8.0), 2.0 * nt * (double)N2 * N);
+      e = launch_leaf(dtype, kF64, nt, N, N, N, at, N2, bt, N2, ref, s_truth);
     }
     if (e != cudaSuccess) return fail_cuda(e, "truth", __FILE__, __LINE__);
+    CUDA_TRY(cudaEventRecord(ax->truth_done, s_truth));
     for (int which = 0; which < 2; ++which) {
+      cudaStream_t ls = ax->s[1 + which];
+      char* lane = base + L.ref + (size_t)which * L.lane;
+      void* prod = lane;
+      void* scratch = lane + L.prod;
+      void* eng = lane + L.prod + L.scratch;
       const void* plans = which == 0 ? det_plans : rand_plans;
-      if (!plans) continue;
+      if (!plans) {
+        CUDA_TRY(cudaEventRecord(ax->lane_done[which], ls));
+        continue;
+      }
       double* err = which == 0 ? err_det : err_rand;
       uint8_t* nf = which == 0 ? nf_det : nf_rand;
       const int64_t Tp = which == 0 ? 1 : nt;
       const void* pl = which == 0 ? plans : (const char*)plans + (size_t)t0 * Q * RBC_PLAN_BYTES;
       int rc = rbc_apply_plans_async(dtype, formula, Q, Tp, pl, nt, N, at, bt, nt, prod,
-                                     nf ? nf + t0 : nullptr, eng, L.engine, stream);
+                                     nf ? nf + t0 : nullptr, eng, L.engine, ls);
       if (rc != RBC_OK) return rc;
+      CUDA_TRY(cudaStreamWaitEvent(ls, ax->truth_done, 0));
       if (err) {
-        Stage stage(st, "rel_errors", (double)nt * N2 * (es + 8.0), 3.0 * nt * (double)N2);
-        e = launch_rel_errors(dtype, nt, N2, prod, ref, N2, err + t0, scratch, st);
+        Stage stage(ls, "rel_errors", (double)nt * N2 * (es + 8.0), 3.0 * nt * (double)N2);
+        e = launch_rel_errors(dtype, nt, N2, prod, ref, N2, err + t0, scratch, ls);
         if (e != cudaSuccess) return fail_cuda(e, "rel_errors", __FILE__, __LINE__);
       }
+      CUDA_TRY(cudaEventRecord(ax->lane_done[which], ls));
     }
+  }
+  for (int i = 0; i < 3; ++i) {
+    CUDA_TRY(cudaEventRecord(ax->join[i], ax->s[i]));
+    CUDA_TRY(cudaStreamWaitEvent(st, ax->join[i], 0));
   }
   return RBC_OK;
 }

@@ -180,6 +180,61 @@ def apply_plans(formula_id: int, Q: int, packed: np.ndarray, a, b, mode, stats=N
     return (out, flags[:T].astype(bool)) if return_flags else out
 
 
+def _vp(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class DeviceEngine:
+    """Device-resident twin of apply_levels / apply_plans over torch CUDA
+    tensors and one stream (no host copies, no synchronisation)."""
+
+    def __init__(self, mode, device="cuda:0", stream=None):
+        import torch
+
+        self.torch = torch
+        self.m = mode_of(mode)
+        self.code = dtype_code(self.m)
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._ws = None
+
+    def _workspace(self, nbytes):
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = self.torch.empty(max(int(nbytes), 1), dtype=self.torch.uint8, device=self.device)
+        return self._ws
+
+    def apply_plans(self, fid, Q, packed, a, b, out, nonfinite):
+        """packed (Tp, Q, 40) uint8, a/b (T0, N, N), out (T, N, N), nonfinite (T,) uint8."""
+        T, N = out.shape[0], out.shape[-1]
+        lib = _lib.load()
+        ws = self._workspace(lib.rbc_plans_workspace_bytes(self.code, fid, Q, T, N))
+        rc = lib.rbc_apply_plans_async(
+            self.code, fid, Q, packed.shape[0], _vp(packed), a.shape[0], N, _vp(a), _vp(b), T,
+            _vp(out), _vp(nonfinite), _vp(ws), ws.numel(), ctypes.c_void_p(self.stream.cuda_stream))
+        _lib.check(rc)
+
+    def apply_levels(self, levels, a, b, out, nonfinite):
+        """levels: Q device triples (Tc, R, n, n)."""
+        Q = len(levels)
+        T, N = out.shape[0], out.shape[-1]
+        n_arr = (ctypes.c_int32 * Q)(*[lv[0].shape[2] for lv in levels])
+        R_arr = (ctypes.c_int32 * Q)(*[lv[0].shape[1] for lv in levels])
+        Tc = (ctypes.c_int64 * Q)(*[lv[0].shape[0] for lv in levels])
+        ptrs = [(ctypes.c_void_p * Q)(*[lv[k].data_ptr() for lv in levels]) for k in range(3)]
+        lib = _lib.load()
+        ws = self._workspace(lib.rbc_levels_workspace_bytes(self.code, Q, n_arr, R_arr, T, N))
+        rc = lib.rbc_apply_levels_async(
+            self.code, Q, n_arr, R_arr, Tc, ptrs[0], ptrs[1], ptrs[2], a.shape[0], N, _vp(a), _vp(b),
+            T, _vp(out), _vp(nonfinite), _vp(ws), ws.numel(), ctypes.c_void_p(self.stream.cuda_stream))
+        _lib.check(rc)
+
+    def sum_trials(self, x, total):
+        """total (N*N,) float64 += x[0] + ... + x[T-1], sequentially."""
+        rc = _lib.load().rbc_sum_trials_async(self.code, x.shape[0], x.shape[-1], _vp(x), _vp(total),
+                                              ctypes.c_void_p(self.stream.cuda_stream))
+        _lib.check(rc)
+
+
 _saved = {}
 
 

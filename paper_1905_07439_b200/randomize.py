@@ -230,6 +230,86 @@ def _run(f, rplans, A, B, mode, stats):
     return engine.apply_levels(levels, A[None], B[None], mode, stats)
 
 
+def plan_count(n: int) -> int:
+    """Number of distinct plans (2^n)^3 (n!)^3 (randomize.py:277-279)."""
+    import math
+
+    return (2 ** n) ** 3 * math.factorial(n) ** 3
+
+
+def _all_plans(n: int):
+    """Every plan, signs lexicographic with +1 first, permutations in
+    itertools order (randomize.py:282-290)."""
+    import itertools
+
+    sign_rows = list(itertools.product((1.0, -1.0), repeat=n))
+    perm_rows = list(itertools.permutations(range(n)))
+    for s1, s2, s3, p1, p2, p3 in itertools.product(
+        sign_rows, sign_rows, sign_rows, perm_rows, perm_rows, perm_rows
+    ):
+        yield RandomizationPlan(np.array([s1, s2, s3]), np.array([p1, p2, p3]))
+
+
+def enumerate_expectation(f, A, B, mode=DOUBLE, chunk_elements: int = DEFAULT_CHUNK_ELEMENTS,
+                          device="cuda:0") -> np.ndarray:
+    """Exact expectation of the single-level randomized product over every
+    plan (randomize.py:293-334), on the device: plans are evaluated in
+    batches and accumulated sequentially in binary64 in enumeration order;
+    the average is total / count.  ``chunk_elements`` bounds the batch the
+    same way as the reference (values never depend on it)."""
+    import torch
+
+    from .multiply import _as_operands, _check_blocked
+
+    count = plan_count(f.n)
+    if count > 1_000_000:
+        raise ValueError(f"{count} plans exceed the enumeration budget")
+    m = mode_of(mode)
+    A, B = _as_operands(A, B, m)
+    _check_blocked(A, B, f.n, 1)
+    _rescale_factor(f)
+    N = A.shape[0]
+    per_trial = max(1, N * N * f.rank // (f.n * f.n))
+    chunk = max(1, int(chunk_elements) // per_trial)
+    eng = engine.DeviceEngine(m, device=device)
+    dev = eng.device
+    a = torch.from_numpy(np.ascontiguousarray(A)[None]).to(dev)
+    b = torch.from_numpy(np.ascontiguousarray(B)[None]).to(dev)
+    total = torch.zeros(N * N, dtype=torch.float64, device=dev)
+    fid = plan_formula_id(f)
+    tdt = {np.float64: torch.float64, np.float32: torch.float32, np.float16: torch.float16}[m.dtype]
+    done = 0
+    batch = []
+
+    def flush():
+        nonlocal done
+        if not batch:
+            return
+        T = len(batch)
+        out = torch.empty((T, N, N), dtype=tdt, device=dev)
+        nf = torch.zeros(T, dtype=torch.uint8, device=dev)
+        if fid is not None:
+            packed = pack_recursive_plans([RecursivePlan((p,)) for p in batch], 1, f.n)
+            eng.apply_plans(fid, 1, torch.from_numpy(packed).to(dev), a, b, out, nf)
+        else:
+            lv = [tuple(torch.from_numpy(t).to(dev) for t in plan_levels(f, batch, m))]
+            eng.apply_levels(lv, a, b, out, nf)
+        if bool(nf.any()):
+            raise OverflowError(f"result left the {m.kind} range")
+        eng.sum_trials(out, total)
+        done += T
+        batch.clear()
+
+    for plan in _all_plans(f.n):
+        batch.append(plan)
+        if len(batch) >= chunk:
+            flush()
+    flush()
+    assert done == count
+    torch.cuda.synchronize(dev)
+    return total.cpu().numpy().reshape(N, N) / float(count)
+
+
 def randomized_apply(f, plan, A, B, mode=DOUBLE, stats=None) -> np.ndarray:
     A, B = _as_operands(A, B, mode)
     _check_blocked(A, B, f.n, 1)

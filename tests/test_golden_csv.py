@@ -110,12 +110,17 @@ def test_golden_rows_gpu(kind):
     std = standard_multiply(Am, Bm, SINGLE)
     assert frob(std.astype(np.float64) - ref) / refnorm == pytest.approx(
         rows[(kind, "standard", 0)][0], rel=RTOL)
+    from paper_1905_07439_b200.rescale import DEFAULT_SCHEDULE, rescaled_multiply
+
     checked = 1
     for Q in range(1, 6):
         det = recursive_apply(f, Am, Bm, Q, SINGLE)
         assert frob(det.astype(np.float64) - ref) / refnorm == pytest.approx(
             rows[(kind, "deterministic", Q)][0], rel=RTOL)
-        checked += 1
+        resc = rescaled_multiply(Am, Bm, Q, DEFAULT_SCHEDULE, SINGLE)
+        assert frob(resc.astype(np.float64) - ref) / refnorm == pytest.approx(
+            rows[(kind, "rescaled_2xoi", Q)][0], rel=RTOL)
+        checked += 2
         for alg, var in VARIANT.items():
             rplans = trial_plans(Q, range(1, 101), var)
             C = recursive_randomized_apply_many(f, rplans, Am, Bm, SINGLE)
@@ -123,4 +128,4 @@ def test_golden_rows_gpu(kind):
             want = [rows[(kind, alg, Q)][t] for t in range(1, 101)]
             np.testing.assert_allclose(got, want, rtol=RTOL, atol=0)
             checked += 100
-    assert checked == 1 + 5 * 301
+    assert checked == 1 + 5 * 302
