@@ -16,6 +16,8 @@
 // Shared memory: for l = 1..L, X_l and Y_l (R^l blocks of (s0/n^l)^2), plus
 // the leaf products P_L (R^L M^2).  Contractions reuse the dead X_l buffers.
 
+#include <cstdlib>
+
 #include "kernels.h"
 #include "plan_ops.cuh"
 
@@ -96,8 +98,8 @@ __device__ __forceinline__ void expand_stage(const GatherTab<F::n>& gt_sm, const
   }
 }
 
-template <class F, class T, int L, int M>
-__global__ void __launch_bounds__(kThreads) subtree_kernel(
+template <class F, class T, int L, int M, int NT>
+__global__ void __launch_bounds__(NT) subtree_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0,
     T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
     int64_t ntr, uint8_t* __restrict__ nonfinite) {
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(kThreads) subtree_kernel(
   constexpr int n = F::n;
   constexpr int R = F::R;
   constexpr int s0 = S::s0;
+  constexpr int kThreads = NT;
   constexpr int kHalf = kThreads / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
@@ -119,7 +122,12 @@ __global__ void __launch_bounds__(kThreads) subtree_kernel(
 
   for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
     __syncthreads();  // previous trial's readers of spl / sm are done
-    if (threadIdx.x < L) spl[threadIdx.x] = plans[t * plan_tstride + q0 + threadIdx.x];
+    {
+      // the L plan records q0 .. q0+L-1 are contiguous: copy them as words
+      constexpr int kWords = (int)(sizeof(PlanLevel) / 4) * L;
+      const int* src = reinterpret_cast<const int*>(plans + t * plan_tstride + q0);
+      if (threadIdx.x < kWords) reinterpret_cast<int*>(spl)[threadIdx.x] = src[threadIdx.x];
+    }
     __syncthreads();
     // one thread per (level, table): X gather, Y gather, contraction scatter
     if (threadIdx.x < 3 * L) {
@@ -231,19 +239,209 @@ __global__ void __launch_bounds__(kThreads) subtree_kernel(
   }
 }
 
+// ---- warp-specialised two-level subtree ------------------------------------
+// Same arithmetic as subtree_kernel<F, T, 2, M>, other schedule: the top
+// expansion (level q0 -> q0+1) and the last contraction run CTA-wide, but
+// everything below a level-(q0+1) block -- its R children, their R leaf
+// products and its contraction -- is done by one warp on its own shared
+// scratch, synchronised with __syncwarp only.  Each warp takes G level-1
+// blocks at a time, so the CTA-wide barriers that dominated the stalls of
+// the stage-synchronous kernel disappear from the inner levels.
+template <class F, class T, int M, int G>
+struct Subtree2W {
+  static constexpr int n = F::n;
+  static constexpr int R = F::R;
+  static constexpr int s1 = M * n;
+  static constexpr int s0 = s1 * n;
+  static constexpr int kids1 = s1 * s1;
+  static constexpr int leafE = M * M;
+  static constexpr int scratch = 2 * G * R * leafE;  // per warp: X2 and Y2 of G blocks
+  static constexpr size_t header() {
+    return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 6 * sizeof(GatherTab<n>);
+  }
+  static constexpr size_t smem_bytes(int warps) {
+    return header() + sizeof(T) * ((size_t)2 * R * kids1 + (size_t)warps * scratch);
+  }
+};
+
+template <class F, class T, int M, int G, int NT>
+__global__ void __launch_bounds__(NT, 4) subtree2w_kernel(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0,
+    T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
+    int64_t ntr, uint8_t* __restrict__ nonfinite) {
+  using S = Subtree2W<F, T, M, G>;
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  constexpr int s0 = S::s0, s1 = S::s1, kids1 = S::kids1, leafE = S::leafE;
+  constexpr int NW = NT / 32;
+  constexpr int kHalf = NT / 2;
+  using A = Arith<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
+  GatherTab<n>* tabs =
+      reinterpret_cast<GatherTab<n>*>(smem_raw + ((sizeof(PlanLevel) * 2 + 15) / 16) * 16);
+  T* X1 = reinterpret_cast<T*>(smem_raw + S::header());
+  T* Y1 = X1 + R * kids1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* X2 = Y1 + R * kids1 + warp * S::scratch;
+  T* Y2 = X2 + G * R * leafE;
+  const int k0 = blockIdx.x;
+  const int which = threadIdx.x >= kHalf;
+  const int lt = threadIdx.x - which * kHalf;
+
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    __syncthreads();
+    {
+      constexpr int kWords = (int)(sizeof(PlanLevel) / 4) * 2;
+      const int* src = reinterpret_cast<const int*>(plans + t * plan_tstride + q0);
+      if (threadIdx.x < kWords) reinterpret_cast<int*>(spl)[threadIdx.x] = src[threadIdx.x];
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      const int l = threadIdx.x / 3, kind = threadIdx.x - 3 * (threadIdx.x / 3);
+      const int sp = l == 0 ? s0 : s1;
+      GatherTab<n> tab;
+      if (kind == 0)
+        make_gather<n, 0>(spl[l], sp, tab);
+      else if (kind == 1)
+        make_gather<n, 1>(spl[l], sp, tab);
+      else
+        make_scatter<n>(spl[l], sp / n, tab);
+      tabs[threadIdx.x] = tab;
+    }
+    __syncthreads();
+
+    // ---- level q0 -> q0+1, CTA-wide (A on the first half, B on the second)
+    {
+      const T* src = (which ? y : x) + t * xy_tstride + (int64_t)k0 * s0 * s0;
+      T* dst = which ? Y1 : X1;
+      const GatherTab<n> gt = tabs[which];
+      for (int e = lt; e < kids1; e += kHalf) {
+        const int i = e / s1, j = e - (e / s1) * s1;
+        if (which)
+          expand_tab<F, T, 1, 1>(src + i * s0 + j, gt, dst + i * s1 + j, kids1);
+        else
+          expand_tab<F, T, 1, 0>(src + i * s0 + j, gt, dst + i * s1 + j, kids1);
+      }
+    }
+    __syncthreads();
+
+    // ---- per warp: G level-(q0+1) blocks at a time, everything below them
+    {
+      const GatherTab<n> gx = tabs[3], gy = tabs[4], sc1 = tabs[5];
+      for (int b = warp; b * G < R; b += NW) {
+        const int k1a = b * G;
+        const int nk = R - k1a < G ? R - k1a : G;
+        const int items = nk * leafE;
+        for (int e = lane; e < items; e += 32) {
+          const int pos = e / nk, kl = e - (e / nk) * nk;
+          const int i = pos / M, j = pos - (pos / M) * M;
+          expand_tab<F, T, 1, 0>(X1 + (k1a + kl) * kids1 + i * s1 + j, gx,
+                                 X2 + kl * R * leafE + pos, leafE);
+        }
+        for (int e = lane; e < items; e += 32) {
+          const int pos = e / nk, kl = e - (e / nk) * nk;
+          const int i = pos / M, j = pos - (pos / M) * M;
+          expand_tab<F, T, 1, 1>(Y1 + (k1a + kl) * kids1 + i * s1 + j, gy,
+                                 Y2 + kl * R * leafE + pos, leafE);
+        }
+        __syncwarp();
+        // leaf products in place over X2 (one lane per leaf)
+        for (int lf = lane; lf < nk * R; lf += 32) {
+          T xa[leafE], yb[leafE];
+#pragma unroll
+          for (int q = 0; q < leafE; ++q) {
+            xa[q] = X2[lf * leafE + q];
+            yb[q] = Y2[lf * leafE + q];
+          }
+#pragma unroll
+          for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+              T acc = A::mul(xa[i * M], yb[j]);
+#pragma unroll
+              for (int k = 1; k < M; ++k) acc = A::add(acc, A::mul(xa[i * M + k], yb[k * M + j]));
+              X2[lf * leafE + i * M + j] = acc;
+            }
+        }
+        __syncwarp();
+        // contraction into the block's (now dead) X1 slot
+        for (int e = lane; e < items; e += 32) {
+          const int pos = e / nk, kl = e - (e / nk) * nk;
+          const int i = pos / M, j = pos - (pos / M) * M;
+          contract_tab<F, T, 1, false>(X2 + kl * R * leafE + pos, leafE,
+                                       X1 + (k1a + kl) * kids1 + i * s1 + j, sc1);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+
+    // ---- level q0+1 -> q0, CTA-wide, to HBM
+    bool ok = true;
+    {
+      const GatherTab<n> sc0 = tabs[2];
+      T* dbase = out + (t * K0 + k0) * (int64_t)s0 * s0;
+      for (int e = threadIdx.x; e < kids1; e += NT) {
+        const int i = e / s1, j = e - (e / s1) * s1;
+        if (nonfinite)
+          ok = contract_tab<F, T, 1, true>(X1 + i * s1 + j, kids1, dbase + i * s0 + j, sc0) && ok;
+        else
+          contract_tab<F, T, 1, false>(X1 + i * s1 + j, kids1, dbase + i * s0 + j, sc0);
+      }
+    }
+    if (nonfinite && !ok) nonfinite[t] = 1;
+  }
+}
+
+template <class F, class T, int M, int G>
+cudaError_t launch_subtree2w(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
+                             void* out, const PlanLevel* plans, int64_t pts, int q0, int64_t ntr,
+                             uint8_t* nonfinite, cudaStream_t st) {
+  constexpr int NT = 256;
+  using S = Subtree2W<F, T, M, G>;
+  const size_t smem = S::smem_bytes(NT / 32);
+  auto kern = subtree2w_kernel<F, T, M, G, NT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)K0, (unsigned)(ntr < 65535 ? ntr : 65535));
+  kern<<<grid, NT, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, (T*)out, plans, pts,
+                               q0, ntr, nonfinite);
+  return cudaGetLastError();
+}
+
 template <class F, class T, int L, int M>
 cudaError_t launch_subtree_t(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
                              void* out, const PlanLevel* plans, int64_t pts, int q0, int64_t ntr,
                              uint8_t* nonfinite, cudaStream_t st) {
   using S = Subtree<F, T, L, M>;
   const size_t smem = S::smem_bytes();
-  auto kern = subtree_kernel<F, T, L, M>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)K0, (unsigned)(ntr < 65535 ? ntr : 65535));
-  kern<<<grid, kThreads, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, (T*)out, plans,
-                                     pts, q0, ntr, nonfinite);
-  return cudaGetLastError();
+  // RBC_SUBTREE_THREADS=<128|256|512> overrides the CTA size (tuning aid)
+  static const int forced = [] {
+    const char* v = getenv("RBC_SUBTREE_THREADS");
+    return v ? atoi(v) : 0;
+  }();
+  auto launch = [&](auto kern, int nt) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)K0, (unsigned)(ntr < 65535 ? ntr : 65535));
+    kern<<<grid, nt, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, (T*)out, plans,
+                                 pts, q0, ntr, nonfinite);
+    return cudaGetLastError();
+  };
+  // warp-specialised variant for two fused levels (RBC_SUBTREE_WARP=1; measured
+  // slower on config 2 -- 8.4 vs 7.5 ms per launch -- so not the default)
+  if constexpr (L == 2) {
+    static const int mode = [] {
+      const char* v = getenv("RBC_SUBTREE_WARP");
+      return v ? atoi(v) : 0;
+    }();
+    if (mode)
+      return launch_subtree2w<F, T, M, 3>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
+  }
+  if (forced == 128) return launch(subtree_kernel<F, T, L, M, 128>, 128);
+  if (forced == 512) return launch(subtree_kernel<F, T, L, M, 512>, 512);
+  return launch(subtree_kernel<F, T, L, M, 256>, 256);
 }
 
 // Table of instantiated (formula, L, M) shapes.
