@@ -91,6 +91,75 @@ def dist_env():
     return world, rank, local
 
 
+class NvmlClocks:
+    """NVML poller (5 ms) across the timed region: SM clock samples and the
+    clock-event (throttle) reasons seen; falls back to nvidia-smi."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
+
+    def __init__(self, index: int):
+        import threading
+
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [v for v in vis.split(",") if v.strip()]
+            if index < len(ids) and ids[index].strip().isdigit():
+                index = int(ids[index])
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.samples, self.mask = [], 0
+        self.stop_ev = threading.Event()
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+
+    def _reasons(self):
+        nv = self.nv
+        for name in ("nvmlDeviceGetCurrentClocksEventReasons", "nvmlDeviceGetCurrentClocksThrottleReasons"):
+            fn = getattr(nv, name, None)
+            if fn is not None:
+                try:
+                    return int(fn(self.h))
+                except Exception:  # noqa: BLE001
+                    continue
+        return 0
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.mask |= self._reasons()
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        self.thread.start()
+
+    def stop(self):
+        self.stop_ev.set()
+        self.thread.join(timeout=5)
+        reasons = sorted(v for k, v in self.REASONS.items() if self.mask & k)
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": reasons,
+            "samples": len(self.samples),
+            "source": "nvml 5 ms poll over the timed region",
+        }
+
+
+def make_clocks(index: int):
+    try:
+        return NvmlClocks(index)
+    except Exception:  # noqa: BLE001
+        return Clocks(index)
+
+
 class Clocks:
     """nvidia-smi sampler running across the timed region."""
 
@@ -451,12 +520,12 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
-    clocks = Clocks(local)
-    clocks.start()
     for _ in range(args.warmup):
         wl.run(stream)
     torch.cuda.synchronize()
     barrier()
+    clocks = make_clocks(local)
+    clocks.start()
     _lib.profile_enable(True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)

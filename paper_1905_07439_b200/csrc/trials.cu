@@ -177,10 +177,21 @@ int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, 
   double* ref = (double*)base;
   const size_t es = dtype_size(dtype);
   const int64_t N2 = N * N;
+  // Concurrent lanes unless the stage profiler is on (overlapping stages
+  // would blur its per-kernel durations) or RBC_SERIAL_LANES=1.
+  static const bool serial_env = [] {
+    const char* v = getenv("RBC_SERIAL_LANES");
+    return v && v[0] == '1';
+  }();
+  const bool conc = !prof_on() && !serial_env;
   AuxStreams* ax = aux_streams();
-  cudaStream_t s_truth = ax->s[0];
-  CUDA_TRY(cudaEventRecord(ax->fork, st));
-  for (int i = 0; i < 3; ++i) CUDA_TRY(cudaStreamWaitEvent(ax->s[i], ax->fork, 0));
+  cudaStream_t lanes[3] = {st, st, st};
+  if (conc) {
+    for (int i = 0; i < 3; ++i) lanes[i] = ax->s[i];
+    CUDA_TRY(cudaEventRecord(ax->fork, st));
+    for (int i = 0; i < 3; ++i) CUDA_TRY(cudaStreamWaitEvent(ax->s[i], ax->fork, 0));
+  }
+  cudaStream_t s_truth = lanes[0];
   for (int64_t t0 = 0; t0 < T; t0 += chunk) {
     const int64_t nt = std::min(chunk, T - t0);
     const char* at = (const char*)a + (size_t)t0 * N2 * es;
@@ -195,7 +206,7 @@ int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, 
     if (e != cudaSuccess) return fail_cuda(e, "truth", __FILE__, __LINE__);
     CUDA_TRY(cudaEventRecord(ax->truth_done, s_truth));
     for (int which = 0; which < 2; ++which) {
-      cudaStream_t ls = ax->s[1 + which];
+      cudaStream_t ls = lanes[1 + which];
       char* lane = base + L.ref + (size_t)which * L.lane;
       void* prod = lane;
       void* scratch = lane + L.prod;
@@ -221,9 +232,11 @@ int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, 
       CUDA_TRY(cudaEventRecord(ax->lane_done[which], ls));
     }
   }
-  for (int i = 0; i < 3; ++i) {
-    CUDA_TRY(cudaEventRecord(ax->join[i], ax->s[i]));
-    CUDA_TRY(cudaStreamWaitEvent(st, ax->join[i], 0));
+  if (conc) {
+    for (int i = 0; i < 3; ++i) {
+      CUDA_TRY(cudaEventRecord(ax->join[i], ax->s[i]));
+      CUDA_TRY(cudaStreamWaitEvent(st, ax->join[i], 0));
+    }
   }
   return RBC_OK;
 }
