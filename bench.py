@@ -232,7 +232,28 @@ def ncu_traffic(stage: str, config: str):
     return d.get(config, {}).get(stage)
 
 
-def roofline(prof: dict, config: str):
+def subtree_smem_bytes_per_launch(cfg, pairs: int) -> float:
+    """Algorithmic shared-memory bytes of one fused two-level subtree launch:
+    per CTA (level-q0 block, side s0 = M n^2, s1 = M n) the expansions write
+    and re-read R s1^2 + R^2 M^2 elements per operand, the leaves read both
+    operands and write the products, the contractions read and write back:
+    6 R s1^2 + 6 R^2 M^2 element accesses.  CTAs per launch: pairs x R^(Q-2)."""
+    import numpy as np
+
+    n, R, Q = cfg.n, cfg.rank, cfg.Q
+    M = cfg.N // n ** Q
+    s1 = M * n
+    e = np.dtype(cfg.mode.dtype).itemsize
+    per_cta = (6 * R * s1 * s1 + 6 * R * R * M * M) * e
+    return float(per_cta) * pairs * R ** (Q - 2)
+
+
+def smem_peak_gbs(sm_mhz):
+    """Nominal shared-memory bandwidth: 128 B/clk/SM x 148 SMs x SM clock."""
+    return 128.0 * 148 * (sm_mhz or 1965.0) * 1e6 / 1e9
+
+
+def roofline(prof: dict, config: str, cfg=None, pairs=None, sm_max_mhz=None):
     if not prof:
         return None
     stage, agg = max(prof.items(), key=lambda kv: kv[1]["ms"])
@@ -240,6 +261,25 @@ def roofline(prof: dict, config: str):
     per_launch_bytes = agg["bytes"] / agg["count"]
     per_launch_flops = agg["flops"] / agg["count"]
     total_ms = sum(v["ms"] for v in prof.values())
+    if stage == "subtree_fused" and cfg is not None:
+        # on-chip bound: report against shared-memory bandwidth; HBM view kept
+        smem_b = subtree_smem_bytes_per_launch(cfg, pairs)
+        achieved = smem_b / avg_s / 1e9
+        peak = smem_peak_gbs(sm_max_mhz)
+        hbm_peak, hbm_how = measured_peaks()
+        return {
+            "bound": "smem", "kernel": stage, "achieved": round(achieved, 2), "peak": round(peak, 2),
+            "peak_source": "nominal 128 B/clk/SM x 148 SMs x max SM clock", "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": ncu_traffic(stage, config),
+            "algorithmic_smem_bytes_per_launch": smem_b,
+            "algorithmic_bytes_per_launch": per_launch_bytes,
+            "hbm_view": {"achieved": round(per_launch_bytes / avg_s / 1e9, 2), "peak": hbm_peak,
+                         "peak_source": hbm_how,
+                         "frac": round(per_launch_bytes / avg_s / 1e9 / hbm_peak, 4)},
+            "algorithmic_flops_per_launch": per_launch_flops, "avg_launch_ms": round(avg_s * 1e3, 5),
+            "share_of_profiled_time": round(agg["ms"] / total_ms, 4) if total_ms else None,
+            "stages": {k: {"count": v["count"], "ms": round(v["ms"], 4)} for k, v in prof.items()},
+        }
     if stage.startswith(("leaf", "truth")):
         peaks, how = fp_peaks()
         key = {"leaf_f32": "f32_tflops", "leaf_f16": "f16_tflops"}.get(stage, "f64_tflops")
@@ -574,7 +614,7 @@ def run_ours(args):
         },
         "gpu_launches": launches,
         "clocks": clk,
-        "roofline": roofline(prof, cfg.name),
+        "roofline": roofline(prof, cfg.name, cfg, T, clk.get("sm_max_mhz")),
         "errors": distributed.trial_stats(allerr[0], alldet[0], allerr[1] > 0, alldet[1] > 0),
     }
     if hasattr(wl, "mean_errors"):
