@@ -43,6 +43,31 @@ template <> __device__ __forceinline__ float widen_to<__half, float>(__half v) {
   return __half2float(v);
 }
 
+// Multiply-add step acc <- fl(acc + fl(a*b)).  When the operands were widened
+// from a narrower type into binary64 (f32 or f16 -> f64: the binary64 truth),
+// a*b has at most 48 significant bits and is exact in binary64, so
+// fl(acc + fl(a*b)) == fl(acc + a*b) == fma(a, b, acc) bit for bit: one DFMA
+// replaces DMUL + DADD with identical results.  Same-type products are not
+// exact and keep the separately rounded multiply and add.
+template <class TIn, class TAcc>
+struct Mac {
+  static __device__ __forceinline__ TAcc step(TAcc acc, TAcc a, TAcc b) {
+    return Arith<TAcc>::add(acc, Arith<TAcc>::mul(a, b));
+  }
+};
+template <>
+struct Mac<float, double> {
+  static __device__ __forceinline__ double step(double acc, double a, double b) {
+    return __fma_rn(a, b, acc);
+  }
+};
+template <>
+struct Mac<__half, double> {
+  static __device__ __forceinline__ double step(double acc, double a, double b) {
+    return __fma_rn(a, b, acc);
+  }
+};
+
 template <class TIn, class TAcc>
 __global__ void __launch_bounds__(256) leaf_small_kernel(int64_t batch, int M, int K, int N,
                                                          const TIn* __restrict__ x, int64_t xs,
@@ -61,7 +86,7 @@ __global__ void __launch_bounds__(256) leaf_small_kernel(int64_t batch, int M, i
     const TIn* yc = y + b * ys + j;
     TAcc acc = A::mul(widen_to<TIn, TAcc>(xr[0]), widen_to<TIn, TAcc>(yc[0]));
     for (int k = 1; k < K; ++k)
-      acc = A::add(acc, A::mul(widen_to<TIn, TAcc>(xr[k]), widen_to<TIn, TAcc>(yc[(int64_t)k * N])));
+      acc = Mac<TIn, TAcc>::step(acc, widen_to<TIn, TAcc>(xr[k]), widen_to<TIn, TAcc>(yc[(int64_t)k * N]));
     out[idx] = acc;
   }
 }
@@ -159,7 +184,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 #pragma unroll
           for (int ii = 0; ii < TM; ++ii)
 #pragma unroll
-            for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = A::add(acc[ii][jj], A::mul(a[ii], bv[jj]));
+            for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = Mac<TIn, TAcc>::step(acc[ii][jj], a[ii], bv[jj]);
         }
       }
     }
@@ -227,7 +252,7 @@ __global__ void __launch_bounds__(256) leaf_smem_kernel(int64_t batch, const TIn
 #pragma unroll
     for (int i = 0; i < TR; ++i)
 #pragma unroll
-      for (int j = 0; j < TR; ++j) acc[i][j] = A::add(acc[i][j], A::mul(a[i], bb[j]));
+      for (int j = 0; j < TR; ++j) acc[i][j] = Mac<TIn, TAcc>::step(acc[i][j], a[i], bb[j]);
   }
   TAcc* o = out + (b0 + l) * (int64_t)M * M;
 #pragma unroll
@@ -463,6 +488,10 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
     return run_tiled<TIn, TAcc, 64, 64, 16, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
   if (forced == 204 && M >= 64 && N >= 64)
     return run_tiled<TIn, TAcc, 64, 64, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (forced == 207 && M >= 64 && N >= 128)
+    return run_tiled<TIn, TAcc, 64, 128, 16, 4, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+  if (forced == 208 && M >= 128 && N >= 128)
+    return run_tiled<TIn, TAcc, 128, 128, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
   if (forced == 206 && M >= 64 && N >= 64)
     return run_tiled<TIn, TAcc, 64, 64, 4, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
   if (forced == 128 && M >= 128 && N >= 128)

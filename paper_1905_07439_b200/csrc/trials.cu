@@ -68,8 +68,12 @@ AuxStreams* aux_streams() {
   cudaGetDevice(&dev);
   if (!per_dev[dev]) {
     AuxStreams* a = new AuxStreams;
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
     for (int i = 0; i < 3; ++i) {
-      cudaStreamCreateWithFlags(&a->s[i], cudaStreamNonBlocking);
+      // the truth lane (FP64 pipe) gets the highest priority so its CTAs
+      // interleave with the shared-memory-bound product kernels
+      cudaStreamCreateWithPriority(&a->s[i], cudaStreamNonBlocking, i == 0 ? hi : lo);
       cudaEventCreateWithFlags(&a->join[i], cudaEventDisableTiming);
     }
     cudaEventCreateWithFlags(&a->fork, cudaEventDisableTiming);

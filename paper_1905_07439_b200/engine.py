@@ -235,6 +235,29 @@ class DeviceEngine:
         _lib.check(rc)
 
 
+def truth(A, B, mode, device="cuda:0") -> np.ndarray:
+    """Binary64 inner-product truth of mode-typed operands (T, N, N) -> (T, N, N)
+    float64, k ascending (reference experiments.py:251-254 with
+    standard_multiply(Ad, Bd, DOUBLE)); C ABI rbc_truth_async."""
+    import torch
+
+    m = mode_of(mode)
+    A = np.ascontiguousarray(A, dtype=m.dtype)
+    B = np.ascontiguousarray(B, dtype=m.dtype)
+    if A.ndim != 3 or A.shape != B.shape or A.shape[1] != A.shape[2]:
+        raise ValueError("operands must be (T, N, N) stacks of equal square matrices")
+    T, N, _ = A.shape
+    dev = torch.device(device)
+    a = torch.from_numpy(A).to(dev)
+    b = torch.from_numpy(B).to(dev)
+    ref = torch.empty((T, N, N), dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream(dev)
+    rc = _lib.load().rbc_truth_async(dtype_code(m), T, N, _vp(a), _vp(b), _vp(ref),
+                                     ctypes.c_void_p(st.cuda_stream))
+    _lib.check(rc)
+    return ref.cpu().numpy()
+
+
 _saved = {}
 
 

@@ -53,6 +53,31 @@ def test_error_trials_match_oracle(name, N, Q, T):
         np.testing.assert_allclose(got["err_" + key][ok], want["err_" + key][ok], rtol=1e-12, atol=0)
 
 
+@pytest.mark.parametrize("label,N", [("f32", 243), ("f32", 256), ("f16", 200), ("f32", 37)])
+def test_truth_bitwise(label, N):
+    """The binary64 truth of narrow operands uses DFMA, which is exact here
+    because every product of two widened f32/f16 values is exact in binary64:
+    results must equal the sequential DMUL+DADD oracle bit for bit, including
+    subnormal and large-magnitude inputs."""
+    from paper_1905_07439_b200 import engine
+    from paper_1905_07439_b200.precision import parse_precision
+
+    mode = parse_precision(label)
+    g = np.random.default_rng(N)
+    A = g.standard_normal((3, N, N))
+    B = g.standard_normal((3, N, N))
+    tiny = 1e-40 if label == "f32" else 1e-7
+    big = 1e30 if label == "f32" else 3e2
+    A[0, :5, :5] *= tiny
+    B[1, -5:, :] *= big
+    A[2] = np.round(A[2] * 8) / 8  # heavy cancellation
+    A, B = mode.array(A), mode.array(B)
+    got = engine.truth(A, B, mode)
+    for t in range(3):
+        want = oracle.standard_multiply(A[t].astype(np.float64), B[t].astype(np.float64))
+        assert got[t].tobytes() == want.tobytes()
+
+
 def test_device_runner_matches_host_call():
     import torch
 
