@@ -155,6 +155,30 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   };
 
   TAcc acc[TM][TN];
+  // one k step of the register tile: fragments from shared memory, then the
+  // TM x TN multiply-adds (the very first k initialises the accumulators)
+  auto kstep = [&](int buf, int kk, bool first) {
+    TAcc a[TM], bv[TN];
+#pragma unroll
+    for (int g = 0; g < GM; ++g)
+#pragma unroll
+      for (int v = 0; v < VW; ++v) a[g * VW + v] = As[buf][kk][g * DY * VW + ty * VW + v];
+#pragma unroll
+    for (int g = 0; g < GN; ++g)
+#pragma unroll
+      for (int v = 0; v < VW; ++v) bv[g * VW + v] = Bs[buf][kk][g * DX * VW + tx * VW + v];
+    if (first) {
+#pragma unroll
+      for (int ii = 0; ii < TM; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = A::mul(a[ii], bv[jj]);
+    } else {
+#pragma unroll
+      for (int ii = 0; ii < TM; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = Mac<TIn, TAcc>::step(acc[ii][jj], a[ii], bv[jj]);
+    }
+  };
   const int ktiles = (K + BK - 1) / BK;
   load_tile(0);
   store_tile(0);
@@ -164,30 +188,8 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
     const int kmax = min(BK, K - kt * BK);
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      if (kk < kmax) {
-        TAcc a[TM], bv[TN];
-#pragma unroll
-        for (int g = 0; g < GM; ++g)
-#pragma unroll
-          for (int v = 0; v < VW; ++v) a[g * VW + v] = As[buf][kk][g * DY * VW + ty * VW + v];
-#pragma unroll
-        for (int g = 0; g < GN; ++g)
-#pragma unroll
-          for (int v = 0; v < VW; ++v) bv[g * VW + v] = Bs[buf][kk][g * DX * VW + tx * VW + v];
-        if (kt == 0 && kk == 0) {
-#pragma unroll
-          for (int ii = 0; ii < TM; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = A::mul(a[ii], bv[jj]);
-        } else {
-#pragma unroll
-          for (int ii = 0; ii < TM; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = Mac<TIn, TAcc>::step(acc[ii][jj], a[ii], bv[jj]);
-        }
-      }
-    }
+    for (int kk = 0; kk < BK; ++kk)
+      if (kk < kmax) kstep(buf, kk, kt == 0 && kk == 0);
     if (kt + 1 < ktiles) {
       store_tile(buf ^ 1);
       __syncthreads();
@@ -351,31 +353,41 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   load_tile(0);
   store_tile(0);
   __syncthreads();
+  // fragments are read with one vector LDS each (TM and TN contiguous halves)
+  auto kstep = [&](int buf, int kk, bool first) {
+    const Pack<__half, TM> pa = pload<__half, TM>(&As[buf][kk][ty * TM]);
+    const Pack<__half, TN> pb = pload<__half, TN>(&Bs[buf][kk][tx * TN]);
+    const __half2* b2 = reinterpret_cast<const __half2*>(pb.v);
+    __half2 a2[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) a2[i] = __half2half2(pa.v[i]);
+    if (first) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN2; ++j) acc[i][j] = __hmul2_rn(a2[i], b2[j]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN2; ++j) acc[i][j] = __hadd2_rn(acc[i][j], __hmul2_rn(a2[i], b2[j]));
+    }
+  };
   for (int kt = 0; kt < ktiles; ++kt) {
     const int buf = kt & 1;
     if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
-    const int kmax = min(BK, K - kt * BK);
+    if ((kt + 1) * BK <= K) {
+      if (kt == 0) {
+        kstep(buf, 0, true);
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      if (kk < kmax) {
-        __half2 a2[TM], b2[TN2];
+        for (int kk = 1; kk < BK; ++kk) kstep(buf, kk, false);
+      } else {
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a2[i] = __half2half2(As[buf][kk][ty * TM + i]);
-#pragma unroll
-        for (int j = 0; j < TN2; ++j)
-          b2[j] = *reinterpret_cast<const __half2*>(&Bs[buf][kk][tx * TN + 2 * j]);
-        if (kt == 0 && kk == 0) {
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN2; ++j) acc[i][j] = __hmul2_rn(a2[i], b2[j]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN2; ++j) acc[i][j] = __hadd2_rn(acc[i][j], __hmul2_rn(a2[i], b2[j]));
-        }
+        for (int kk = 0; kk < BK; ++kk) kstep(buf, kk, false);
       }
+    } else {
+      const int kmax = K - kt * BK;
+      for (int kk = 0; kk < kmax; ++kk) kstep(buf, kk, kt == 0 && kk == 0);
     }
     if (kt + 1 < ktiles) {
       store_tile(buf ^ 1);
