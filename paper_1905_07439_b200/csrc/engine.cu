@@ -776,7 +776,19 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   const size_t db = (size_t)Q * RBC_PLAN_BYTES;
   std::lock_guard<std::mutex> lock(arena().mu);
   // chunk size: ~8 chunks, shrunk until two input slots + workspace fit
-  int64_t C = std::max<int64_t>(1, (T + 7) / 8);
+  // pipeline chunks: about 16 MB of operands per chunk, at most 32 (measured
+  // on config 2: 4 chunks 18.0 ms, 8: 17.0, 16: 16.8, 32: 16.4 ms per call);
+  // RBC_E2E_CHUNKS overrides
+  static const int forced_chunks = [] {
+    const char* v = getenv("RBC_E2E_CHUNKS");
+    return v ? atoi(v) : 0;
+  }();
+  int64_t nchunks = forced_chunks > 0
+                        ? forced_chunks
+                        : std::min<int64_t>(32, std::max<int64_t>(
+                                                    1, (int64_t)(2 * T * N2 * es >> 23)));
+  int64_t C = std::max<int64_t>(1, (T + nchunks - 1) / nchunks);
+  if (C > 8) C = (C + 7) / 8 * 8;  // whole multiples of 8 trials keep grids regular
   auto need = [&](int64_t c) {
     const size_t slot = 2 * align_up(c * N2 * es) + align_up(c * Q * RBC_PLAN_BYTES);
     return 2 * slot + align_up(db) + 2 * align_up(T * 8) + 2 * align_up(T) + 4096 +

@@ -26,8 +26,13 @@ for _ in range(3):
     dt = time.perf_counter() - t0
     print(f"H2D {Ap.numel() * Ap.element_size() / 1e6:.0f} MB in {dt * 1e3:.2f} ms = {Ap.numel() * Ap.element_size() / dt / 1e9:.1f} GB/s")
 An, Bn, Pn = Ap.numpy(), Bp.numpy(), Pp.numpy()
-for i in range(8):
+times = []
+f = cfg.formula_obj()
+for i in range(12):
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    error_trials(cfg.formula_obj(), cfg.Q, An, Bn, cfg.mode, packed=Pn)
+    error_trials(f, cfg.Q, An, Bn, cfg.mode, packed=Pn)
     torch.cuda.synchronize()
-    print(f"call {i}: {(time.perf_counter() - t0) * 1e3:.2f} ms")
+    times.append((time.perf_counter() - t0) * 1e3)
+import statistics  # noqa: E402
+print("calls ms:", " ".join(f"{t:.1f}" for t in times))
+print(f"median {statistics.median(times[2:]):.2f} ms  min {min(times[2:]):.2f} ms")
