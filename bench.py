@@ -308,15 +308,6 @@ def roofline(prof: dict, config: str, cfg=None, pairs=None, sm_max_mhz=None):
 
 
 # ------------------------------------------------------------ CPU oracle ----
-def _descend(x, coeff_level, depth_levels):
-    """Branch 0 of the top levels: combine, keep child 0 only."""
-    from oracle import engine as oracle
-
-    for c in depth_levels:
-        x = oracle.combine(x, c[:, :1])[:, :1]
-    return x
-
-
 def _cpu_job(job):
     """One CPU work unit through the oracle: pair p, products js (0 = the
     deterministic product, j >= 1 = randomized plan j), evaluated on branch 0
