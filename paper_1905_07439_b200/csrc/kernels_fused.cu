@@ -239,6 +239,224 @@ __global__ void __launch_bounds__(NT) subtree_kernel(
   }
 }
 
+// ---- position-major (SoA) two-level subtree ---------------------------------
+// Same arithmetic and stages as subtree_kernel<F, T, 2, M>, different shared
+// memory layout.  Element (block beta, position pi) of a level is stored at
+// pi * NB + beta (NB = blocks of that level in the subtree), level-1 blocks in
+// blocked order (their n x n sub-blocks contiguous).  With the parent-minor
+// item order e = Kp + R * pi, every access of every stage is bank-conflict
+// free for odd R: parents read at e + off, children written at R * e + r, leaves
+// read at consecutive addresses (simulated 1338 vs 1956 wavefronts per CTA for
+// config 2 with the row-major layout).
+template <class F, class T, int M, int H>
+struct SubtreeSoA {
+  static constexpr int n = F::n;
+  static constexpr int R = F::R;
+  static constexpr int s1 = M * n;
+  static constexpr int s0 = s1 * n;
+  static constexpr int kids1 = s1 * s1;
+  static constexpr int leafE = M * M;
+  // level-1 parents are processed in H groups of at most G (smaller leaf
+  // buffers -> more CTAs per SM, which this latency-bound kernel needs)
+  static constexpr int G = (R + H - 1) / H;
+  static constexpr int NB2 = G * R;  // leaves held at a time
+  static constexpr bool kInPlace = M <= 4;
+  static constexpr int x1_off = 0;
+  static constexpr int y1_off = kids1 * R;
+  static constexpr int x2_off = 2 * kids1 * R;
+  static constexpr int y2_off = x2_off + leafE * NB2;
+  static constexpr int p2_off = kInPlace ? x2_off : y2_off + leafE * NB2;
+  static constexpr int total = kInPlace ? y2_off + leafE * NB2 : p2_off + leafE * NB2;
+  static constexpr size_t header() {
+    return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 6 * sizeof(GatherTab<n>);
+  }
+  static constexpr size_t smem_bytes() { return header() + sizeof(T) * (size_t)total; }
+};
+
+template <class F, class T, int M, int H, int NT>
+__global__ void __launch_bounds__(NT) subtree_soa_kernel(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0,
+    T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
+    int64_t ntr, uint8_t* __restrict__ nonfinite) {
+  using S = SubtreeSoA<F, T, M, H>;
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  constexpr int s0 = S::s0, s1 = S::s1, kids1 = S::kids1, leafE = S::leafE;
+  constexpr int G = S::G;
+  constexpr int kHalf = NT / 2;
+  using A = Arith<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
+  GatherTab<n>* tabs =
+      reinterpret_cast<GatherTab<n>*>(smem_raw + ((sizeof(PlanLevel) * 2 + 15) / 16) * 16);
+  T* sm = reinterpret_cast<T*>(smem_raw + S::header());
+  T* X1 = sm + S::x1_off;
+  T* Y1 = sm + S::y1_off;
+  T* X2 = sm + S::x2_off;
+  T* Y2 = sm + S::y2_off;
+  T* P2 = sm + S::p2_off;
+  const int k0 = blockIdx.x;
+  const int which = threadIdx.x >= kHalf;
+  const int lt = threadIdx.x - which * kHalf;
+
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    __syncthreads();
+    {
+      constexpr int kWords = (int)(sizeof(PlanLevel) / 4) * 2;
+      const int* src = reinterpret_cast<const int*>(plans + t * plan_tstride + q0);
+      if (threadIdx.x < kWords) reinterpret_cast<int*>(spl)[threadIdx.x] = src[threadIdx.x];
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      GatherTab<n> tab;
+      switch (threadIdx.x) {
+        case 0: make_gather<n, 0>(spl[0], s0, tab); break;  // level q0, row-major in HBM
+        case 1: make_gather<n, 1>(spl[0], s0, tab); break;
+        case 2: make_scatter<n>(spl[0], s1, tab); break;
+        case 3: make_gather_soa<n, 0>(spl[1], leafE * R, tab); break;  // level q0+1, SoA
+        case 4: make_gather_soa<n, 1>(spl[1], leafE * R, tab); break;
+        default: make_scatter_soa<n>(spl[1], leafE * R, tab); break;
+      }
+      tabs[threadIdx.x] = tab;
+    }
+    __syncthreads();
+
+    // ---- expansion q0 -> q0+1: HBM (row-major) -> X1/Y1 (SoA, blocked)
+    {
+      const T* src = (which ? y : x) + t * xy_tstride + (int64_t)k0 * s0 * s0;
+      T* dst = which ? Y1 : X1;
+      const GatherTab<n> gt = tabs[which];
+      for (int b = lt; b < kids1; b += kHalf) {
+        const int sb = b / leafE, ip = b - (b / leafE) * leafE;
+        const int i = (sb / n) * M + ip / M, j = (sb - (sb / n) * n) * M + (ip - (ip / M) * M);
+        if (which)
+          expand_tab<F, T, 1, 1>(src + i * s0 + j, gt, dst + b * R, 1);
+        else
+          expand_tab<F, T, 1, 0>(src + i * s0 + j, gt, dst + b * R, 1);
+      }
+    }
+    __syncthreads();
+
+#pragma unroll 1
+    for (int kp0 = 0; kp0 < R; kp0 += G) {
+      const int ng = R - kp0 < G ? R - kp0 : G;  // parents in this group
+      const int nb2 = ng * R;                    // leaves in this group
+      // ---- expansion q0+1 -> q0+2 of the group, item e = Kl + ng * pi
+      {
+        const GatherTab<n> gt = tabs[3 + which];
+        const T* par = (which ? Y1 : X1) + kp0;
+        T* kid = which ? Y2 : X2;
+        for (int e = lt; e < ng * leafE; e += kHalf) {
+          const int pi = e / ng, kl = e - (e / ng) * ng;
+          if (which)
+            expand_tab<F, T, 1, 1>(par + pi * R + kl, gt, kid + e * R, 1);
+          else
+            expand_tab<F, T, 1, 0>(par + pi * R + kl, gt, kid + e * R, 1);
+        }
+      }
+      __syncthreads();
+
+      // ---- leaf products, k ascending; element q of leaf l at q * nb2 + l
+      if (S::kInPlace) {
+        for (int l = threadIdx.x; l < nb2; l += NT) {
+          T xa[leafE], yb[leafE];
+#pragma unroll
+          for (int q = 0; q < leafE; ++q) {
+            xa[q] = X2[q * nb2 + l];
+            yb[q] = Y2[q * nb2 + l];
+          }
+#pragma unroll
+          for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+              T acc = A::mul(xa[i * M], yb[j]);
+#pragma unroll
+              for (int k = 1; k < M; ++k) acc = A::add(acc, A::mul(xa[i * M + k], yb[k * M + j]));
+              P2[(i * M + j) * nb2 + l] = acc;
+            }
+        }
+      } else {
+        for (int it = threadIdx.x; it < nb2 * M; it += NT) {
+          const int i = it / nb2, l = it - (it / nb2) * nb2;
+          T acc[M];
+#pragma unroll
+          for (int j = 0; j < M; ++j) acc[j] = A::mul(X2[(i * M) * nb2 + l], Y2[j * nb2 + l]);
+#pragma unroll
+          for (int k = 1; k < M; ++k) {
+            const T xv = X2[(i * M + k) * nb2 + l];
+#pragma unroll
+            for (int j = 0; j < M; ++j) acc[j] = A::add(acc[j], A::mul(xv, Y2[(k * M + j) * nb2 + l]));
+          }
+#pragma unroll
+          for (int j = 0; j < M; ++j) P2[(i * M + j) * nb2 + l] = acc[j];
+        }
+      }
+      __syncthreads();
+
+      // ---- contraction q0+2 -> q0+1 of the group into the dead X1 slots
+      {
+        const GatherTab<n> st = tabs[5];
+        for (int e = threadIdx.x; e < ng * leafE; e += NT) {
+          const int pi = e / ng, kl = e - (e / ng) * ng;
+          contract_tab<F, T, 1, false>(P2 + e * R, 1, X1 + pi * R + kp0 + kl, st);
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---- contraction q0+1 -> q0: X1 -> HBM (row-major)
+    bool ok = true;
+    {
+      const GatherTab<n> st = tabs[2];
+      T* dbase = out + (t * K0 + k0) * (int64_t)s0 * s0;
+      for (int b = threadIdx.x; b < kids1; b += NT) {
+        const int sb = b / leafE, ip = b - (b / leafE) * leafE;
+        const int i = (sb / n) * M + ip / M, j = (sb - (sb / n) * n) * M + (ip - (ip / M) * M);
+        if (nonfinite)
+          ok = contract_tab<F, T, 1, true>(X1 + b * R, 1, dbase + i * s0 + j, st) && ok;
+        else
+          contract_tab<F, T, 1, false>(X1 + b * R, 1, dbase + i * s0 + j, st);
+      }
+    }
+    if (nonfinite && !ok) nonfinite[t] = 1;
+  }
+}
+
+template <class F, class T, int M, int H>
+cudaError_t launch_subtree_soa_h(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
+                                 void* out, const PlanLevel* plans, int64_t pts, int q0,
+                                 int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
+  constexpr int NT = 256;
+  using S = SubtreeSoA<F, T, M, H>;
+  static const size_t pad = [] {  // RBC_SUBTREE_SMEM_PAD: occupancy experiments
+    const char* v = getenv("RBC_SUBTREE_SMEM_PAD");
+    return v ? (size_t)atol(v) : (size_t)0;
+  }();
+  const size_t smem = S::smem_bytes() + pad;
+  auto kern = subtree_soa_kernel<F, T, M, H, NT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)K0, (unsigned)(ntr < 65535 ? ntr : 65535));
+  kern<<<grid, NT, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, (T*)out, plans, pts,
+                               q0, ntr, nonfinite);
+  return cudaGetLastError();
+}
+
+// Parent groups per subtree (RBC_SUBTREE_H=2 halves the leaf buffers: 6
+// instead of 4 CTAs/SM on config 2, but measured 5.3 vs 5.0 ms per launch --
+// the extra barrier rounds cost more than the occupancy gains; default 1).
+template <class F, class T, int M>
+cudaError_t launch_subtree_soa(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
+                               void* out, const PlanLevel* plans, int64_t pts, int q0,
+                               int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
+  static const int h = [] {
+    const char* v = getenv("RBC_SUBTREE_H");
+    return v ? atoi(v) : 1;
+  }();
+  if (h == 2) return launch_subtree_soa_h<F, T, M, 2>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
+  return launch_subtree_soa_h<F, T, M, 1>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
+}
+
 // ---- warp-specialised two-level subtree ------------------------------------
 // Same arithmetic as subtree_kernel<F, T, 2, M>, other schedule: the top
 // expansion (level q0 -> q0+1) and the last contraction run CTA-wide, but
@@ -438,6 +656,13 @@ cudaError_t launch_subtree_t(const void* x, const void* y, int64_t xy_tstride, i
     }();
     if (mode)
       return launch_subtree2w<F, T, M, 3>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
+    // position-major layout (default; RBC_SUBTREE_SOA=0 selects the row-major one)
+    static const int soa = [] {
+      const char* v = getenv("RBC_SUBTREE_SOA");
+      return v ? atoi(v) : 1;
+    }();
+    if (soa)
+      return launch_subtree_soa<F, T, M>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
   }
   if (forced == 128) return launch(subtree_kernel<F, T, L, M, 128>, 128);
   if (forced == 512) return launch(subtree_kernel<F, T, L, M, 512>, 512);

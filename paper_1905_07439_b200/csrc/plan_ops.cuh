@@ -123,6 +123,46 @@ __device__ __forceinline__ void make_scatter(const PlanLevel& pl, int mb, Gather
   gt.lastrow = gt.lastcol = 0;
 }
 
+// Position-major ("SoA") shared-memory layouts of the fused subtree: element
+// (block beta, position pi) of a level lives at pi * NB + beta, and a level-1
+// block stores its n x n sub-blocks contiguously (blocked order).  Gather and
+// scatter offsets then only depend on the hatted sub-block index:
+// off = (hk * n + hl) * sub_stride.
+template <int n, int WHICH>
+__device__ __forceinline__ void make_gather_soa(const PlanLevel& pl, int sub_stride,
+                                                GatherTab<n>& gt) {
+  constexpr int ri = WHICH == 0 ? 0 : 1;
+  constexpr int ci = WHICH == 0 ? 1 : 2;
+#pragma unroll
+  for (int kb = 0; kb < n; ++kb) {
+    const int hk = pl.inv[ri][kb];
+#pragma unroll
+    for (int lb = 0; lb < n; ++lb) {
+      const int hl = pl.inv[ci][lb];
+      gt.off[kb * n + lb] = (hk * n + hl) * sub_stride;
+      gt.msk[kb * n + lb] = sign_mask(pl.neg[ri][hk] ^ pl.neg[ci][hl]);
+    }
+  }
+  gt.lastrow = pl.perm[ri][n - 1];
+  gt.lastcol = pl.perm[ci][n - 1];
+}
+
+template <int n>
+__device__ __forceinline__ void make_scatter_soa(const PlanLevel& pl, int sub_stride,
+                                                 GatherTab<n>& gt) {
+#pragma unroll
+  for (int I = 0; I < n; ++I) {
+    const int hi = pl.inv[0][I];
+#pragma unroll
+    for (int J = 0; J < n; ++J) {
+      const int hj = pl.inv[2][J];
+      gt.off[I * n + J] = (hi * n + hj) * sub_stride;
+      gt.msk[I * n + J] = sign_mask(pl.neg[0][hi] ^ pl.neg[2][hj]);
+    }
+  }
+  gt.lastrow = gt.lastcol = 0;
+}
+
 template <class F, class T, int W, int WHICH>
 __device__ __forceinline__ void expand_tab(const T* __restrict__ base, const GatherTab<F::n>& gt,
                                            T* __restrict__ kid0, int kid_stride) {
