@@ -460,9 +460,13 @@ class ErrorTrialWorkload:
         if not (np.array_equal(res["err_rand"], err_r, equal_nan=True)
                 and np.array_equal(res["err_det"], err_d, equal_nan=True)):
             raise SystemExit("e2e errors differ from the device-resident run")
+        pn = P_pin.numpy()
+        self.e2e_calls = []
         t0 = time.perf_counter()
         for _ in range(steps):
-            error_trials(*args, packed=P_pin.numpy())
+            t1 = time.perf_counter()
+            error_trials(*args, packed=pn)
+            self.e2e_calls.append((time.perf_counter() - t1) * 1e3)
         ms = (time.perf_counter() - t0) / steps * 1e3
         h2d = self.A.nbytes + self.B.nbytes + self.packed.nbytes
         d2h = 2 * len(err_r) * 9
@@ -623,6 +627,9 @@ def run_ours(args):
         line["e2e"] = {"value": round(flops_step / (e2e_ms / 1e3) / 1e9, 3), "unit": "GFLOP/s",
                        "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(e2e[1]),
                        "d2h_bytes_per_step": int(e2e[2])}
+        calls = getattr(wl, "e2e_calls", None)
+        if calls:
+            line["e2e"]["ms_per_call"] = [round(c, 2) for c in calls]
 
     if rank == 0 and world == 1 and not args.no_cpu:
         count, per_pair, depth = DEFAULTS[cfg.name]["cpu"]
