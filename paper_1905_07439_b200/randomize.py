@@ -188,11 +188,8 @@ _plan_level_alias = plan_levels  # reference name: _plan_levels
 _KNOWN = None
 
 
-def plan_formula_id(f: BilinearFormula):
-    """Engine id of an exact +-1 formula with compiled networks, else None.
-
-    Such a formula has kappa == 0 exactly, so its rescale factor is 1 and the
-    hatted tables are pure signed permutations of the base coefficients."""
+def _known_formulas():
+    """(engine id, formula) for every exact +-1 formula with compiled networks."""
     global _KNOWN
     if _KNOWN is None:
         from ._lib import FORMULA_IDS
@@ -203,7 +200,15 @@ def plan_formula_id(f: BilinearFormula):
             (FORMULA_IDS["standard2"], standard_formula(2)),
             (FORMULA_IDS["standard3"], standard_formula(3)),
         ]
-    for fid, g in _KNOWN:
+    return _KNOWN
+
+
+def plan_formula_id(f: BilinearFormula):
+    """Engine id of an exact +-1 formula with compiled networks, else None.
+
+    Such a formula has kappa == 0 exactly, so its rescale factor is 1 and the
+    hatted tables are pure signed permutations of the base coefficients."""
+    for fid, g in _known_formulas():
         if g.u.shape == f.u.shape and all(
             np.array_equal(getattr(g, x), getattr(f, x)) for x in "uvw"
         ):

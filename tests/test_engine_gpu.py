@@ -18,8 +18,11 @@ def eng():
     return engine
 
 
-def test_golden_engine_cases_dense_path(eng, engine_cases):
-    """apply_levels (hatted coefficient tables -> dense kernels) == reference."""
+@pytest.mark.parametrize("detect", ["0", "1"])
+def test_golden_engine_cases_dense_path(eng, engine_cases, monkeypatch, detect):
+    """apply_levels == reference, with hatted +-1 tables recognised and run
+    on the plan kernels (detect=1) and with everything dense (detect=0)."""
+    monkeypatch.setenv("RBC_DETECT_PLANS", detect)
     meta, arrs = engine_cases
     for case in meta["engine"]:
         name = case["name"]
@@ -91,8 +94,8 @@ def test_golden_leaf_cases(eng, engine_cases):
         ("f64", "strassen", 1, 260, 1),   # 130x130 binary64 leaves
     ],
 )
-def test_random_plans_vs_oracle(eng, label, fname, Q, N, T):
-    """Both engine paths equal the oracle on seeded larger problems."""
+def test_random_plans_vs_oracle(eng, monkeypatch, label, fname, Q, N, T):
+    """Every engine path equals the oracle on seeded larger problems."""
     import paper_1905_07439_b200 as rbc
 
     mode = mode_for(label)
@@ -103,9 +106,12 @@ def test_random_plans_vs_oracle(eng, label, fname, Q, N, T):
     rplans = [rbc.draw_recursive_plan(f.n, Q, rbc.derive_rng(78, t)) for t in range(T)]
     levels = [rbc.plan_levels(f, [rp.levels[q] for rp in rplans], mode) for q in range(Q)]
     want = oracle.apply_levels(levels, A[None], B[None], mode)
-    got_dense = eng.apply_levels(levels, A[None], B[None], mode)
+    got_detected = eng.apply_levels(levels, A[None], B[None], mode)
     got_plan = rbc.recursive_randomized_apply_many(f, rplans, A, B, mode)
+    monkeypatch.setenv("RBC_DETECT_PLANS", "0")
+    got_dense = eng.apply_levels(levels, A[None], B[None], mode)
     assert same_values(got_dense, want)
+    assert same_values(got_detected, want)
     assert same_values(got_plan, want)
 
 

@@ -91,7 +91,7 @@ def test_golden_subset_cpu_oracle():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kind", ["gaussian", "adv1"])
+@pytest.mark.parametrize("kind", ["gaussian", "uniform", "adv1", "adv2", "adv3", "hilbert"])
 def test_golden_rows_gpu(kind):
     from paper_1905_07439_b200 import (
         DOUBLE,

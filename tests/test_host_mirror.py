@@ -84,3 +84,39 @@ def test_config_seed_layout_matches_experiments():
     assert np.array_equal(rp.levels[0].perms, p0.perms)
     c3 = get_config("c3")
     assert c3.plan_key(2, 5) == 37
+
+
+@pytest.mark.parametrize("name", ["strassen", "laderman", "standard2", "standard3"])
+def test_plan_recognition_reproduces_tables(name):
+    """engine.match_plans recovers plans whose hatted tables equal the ones
+    the reference's L2 builds (randomize.py:163-178), so the drop-in boundary
+    can route them to the plan-path kernels."""
+    from paper_1905_07439_b200.engine import match_plans
+    from paper_1905_07439_b200.multiply import mode_tensors
+    from paper_1905_07439_b200.randomize import plan_levels
+
+    f = {"strassen": rbc.strassen_formula, "laderman": rbc.laderman_formula,
+         "standard2": lambda: rbc.standard_formula(2),
+         "standard3": lambda: rbc.standard_formula(3)}[name]()
+    Q, T = 2, 40
+    rps = [[rbc.draw_plan(f.n, rbc.derive_rng(7, t, q)) for q in range(Q)] for t in range(T)]
+    for mode in (rbc.DOUBLE, rbc.SINGLE, rbc.HALF):
+        tabs = [list(plan_levels(f, [rp[q] for rp in rps], mode)) for q in range(Q)]
+        fid, perms, signs = match_plans(tabs)
+        for t in range(T):
+            for q in range(Q):
+                plan = rbc.RandomizationPlan(signs=signs[t, q], perms=perms[t, q])
+                got = plan_levels(f, [plan], mode)
+                for a, b in zip(got, tabs[q]):
+                    np.testing.assert_array_equal(a[0], b[t])
+        # a broadcast (Tc == 1) deterministic level mixes with per-trial ones
+        mixed = [list(mode_tensors(f, mode))] + tabs[1:]
+        fid2, perms2, _ = match_plans(mixed)
+        assert fid2 == fid and perms2.shape == (T, Q, 3, f.n)
+        assert np.array_equal(perms2[:, 0], np.tile(np.arange(f.n), (T, 3, 1)))
+    # perturbed (non +-1) and mixed-formula levels stay on the dense path
+    g = rbc.perturb(f, 1e-3, 0, rbc.derive_rng(5))
+    assert match_plans([list(mode_tensors(g, rbc.DOUBLE))]) is None
+    u, v, w = (t.copy() for t in mode_tensors(f, rbc.DOUBLE))
+    u[0, 0, 0, 0] = -u[0, 0, 0, 0] if u[0, 0, 0, 0] else 1.0
+    assert match_plans([[u, v, w]]) is None
