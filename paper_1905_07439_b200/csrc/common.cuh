@@ -67,8 +67,10 @@ __device__ __forceinline__ uint32_t sign_mask(int negative) { return negative ? 
 
 // ----------------------------------------------------------------- pack ----
 // W consecutive elements handled by one thread; loaded and stored with one
-// vector access when the address is sizeof(Pack)-aligned.
-template <class T, int W> struct alignas(sizeof(T) * W) Pack {
+// vector access when the address is sizeof(Pack)-aligned (power-of-two W;
+// other widths are register-only packs).
+template <class T, int W>
+struct alignas((W & (W - 1)) == 0 ? sizeof(T) * W : sizeof(T)) Pack {
   T v[W];
 };
 

@@ -17,6 +17,7 @@
 // the leaf products P_L (R^L M^2).  Contractions reuse the dead X_l buffers.
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.h"
 #include "plan_ops.cuh"
@@ -628,6 +629,211 @@ cudaError_t launch_subtree2w(const void* x, const void* y, int64_t xy_tstride, i
   return cudaGetLastError();
 }
 
+// ---- register-resident two-level subtree (small leaves) ----------------------
+// Same arithmetic as subtree_kernel<F, T, 2, M>, with the level-(q0+1) stage
+// moved out of shared memory.  Lane (r1, i) of a group of M lanes owns leaf
+// row i of every sub-block of level-(q0+1) block r1: its X, Y and Z "fibers"
+// (n*n sub-blocks x M columns) sit in registers.  Both folds of that level
+// run element-wise down the fibers:
+//   expansion  child r2 = fold over the n*n sub-blocks (formula networks,
+//              one output r2 at a time: expand_u1 / expand_v1);
+//   contraction Z(I,J)  = fold over r2 ascending (contract_w_step), i.e. the
+//              reference's order (_engine.py:104-112) streamed over r2.
+// Only the M x M leaf needs other lanes' data: the Y rows of the group,
+// exchanged with warp shuffles.  The leaf keeps the reference's k-ascending
+// order (_engine.py:42-61).  Level q0 (HBM <-> shared) is as in the SoA
+// kernel; X1/Y1 are position-major with a padded child stride RP so the
+// fiber loads of a warp hit distinct banks.  Z overwrites X1 in place: a
+// lane writes exactly the rows {hk*M + i} of block r1 it read.
+template <class F, class T, int M>
+struct SubtreeReg {
+  static constexpr int n = F::n;
+  static constexpr int R = F::R;
+  static constexpr int s1 = M * n;
+  static constexpr int s0 = s1 * n;
+  static constexpr int kids1 = s1 * s1;
+  static constexpr int GPW = 32 / M;                // leaf-row groups per warp
+  static constexpr int NW = (R + GPW - 1) / GPW;    // one group per level-1 block
+  static constexpr int NT = NW * 32;
+  // child stride: (s1 * RP) mod 32 spreads the M rows of a warp over disjoint banks
+  static constexpr int RP = (F::R == 23 && M == 3) ? 26 : R;
+  static constexpr size_t header() {
+    return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 5 * sizeof(GatherTab<n>);
+  }
+  static constexpr size_t smem_bytes() { return header() + sizeof(T) * (size_t)2 * kids1 * RP; }
+};
+
+template <class T>
+__device__ __forceinline__ T shfl_val(T v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+template <class F, class T, int M>
+__global__ void __launch_bounds__(SubtreeReg<F, T, M>::NT) subtree_reg_kernel(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0, int kchunk,
+    T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
+    int64_t ntr, uint8_t* __restrict__ nonfinite) {
+  using S = SubtreeReg<F, T, M>;
+  using P = Pack<T, M>;
+  using A = Arith<T>;
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  constexpr int s0 = S::s0, s1 = S::s1, kids1 = S::kids1, RP = S::RP, NT = S::NT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
+  GatherTab<n>* tabs =
+      reinterpret_cast<GatherTab<n>*>(smem_raw + ((sizeof(PlanLevel) * 2 + 15) / 16) * 16);
+  T* X1 = reinterpret_cast<T*>(smem_raw + S::header());
+  T* Y1 = X1 + kids1 * RP;
+
+  // stage-B role of this lane
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int gw = lane / M;
+  const int gbase = (gw < S::GPW ? gw : S::GPW - 1) * M;  // lanes past the last group mirror it
+  const int li = lane - gw * M < M ? lane - gw * M : 0;
+  int r1 = warp * S::GPW + (gw < S::GPW ? gw : S::GPW - 1);
+  const bool active = gw < S::GPW && r1 < R;
+  if (r1 >= R) r1 = R - 1;
+
+  const int kbeg = blockIdx.x * kchunk;
+  const int kend = kbeg + kchunk < K0 ? kbeg + kchunk : K0;
+
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    __syncthreads();
+    {
+      constexpr int kWords = (int)(sizeof(PlanLevel) / 4) * 2;
+      const int* src = reinterpret_cast<const int*>(plans + t * plan_tstride + q0);
+      if (threadIdx.x < kWords) reinterpret_cast<int*>(spl)[threadIdx.x] = src[threadIdx.x];
+    }
+    __syncthreads();
+    if (threadIdx.x < 5) {
+      GatherTab<n> tab;
+      switch (threadIdx.x) {
+        case 0: make_gather<n, 0>(spl[0], s0, tab); break;  // level q0 (HBM, row-major)
+        case 1: make_gather<n, 1>(spl[0], s0, tab); break;
+        case 2: make_scatter<n>(spl[0], s1, tab); break;
+        case 3: make_gather<n, 0>(spl[1], s1, tab); break;  // level q0+1 (fibers)
+        default: make_gather<n, 1>(spl[1], s1, tab); break;
+      }
+      tabs[threadIdx.x] = tab;
+    }
+    __syncthreads();
+    bool ok = true;
+
+    for (int k0 = kbeg; k0 < kend; ++k0) {
+      // ---- stage A: level q0 -> q0+1, HBM -> X1 / Y1 (position-major)
+      {
+        const T* xs = x + t * xy_tstride + (int64_t)k0 * s0 * s0;
+        const T* ys = y + t * xy_tstride + (int64_t)k0 * s0 * s0;
+        for (int e = threadIdx.x; e < 2 * kids1; e += NT) {
+          const int which = e >= kids1;
+          const int pos = e - which * kids1;
+          const int i = pos / s1, j = pos - (pos / s1) * s1;
+          if (which)
+            expand_tab<F, T, 1, 1>(ys + i * s0 + j, tabs[1], Y1 + pos * RP, 1);
+          else
+            expand_tab<F, T, 1, 0>(xs + i * s0 + j, tabs[0], X1 + pos * RP, 1);
+        }
+      }
+      __syncthreads();
+
+      // ---- stage B: level q0+1 -> leaves -> level q0+1, in registers
+      {
+        const GatherTab<n>& gx = tabs[3];
+        const GatherTab<n>& gy = tabs[4];
+        P xf[n * n], yf[n * n];
+#pragma unroll
+        for (int k = 0; k < n * n; ++k) {
+          const int ox = (gx.off[k] + li * s1) * RP + r1;
+          const int oy = (gy.off[k] + li * s1) * RP + r1;
+          const uint32_t mx = gx.msk[k], my = gy.msk[k];
+#pragma unroll
+          for (int j = 0; j < M; ++j) {
+            xf[k].v[j] = flip_sign(X1[ox + j * RP], mx);
+            yf[k].v[j] = flip_sign(Y1[oy + j * RP], my);
+          }
+        }
+        const int xlr = gx.lastrow, xlc = gx.lastcol, ylr = gy.lastrow, ylc = gy.lastcol;
+        P z[n * n];
+#pragma unroll
+        for (int r2 = 0; r2 < R; ++r2) {
+          const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
+          const P yg = F::template expand_v1<T, M>(yf, r2, ylr, ylc);
+          P yr[M];
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+#pragma unroll
+            for (int j = 0; j < M; ++j) yr[k].v[j] = shfl_val(yg.v[j], gbase + k);
+          P m;
+#pragma unroll
+          for (int j = 0; j < M; ++j) {
+            T acc = A::mul(xg.v[0], yr[0].v[j]);
+#pragma unroll
+            for (int k = 1; k < M; ++k) acc = A::add(acc, A::mul(xg.v[k], yr[k].v[j]));
+            m.v[j] = acc;
+          }
+          F::template contract_w_step<T, M>(z, m, r2);
+        }
+        F::template contract_w_finish<T, M>(z);
+        // scatter of level q0+1: base block (I, J) -> hatted (p1^-1(I), p3^-1(J))
+        const PlanLevel& pl1 = spl[1];
+        if (active) {
+#pragma unroll
+          for (int I = 0; I < n; ++I) {
+            const int hi = pl1.inv[0][I];
+#pragma unroll
+            for (int J = 0; J < n; ++J) {
+              const int hj = pl1.inv[2][J];
+              const uint32_t msk = sign_mask(pl1.neg[0][hi] ^ pl1.neg[2][hj]);
+              const int o = ((hi * M + li) * s1 + hj * M) * RP + r1;
+#pragma unroll
+              for (int j = 0; j < M; ++j) X1[o + j * RP] = flip_sign(z[I * n + J].v[j], msk);
+            }
+          }
+        }
+      }
+      __syncthreads();
+
+      // ---- stage C: level q0+1 -> q0, X1 -> HBM (row-major)
+      {
+        T* dbase = out + (t * K0 + k0) * (int64_t)s0 * s0;
+        for (int pos = threadIdx.x; pos < kids1; pos += NT) {
+          const int i = pos / s1, j = pos - (pos / s1) * s1;
+          if (nonfinite)
+            ok = contract_tab<F, T, 1, true>(X1 + pos * RP, 1, dbase + i * s0 + j, tabs[2]) && ok;
+          else
+            contract_tab<F, T, 1, false>(X1 + pos * RP, 1, dbase + i * s0 + j, tabs[2]);
+        }
+      }
+      __syncthreads();
+    }
+    if (nonfinite && !ok) nonfinite[t] = 1;
+  }
+}
+
+template <class F, class T, int M>
+cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
+                               void* out, const PlanLevel* plans, int64_t pts, int q0,
+                               int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
+  using S = SubtreeReg<F, T, M>;
+  const size_t smem = S::smem_bytes();
+  auto kern = subtree_reg_kernel<F, T, M>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // subtrees per CTA (one trial's plan tables are built once per chunk)
+  static const int kc_env = [] {
+    const char* v = getenv("RBC_SUBTREE_CHUNK");
+    return v ? atoi(v) : 0;
+  }();
+  int kchunk = kc_env > 0 ? kc_env : 8;
+  if (kchunk > K0) kchunk = (int)K0;
+  const int64_t nkc = (K0 + kchunk - 1) / kchunk;
+  dim3 grid((unsigned)nkc, (unsigned)(ntr < 65535 ? ntr : 65535));
+  kern<<<grid, S::NT, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, kchunk, (T*)out,
+                                  plans, pts, q0, ntr, nonfinite);
+  return cudaGetLastError();
+}
+
 template <class F, class T, int L, int M>
 cudaError_t launch_subtree_t(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
                              void* out, const PlanLevel* plans, int64_t pts, int q0, int64_t ntr,
@@ -656,6 +862,15 @@ cudaError_t launch_subtree_t(const void* x, const void* y, int64_t xy_tstride, i
     }();
     if (mode)
       return launch_subtree2w<F, T, M, 3>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
+    // register-resident level q0+1 for 3x3 Laderman leaves (RBC_SUBTREE_REG=0 disables)
+    if constexpr (F::kId == FLaderman::kId && M == 3 && !std::is_same<T, double>::value) {
+      static const int reg = [] {
+        const char* v = getenv("RBC_SUBTREE_REG");
+        return v ? atoi(v) : 1;
+      }();
+      if (reg)
+        return launch_subtree_reg<F, T, M>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
+    }
     // position-major layout (default; RBC_SUBTREE_SOA=0 selects the row-major one)
     static const int soa = [] {
       const char* v = getenv("RBC_SUBTREE_SOA");

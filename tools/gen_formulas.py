@@ -107,6 +107,41 @@ def expand_body(t, n, lastrow, lastcol):
     return em.lines
 
 
+def expand_one_body(t, n, r, lastrow, lastcol):
+    """Output r alone of expand_body (same operations, same order)."""
+    lines = expand_body(t[r:r + 1], n, lastrow, lastcol)
+    return [ln.replace("o[0] = ", "return ") for ln in lines]
+
+
+def contract_stream(w, n):
+    """contract_body as a stream over r: per r, the accumulator updates that
+    contract_body's chains perform for term r (acc holds sign * value), and
+    the final sign fix-ups.  Same operations in the same order."""
+    R = w.shape[0]
+    sign = {}
+    steps = []
+    for r in range(R):
+        lines = []
+        for i in range(n):
+            for j in range(n):
+                c = w[r, i, j]
+                if c == 0:
+                    continue
+                k = i * n + j
+                st = int(np.sign(c))
+                if k not in sign:
+                    sign[k] = st
+                    lines.append(f"        acc[{k}] = p;")
+                elif sign[k] == st:
+                    lines.append(f"        acc[{k}] = O::add(acc[{k}], p);")
+                else:
+                    lines.append(f"        acc[{k}] = O::sub(acc[{k}], p);")
+        steps.append(lines)
+    assert len(sign) == n * n, "streamed contraction needs a term for every output"
+    finish = [f"    acc[{k}] = O::neg(acc[{k}]);" for k in sorted(sign) if sign[k] < 0]
+    return steps, finish
+
+
 def contract_body(w, n):
     em = Emitter()
     R = w.shape[0]
@@ -159,6 +194,47 @@ def emit():
             out.append("    (void)lastrow; (void)lastcol;")
             out.extend(expand_body(tensor, n, "lastrow", "lastcol"))
             out.append("  }")
+        for tname, tensor in (("expand_u1", f.u), ("expand_v1", f.v)):
+            out.append("  // output r alone (r a compile-time constant after unrolling)")
+            out.append("  template <class T, int W>")
+            out.append(
+                f"  __device__ __forceinline__ static Pack<T, W> {tname}("
+                "const Pack<T, W>* g, int r, int lastrow, int lastcol) {"
+            )
+            out.append("    using P = Pack<T, W>;")
+            out.append("    using O = PackOps<T, W>;")
+            out.append("    (void)lastrow; (void)lastcol;")
+            out.append("    switch (r) {")
+            for r in range(R):
+                out.append(f"      case {r}: {{")
+                out.extend("  " + ln for ln in expand_one_body(tensor, n, r, "lastrow", "lastcol"))
+                out.append("      }")
+            out.append("      default: return g[0];")
+            out.append("    }")
+            out.append("  }")
+        steps, finish = contract_stream(f.w, n)
+        out.append("  // contract_w streamed over r ascending: step(r) for r = 0..R-1, then finish")
+        out.append("  template <class T, int W>")
+        out.append(
+            "  __device__ __forceinline__ static void contract_w_step(Pack<T, W>* acc, "
+            "const Pack<T, W>& p, int r) {"
+        )
+        out.append("    using O = PackOps<T, W>;")
+        out.append("    switch (r) {")
+        for r, lines in enumerate(steps):
+            out.append(f"      case {r}:")
+            out.extend(lines)
+            out.append("        break;")
+        out.append("      default: break;")
+        out.append("    }")
+        out.append("    (void)sizeof(O);")
+        out.append("  }")
+        out.append("  template <class T, int W>")
+        out.append("  __device__ __forceinline__ static void contract_w_finish(Pack<T, W>* acc) {")
+        out.append("    using O = PackOps<T, W>;")
+        out.extend(finish)
+        out.append("    (void)acc; (void)sizeof(O);")
+        out.append("  }")
         out.append("  template <class T, int W>")
         out.append(
             "  __device__ __forceinline__ static void contract_w(const Pack<T, W>* p, Pack<T, W>* o) {"
