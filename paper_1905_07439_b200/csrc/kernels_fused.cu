@@ -641,41 +641,149 @@ cudaError_t launch_subtree2w(const void* x, const void* y, int64_t xy_tstride, i
 //              reference's order (_engine.py:104-112) streamed over r2.
 // Only the M x M leaf needs other lanes' data: the Y rows of the group,
 // exchanged with warp shuffles.  The leaf keeps the reference's k-ascending
-// order (_engine.py:42-61).  Level q0 (HBM <-> shared) is as in the SoA
-// kernel; X1/Y1 are position-major with a padded child stride RP so the
-// fiber loads of a warp hit distinct banks.  Z overwrites X1 in place: a
-// lane writes exactly the rows {hk*M + i} of block r1 it read.
-template <class F, class T, int M>
+// order (_engine.py:42-61).
+//
+// Shared memory holds the level-(q0+1) blocks X1, Y1 position-major
+// (element (block r, position p) at p * RP + r; RP pads R so the M rows a
+// warp loads at once fall in disjoint banks, and keeps 2-element alignment).
+// Positions are in the level-(q0+1) plan's BASE coordinates with the plan's
+// sign already applied: stage A writes each child element where stage B's
+// gather would read it, so stage B addresses are compile-time constants and
+// Z goes back unpermuted; stage C reads Z through the plan's scatter and
+// flips each child before contracting -- the same values the breadth-first
+// kernels produce.  Z overwrites X1 in place: a lane writes exactly the rows
+// {k*M + i} of block r1 it read.
+template <class F, class T, int M, int SUB, bool STG = false>
 struct SubtreeReg {
   static constexpr int n = F::n;
   static constexpr int R = F::R;
   static constexpr int s1 = M * n;
   static constexpr int s0 = s1 * n;
   static constexpr int kids1 = s1 * s1;
-  static constexpr int GPW = 32 / M;                // leaf-row groups per warp
-  static constexpr int NW = (R + GPW - 1) / GPW;    // one group per level-1 block
+  static constexpr int GPW = 32 / M;                      // leaf-row groups per warp
+  static constexpr int NW = (SUB * R + GPW - 1) / GPW;    // one group per level-1 block
   static constexpr int NT = NW * 32;
+  static constexpr int IA = (SUB * 2 * kids1 + NT - 1) / NT;  // stage-A items per thread
+  static constexpr int IC = (SUB * kids1 + NT - 1) / NT;      // stage-C items per thread
   // child stride: (s1 * RP) mod 32 spreads the M rows of a warp over disjoint banks
-  static constexpr int RP = (F::R == 23 && M == 3) ? 26 : R;
+  static constexpr int RP = (F::R == 23 && M == 3) ? 26 : R + (R & 1);
+  static constexpr int slot = 2 * kids1 * RP;             // X1 + Y1 of one subtree
+  // resident CTAs per SM the register budget aims at (about 128 registers a thread)
+  static constexpr int kMinBlocks = 65536 / (128 * NT) > 0 ? 65536 / (128 * NT) : 1;
   static constexpr size_t header() {
-    return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 5 * sizeof(GatherTab<n>);
+    return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 3 * sizeof(GatherTab<n>);
   }
-  static constexpr size_t smem_bytes() { return header() + sizeof(T) * (size_t)2 * kids1 * RP; }
+  // level-q0 blocks of the next subtree(s), prefetched with cp.async (4-byte
+  // elements only): [2 buffers][SUB][X, Y][s0 * s0]
+  static constexpr bool kStage = STG && sizeof(T) == 4;
+  static constexpr int stage_elems = kStage ? 2 * SUB * 2 * s0 * s0 : 0;
+  static constexpr size_t smem_bytes() {
+    return header() + sizeof(T) * ((size_t)SUB * slot + stage_elems);
+  }
 };
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 template <class T>
 __device__ __forceinline__ T shfl_val(T v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
 }
 
-template <class F, class T, int M>
-__global__ void __launch_bounds__(SubtreeReg<F, T, M>::NT) subtree_reg_kernel(
+template <int n>
+__device__ __forceinline__ GatherTab<n> load_tab(const GatherTab<n>& src) {
+  static_assert(sizeof(GatherTab<n>) % 16 == 0, "GatherTab is copied as int4");
+  GatherTab<n> t;
+  const int4* s = reinterpret_cast<const int4*>(&src);
+  int4* d = reinterpret_cast<int4*>(&t);
+#pragma unroll
+  for (int k = 0; k < (int)(sizeof(GatherTab<n>) / 16); ++k) d[k] = s[k];
+  return t;
+}
+
+// Stage-A item: one level-q0 position -> the R children, stored pairwise at
+// dst + r (dst 2-element aligned) with the level-(q0+1) sign m applied.
+template <class F, class T, int WHICH>
+__device__ __forceinline__ void expand_to_children(const T* __restrict__ src,
+                                                   const GatherTab<F::n>& gt, T* dst, uint32_t m) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  using O = PackOps<T, 1>;
+  Pack<T, 1> g[n * n];
+#pragma unroll
+  for (int k = 0; k < n * n; ++k) g[k] = O::flip(pload<T, 1>(src + gt.off[k]), gt.msk[k]);
+  Pack<T, 1> o[R];
+  if (WHICH == 0)
+    F::template expand_u<T, 1>(g, o, gt.lastrow, gt.lastcol);
+  else
+    F::template expand_v<T, 1>(g, o, gt.lastrow, gt.lastcol);
+#pragma unroll
+  for (int r = 0; r + 1 < R; r += 2) {
+    Pack<T, 2> v;
+    v.v[0] = flip_sign(o[r].v[0], m);
+    v.v[1] = flip_sign(o[r + 1].v[0], m);
+    pstore<T, 2>(dst + r, v);
+  }
+  if (R & 1) dst[R - 1] = flip_sign(o[R - 1].v[0], m);
+}
+
+// Leaf row of lane li (k ascending, first term initialises).
+// ROT = false: the three Y rows by 9 shuffles.
+// ROT = true (M = 3): the two foreign rows A, B by 6 shuffles; the X fiber
+// was loaded with its columns in (own, A, B) order, and two selects per
+// output put the row-2 term last (only the last operand of a 3-term fold
+// matters, the first two commute).
+template <class T, int M, bool ROT>
+__device__ __forceinline__ Pack<T, M> leaf_row(const Pack<T, M>& xg, const Pack<T, M>& yg,
+                                               int gbase, int srcA, int srcB, bool own_last) {
+  using A = Arith<T>;
+  Pack<T, M> m;
+  if constexpr (ROT) {
+    static_assert(M == 3, "rotated leaf is for 3x3 leaves");
+    Pack<T, M> ya, yb;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      ya.v[j] = shfl_val(yg.v[j], srcA);
+      yb.v[j] = shfl_val(yg.v[j], srcB);
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const T po = A::mul(xg.v[0], yg.v[j]);
+      const T pa = A::mul(xg.v[1], ya.v[j]);
+      const T pb = A::mul(xg.v[2], yb.v[j]);
+      const T first = own_last ? pb : po;
+      const T last = own_last ? po : pb;
+      m.v[j] = A::add(A::add(first, pa), last);
+    }
+  } else {
+    Pack<T, M> yr[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+#pragma unroll
+      for (int j = 0; j < M; ++j) yr[k].v[j] = shfl_val(yg.v[j], gbase + k);
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      T acc = A::mul(xg.v[0], yr[0].v[j]);
+#pragma unroll
+      for (int k = 1; k < M; ++k) acc = A::add(acc, A::mul(xg.v[k], yr[k].v[j]));
+      m.v[j] = acc;
+    }
+  }
+  return m;
+}
+
+template <class F, class T, int M, int SUB, bool ROT, bool STG>
+__global__ void __launch_bounds__(SubtreeReg<F, T, M, SUB, STG>::NT, SubtreeReg<F, T, M, SUB, STG>::kMinBlocks)
+subtree_reg_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0, int kchunk,
     T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
     int64_t ntr, uint8_t* __restrict__ nonfinite) {
-  using S = SubtreeReg<F, T, M>;
+  using S = SubtreeReg<F, T, M, SUB, STG>;
   using P = Pack<T, M>;
-  using A = Arith<T>;
   constexpr int n = F::n;
   constexpr int R = F::R;
   constexpr int s0 = S::s0, s1 = S::s1, kids1 = S::kids1, RP = S::RP, NT = S::NT;
@@ -683,17 +791,23 @@ __global__ void __launch_bounds__(SubtreeReg<F, T, M>::NT) subtree_reg_kernel(
   PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
   GatherTab<n>* tabs =
       reinterpret_cast<GatherTab<n>*>(smem_raw + ((sizeof(PlanLevel) * 2 + 15) / 16) * 16);
-  T* X1 = reinterpret_cast<T*>(smem_raw + S::header());
-  T* Y1 = X1 + kids1 * RP;
+  T* sm = reinterpret_cast<T*>(smem_raw + S::header());
 
-  // stage-B role of this lane
+  // stage-B role of this lane: group -> (subtree slot u, level-1 block r1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int gw = lane / M;
-  const int gbase = (gw < S::GPW ? gw : S::GPW - 1) * M;  // lanes past the last group mirror it
-  const int li = lane - gw * M < M ? lane - gw * M : 0;
-  int r1 = warp * S::GPW + (gw < S::GPW ? gw : S::GPW - 1);
-  const bool active = gw < S::GPW && r1 < R;
-  if (r1 >= R) r1 = R - 1;
+  const int gw = lane / M;
+  const int gwc = gw < S::GPW ? gw : S::GPW - 1;  // lanes past the last group mirror it
+  const int gbase = gwc * M;
+  const int li = gw < S::GPW ? lane - gw * M : (lane - gbase) % M;
+  int grp = warp * S::GPW + gwc;
+  const bool in_range = gw < S::GPW && grp < SUB * R;
+  if (grp >= SUB * R) grp = SUB * R - 1;
+  const int bu = grp / R, r1 = grp - (grp / R) * R;
+  // rotated leaf: foreign rows A, B and the column order of the X fiber
+  const int rowA = li == 2 ? 0 : 1 - li;
+  const int rowB = li == 2 ? 1 : 2;
+  const int col_of[3] = {li, rowA, rowB};
+  const int fib = bu * S::slot + li * s1 * RP + r1;  // lane's fiber origin
 
   const int kbeg = blockIdx.x * kchunk;
   const int kend = kbeg + kchunk < K0 ? kbeg + kchunk : K0;
@@ -706,132 +820,224 @@ __global__ void __launch_bounds__(SubtreeReg<F, T, M>::NT) subtree_reg_kernel(
       if (threadIdx.x < kWords) reinterpret_cast<int*>(spl)[threadIdx.x] = src[threadIdx.x];
     }
     __syncthreads();
-    if (threadIdx.x < 5) {
+    if (threadIdx.x < 3) {
       GatherTab<n> tab;
       switch (threadIdx.x) {
         case 0: make_gather<n, 0>(spl[0], s0, tab); break;  // level q0 (HBM, row-major)
         case 1: make_gather<n, 1>(spl[0], s0, tab); break;
-        case 2: make_scatter<n>(spl[0], s1, tab); break;
-        case 3: make_gather<n, 0>(spl[1], s1, tab); break;  // level q0+1 (fibers)
-        default: make_gather<n, 1>(spl[1], s1, tab); break;
+        default: make_scatter<n>(spl[0], s1, tab); break;
       }
       tabs[threadIdx.x] = tab;
     }
-    __syncthreads();
+    // per-thread item maps of this trial (level q0+1 plan: hatted -> base)
+    const PlanLevel& pl1 = spl[1];
+    int a_src[S::IA], a_dst[S::IA];
+    uint32_t a_msk[S::IA];
+#pragma unroll
+    for (int it = 0; it < S::IA; ++it) {
+      const int e0 = threadIdx.x + it * NT;
+      const int e = e0 < SUB * 2 * kids1 ? e0 : 0;
+      const int u = e / (2 * kids1);
+      const int eu = e - u * 2 * kids1;
+      const int which = eu >= kids1;
+      const int pos = eu - which * kids1;
+      const int row = pos / s1, col = pos - (pos / s1) * s1;
+      const int hk = row / M, hl = col / M;
+      const int ri = which ? 1 : 0, ci = which ? 2 : 1;
+      a_src[it] = u * s0 * s0 + row * s0 + col;
+      a_dst[it] = u * S::slot + which * kids1 * RP +
+                  ((pl1.perm[ri][hk] * M + (row - hk * M)) * s1 + pl1.perm[ci][hl] * M +
+                   (col - hl * M)) * RP;
+      a_msk[it] = sign_mask(pl1.neg[ri][hk] ^ pl1.neg[ci][hl]);
+    }
+    int c_src[S::IC];
+    uint32_t c_msk[S::IC];
+#pragma unroll
+    for (int it = 0; it < S::IC; ++it) {
+      const int e0 = threadIdx.x + it * NT;
+      const int e = e0 < SUB * kids1 ? e0 : 0;
+      const int u = e / kids1;
+      const int pos = e - u * kids1;
+      const int row = pos / s1, col = pos - (pos / s1) * s1;
+      const int hi = row / M, hj = col / M;
+      c_src[it] = u * S::slot +
+                  ((pl1.perm[0][hi] * M + (row - hi * M)) * s1 + pl1.perm[2][hj] * M +
+                   (col - hj * M)) * RP;
+      c_msk[it] = sign_mask(pl1.neg[0][hi] ^ pl1.neg[2][hj]);
+    }
     bool ok = true;
+    // staged copies of the level-q0 blocks: [buf][u][X, Y][s0 * s0]
+    T* stg = sm + SUB * S::slot;
+    constexpr int blkE = s0 * s0;
+    auto prefetch = [&](int kp, int buf) {
+      const int np = kend - kp < SUB ? kend - kp : SUB;
+      const int64_t blk = t * xy_tstride + (int64_t)kp * blkE;
+      T* dst = stg + buf * SUB * 2 * blkE;
+      for (int e = threadIdx.x; e < np * 2 * blkE; e += NT) {
+        const int u = e / (2 * blkE), r = e - u * 2 * blkE;
+        const int which = r >= blkE;
+        const T* src = (which ? y : x) + blk + u * blkE + (r - which * blkE);
+        cp_async4(dst + e, src);
+      }
+      cp_async_commit();
+    };
+    if (S::kStage && kbeg < kend) prefetch(kbeg, 0);
+    int buf = 0;
 
-    for (int k0 = kbeg; k0 < kend; ++k0) {
-      // ---- stage A: level q0 -> q0+1, HBM -> X1 / Y1 (position-major)
+    for (int k0 = kbeg; k0 < kend; k0 += SUB, buf ^= 1) {
+      const int nsub = kend - k0 < SUB ? kend - k0 : SUB;  // live subtree slots
+      if (S::kStage) cp_async_wait_all();
+      __syncthreads();
+      // ---- stage A: level q0 -> q0+1, level-q0 blocks -> X1 / Y1 (base order, signed)
       {
-        const T* xs = x + t * xy_tstride + (int64_t)k0 * s0 * s0;
-        const T* ys = y + t * xy_tstride + (int64_t)k0 * s0 * s0;
-        for (int e = threadIdx.x; e < 2 * kids1; e += NT) {
-          const int which = e >= kids1;
-          const int pos = e - which * kids1;
-          const int i = pos / s1, j = pos - (pos / s1) * s1;
-          if (which)
-            expand_tab<F, T, 1, 1>(ys + i * s0 + j, tabs[1], Y1 + pos * RP, 1);
-          else
-            expand_tab<F, T, 1, 0>(xs + i * s0 + j, tabs[0], X1 + pos * RP, 1);
+        const T* xsrc = S::kStage ? stg + buf * SUB * 2 * blkE : x + t * xy_tstride + (int64_t)k0 * blkE;
+        const T* ysrc = S::kStage ? xsrc + blkE : y + t * xy_tstride + (int64_t)k0 * blkE;
+        // staged: slot u of X at u * 2 * blkE, Y right after it
+        constexpr int ustride = S::kStage ? 2 * blkE : blkE;
+#pragma unroll
+        for (int it = 0; it < S::IA; ++it) {
+          const int e = threadIdx.x + it * NT;
+          if (e < nsub * 2 * kids1) {
+            const int u = e / (2 * kids1);
+            const int which = (e - u * 2 * kids1) >= kids1;
+            const int so = a_src[it] + u * (ustride - blkE);
+            if (which)
+              expand_to_children<F, T, 1>(ysrc + so, load_tab(tabs[1]), sm + a_dst[it], a_msk[it]);
+            else
+              expand_to_children<F, T, 0>(xsrc + so, load_tab(tabs[0]), sm + a_dst[it], a_msk[it]);
+          }
         }
       }
       __syncthreads();
+      if (S::kStage && k0 + SUB < kend) prefetch(k0 + SUB, buf ^ 1);
 
       // ---- stage B: level q0+1 -> leaves -> level q0+1, in registers
       {
-        const GatherTab<n>& gx = tabs[3];
-        const GatherTab<n>& gy = tabs[4];
+        const T* X1 = sm;
+        const T* Y1 = sm + kids1 * RP;
         P xf[n * n], yf[n * n];
 #pragma unroll
         for (int k = 0; k < n * n; ++k) {
-          const int ox = (gx.off[k] + li * s1) * RP + r1;
-          const int oy = (gy.off[k] + li * s1) * RP + r1;
-          const uint32_t mx = gx.msk[k], my = gy.msk[k];
+          const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
 #pragma unroll
           for (int j = 0; j < M; ++j) {
-            xf[k].v[j] = flip_sign(X1[ox + j * RP], mx);
-            yf[k].v[j] = flip_sign(Y1[oy + j * RP], my);
+            xf[k].v[j] = X1[o + (ROT ? col_of[j] : j) * RP];
+            yf[k].v[j] = Y1[o + j * RP];
           }
         }
-        const int xlr = gx.lastrow, xlc = gx.lastcol, ylr = gy.lastrow, ylc = gy.lastcol;
+        const int xlr = pl1.perm[0][n - 1], xlc = pl1.perm[1][n - 1];
+        const int ylr = pl1.perm[1][n - 1], ylc = pl1.perm[2][n - 1];
         P z[n * n];
 #pragma unroll
         for (int r2 = 0; r2 < R; ++r2) {
           const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
           const P yg = F::template expand_v1<T, M>(yf, r2, ylr, ylc);
-          P yr[M];
-#pragma unroll
-          for (int k = 0; k < M; ++k)
-#pragma unroll
-            for (int j = 0; j < M; ++j) yr[k].v[j] = shfl_val(yg.v[j], gbase + k);
-          P m;
-#pragma unroll
-          for (int j = 0; j < M; ++j) {
-            T acc = A::mul(xg.v[0], yr[0].v[j]);
-#pragma unroll
-            for (int k = 1; k < M; ++k) acc = A::add(acc, A::mul(xg.v[k], yr[k].v[j]));
-            m.v[j] = acc;
-          }
+          const P m = leaf_row<T, M, ROT>(xg, yg, gbase, gbase + rowA, gbase + rowB, li == 2);
           F::template contract_w_step<T, M>(z, m, r2);
         }
         F::template contract_w_finish<T, M>(z);
-        // scatter of level q0+1: base block (I, J) -> hatted (p1^-1(I), p3^-1(J))
-        const PlanLevel& pl1 = spl[1];
-        if (active) {
+        if (in_range && bu < nsub) {
+          T* Z1 = sm;
 #pragma unroll
-          for (int I = 0; I < n; ++I) {
-            const int hi = pl1.inv[0][I];
+          for (int k = 0; k < n * n; ++k) {
+            const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
 #pragma unroll
-            for (int J = 0; J < n; ++J) {
-              const int hj = pl1.inv[2][J];
-              const uint32_t msk = sign_mask(pl1.neg[0][hi] ^ pl1.neg[2][hj]);
-              const int o = ((hi * M + li) * s1 + hj * M) * RP + r1;
-#pragma unroll
-              for (int j = 0; j < M; ++j) X1[o + j * RP] = flip_sign(z[I * n + J].v[j], msk);
-            }
+            for (int j = 0; j < M; ++j) Z1[o + j * RP] = z[k].v[j];
           }
         }
       }
       __syncthreads();
 
-      // ---- stage C: level q0+1 -> q0, X1 -> HBM (row-major)
+      // ---- stage C: level q0+1 -> q0, Z1 -> HBM (row-major)
       {
-        T* dbase = out + (t * K0 + k0) * (int64_t)s0 * s0;
-        for (int pos = threadIdx.x; pos < kids1; pos += NT) {
-          const int i = pos / s1, j = pos - (pos / s1) * s1;
-          if (nonfinite)
-            ok = contract_tab<F, T, 1, true>(X1 + pos * RP, 1, dbase + i * s0 + j, tabs[2]) && ok;
-          else
-            contract_tab<F, T, 1, false>(X1 + pos * RP, 1, dbase + i * s0 + j, tabs[2]);
+        const GatherTab<n> sc = load_tab(tabs[2]);
+#pragma unroll
+        for (int it = 0; it < S::IC; ++it) {
+          const int e = threadIdx.x + it * NT;
+          if (e < nsub * kids1) {
+            using O = PackOps<T, 1>;
+            const int u = e / kids1, pos = e - (e / kids1) * kids1;
+            const T* zc = sm + c_src[it];
+            Pack<T, 1> pr[R];
+#pragma unroll
+            for (int r = 0; r + 1 < R; r += 2) {
+              const Pack<T, 2> v = pload<T, 2>(zc + r);
+              pr[r].v[0] = flip_sign(v.v[0], c_msk[it]);
+              pr[r + 1].v[0] = flip_sign(v.v[1], c_msk[it]);
+            }
+            if (R & 1) pr[R - 1].v[0] = flip_sign(zc[R - 1], c_msk[it]);
+            Pack<T, 1> o[n * n];
+            F::template contract_w<T, 1>(pr, o);
+            const int row = pos / s1, col = pos - (pos / s1) * s1;
+            T* d = out + (t * K0 + k0 + u) * (int64_t)s0 * s0 + row * s0 + col;
+#pragma unroll
+            for (int k = 0; k < n * n; ++k) {
+              const Pack<T, 1> val = O::flip(o[k], sc.msk[k]);
+              if (nonfinite) ok = ok && O::all_finite(val);
+              pstore<T, 1>(d + sc.off[k], val);
+            }
+          }
         }
       }
-      __syncthreads();
     }
     if (nonfinite && !ok) nonfinite[t] = 1;
   }
 }
 
-template <class F, class T, int M>
-cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
-                               void* out, const PlanLevel* plans, int64_t pts, int q0,
-                               int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
-  using S = SubtreeReg<F, T, M>;
+template <class F, class T, int M, int SUB, bool ROT, bool STG>
+cudaError_t launch_subtree_reg_v(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
+                                 void* out, const PlanLevel* plans, int64_t pts, int q0,
+                                 int64_t ntr, uint8_t* nonfinite, cudaStream_t st, int kchunk) {
+  using S = SubtreeReg<F, T, M, SUB, STG>;
   const size_t smem = S::smem_bytes();
-  auto kern = subtree_reg_kernel<F, T, M>;
+  auto kern = subtree_reg_kernel<F, T, M, SUB, ROT, STG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  // subtrees per CTA (one trial's plan tables are built once per chunk)
-  static const int kc_env = [] {
-    const char* v = getenv("RBC_SUBTREE_CHUNK");
-    return v ? atoi(v) : 0;
-  }();
-  int kchunk = kc_env > 0 ? kc_env : 8;
+  kchunk = ((kchunk + SUB - 1) / SUB) * SUB;
   if (kchunk > K0) kchunk = (int)K0;
   const int64_t nkc = (K0 + kchunk - 1) / kchunk;
   dim3 grid((unsigned)nkc, (unsigned)(ntr < 65535 ? ntr : 65535));
   kern<<<grid, S::NT, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, kchunk, (T*)out,
                                   plans, pts, q0, ntr, nonfinite);
   return cudaGetLastError();
+}
+
+// Tuning aids (config 2, ms per launch): RBC_SUBTREE_SUB subtrees per CTA
+// step (1: 3.28, 3: 3.82), RBC_SUBTREE_ROT=1 rotated 6-shuffle leaf (3.38),
+// RBC_SUBTREE_STAGE=1 cp.async prefetch of the level-q0 blocks (3.40),
+// RBC_SUBTREE_CHUNK subtrees per CTA (24; 8: 3.44, 48: 3.46).
+template <class F, class T, int M>
+cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
+                               void* out, const PlanLevel* plans, int64_t pts, int q0,
+                               int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
+  static const int sub = [] {
+    const char* v = getenv("RBC_SUBTREE_SUB");
+    return v ? atoi(v) : 1;
+  }();
+  static const int rot = [] {
+    const char* v = getenv("RBC_SUBTREE_ROT");
+    return v ? atoi(v) : 0;
+  }();
+  static const int kc = [] {
+    const char* v = getenv("RBC_SUBTREE_CHUNK");
+    return v ? atoi(v) : 0;
+  }();
+  static const int stg = [] {
+    const char* v = getenv("RBC_SUBTREE_STAGE");
+    return v ? atoi(v) : 0;
+  }();
+  const int kchunk = kc > 0 ? kc : 24;
+#define RBC_REG(SB, RT, SG)                                                                     \
+  if (sub == SB && (rot != 0) == RT && (stg != 0) == SG)                                        \
+    return launch_subtree_reg_v<F, T, M, SB, RT, SG>(x, y, xy_tstride, K0, out, plans, pts, q0, \
+                                                     ntr, nonfinite, st, kchunk);
+  RBC_REG(1, false, false)
+  RBC_REG(1, true, false)
+  RBC_REG(1, false, true)
+  RBC_REG(3, false, false)
+  RBC_REG(3, false, true)
+#undef RBC_REG
+  return cudaErrorInvalidValue;
 }
 
 template <class F, class T, int L, int M>
