@@ -288,10 +288,10 @@ def roofline(prof: dict, config: str, cfg=None, pairs=None, sm_max_mhz=None):
         bound, unit = ("cuda-core-" + key.split("_")[0] + "-exact-order"), "TFLOP/s"
         if stage == "truth_f64" and cfg is not None and cfg.mode.kind != "double":
             # narrow operands widened to binary64: products are exact, so the
-            # truth runs as DFMA (bit-identical); its pipe peak is 2x DMUL+DADD
-            peak = 2.0 * peaks["f64_tflops"]
+            # truth runs as DFMA (bit-identical); measured DFMA pipe peak
+            peak = peaks.get("dfma_f64_tflops", 2.0 * peaks["f64_tflops"])
             bound = "cuda-core-f64-dfma"
-            how += " x2 (DFMA)"
+            how += " (dfma_f64_tflops)"
     else:
         peak, how = measured_peaks()
         achieved = per_launch_bytes / avg_s / 1e9

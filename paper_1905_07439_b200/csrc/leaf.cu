@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) leaf_small_kernel(int64_t batch, int M, i
 
 // VW = elements per 16-byte fragment read.
 template <class TIn, class TAcc, int BM, int BN, int BK, int TM, int TN>
-__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), (BM / TM) * (BN / TN) >= 256 ? 2 : 4)
     leaf_tiled_kernel(int M, int K, int N, const TIn* __restrict__ x, int64_t xs,
                       const TIn* __restrict__ y, int64_t ys, TAcc* __restrict__ out,
                       int tiles_n) {
@@ -109,8 +109,14 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   static_assert(TM % VW == 0 && TN % VW == 0, "fragment width");
   using A = Arith<TAcc>;
 
-  __shared__ __align__(16) TAcc As[2][BK][BM];
-  __shared__ __align__(16) TAcc Bs[2][BK][BN];
+  // A is stored transposed (k-major).  A row of BM elements is a multiple of
+  // 32 banks, so the 16-byte pad spreads the k rows a warp stores at once
+  // over the banks (8-way -> conflict-free for f32, <= 3-way for f64) and
+  // keeps the 16-byte fragment loads aligned.
+  constexpr int APAD = 16 / (int)sizeof(TAcc);
+  extern __shared__ __align__(16) unsigned char leaf_smem[];
+  auto As = reinterpret_cast<TAcc(*)[BK][BM + APAD]>(leaf_smem);
+  auto Bs = reinterpret_cast<TAcc(*)[BK][BN]>(leaf_smem + sizeof(TAcc) * 2 * BK * (BM + APAD));
 
   const int tid = threadIdx.x;
   const int tx = tid % DX;
@@ -123,60 +129,66 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   const TIn* xb = x + b * xs;
   const TIn* yb = y + b * ys;
 
-  TAcc ra[A_PER];
-  TAcc rb[B_PER];
+  // staged in the input type (narrow operands are widened at the smem store)
+  TIn ra[A_PER];
+  TIn rb[B_PER];
   auto load_tile = [&](int k0) {
 #pragma unroll
     for (int q = 0; q < A_PER; ++q) {
       const int e = tid + q * NT;
       const int mm = e / BK, kk = e % BK;
       const int gm = m0 + mm, gk = k0 + kk;
-      ra[q] = (gm < M && gk < K) ? widen_to<TIn, TAcc>(xb[(int64_t)gm * K + gk]) : TAcc(0);
+      ra[q] = (gm < M && gk < K) ? xb[(int64_t)gm * K + gk] : TIn(0.0f);
     }
 #pragma unroll
     for (int q = 0; q < B_PER; ++q) {
       const int e = tid + q * NT;
       const int kk = e / BN, nn = e % BN;
       const int gk = k0 + kk, gn = n0 + nn;
-      rb[q] = (gk < K && gn < N) ? widen_to<TIn, TAcc>(yb[(int64_t)gk * N + gn]) : TAcc(0);
+      rb[q] = (gk < K && gn < N) ? yb[(int64_t)gk * N + gn] : TIn(0.0f);
     }
   };
   auto store_tile = [&](int buf) {
 #pragma unroll
     for (int q = 0; q < A_PER; ++q) {
       const int e = tid + q * NT;
-      As[buf][e % BK][e / BK] = ra[q];
+      As[buf][e % BK][e / BK] = widen_to<TIn, TAcc>(ra[q]);
     }
 #pragma unroll
     for (int q = 0; q < B_PER; ++q) {
       const int e = tid + q * NT;
-      Bs[buf][e / BN][e % BN] = rb[q];
+      Bs[buf][e / BN][e % BN] = widen_to<TIn, TAcc>(rb[q]);
     }
   };
 
   TAcc acc[TM][TN];
-  // one k step of the register tile: fragments from shared memory, then the
-  // TM x TN multiply-adds (the very first k initialises the accumulators)
-  auto kstep = [&](int buf, int kk, bool first) {
-    TAcc a[TM], bv[TN];
+  // register fragments; for binary64 accumulation double-buffered over k so
+  // the shared-memory loads of step k+1 are in flight during the DFMAs of
+  // step k (f32: the extra registers cost more occupancy than they hide)
+  constexpr bool kPipeFrag = sizeof(TAcc) == 8;
+  TAcc fa[2][TM], fb[2][TN];
+  auto load_frag = [&](int buf, int kk, int s) {
 #pragma unroll
     for (int g = 0; g < GM; ++g)
 #pragma unroll
-      for (int v = 0; v < VW; ++v) a[g * VW + v] = As[buf][kk][g * DY * VW + ty * VW + v];
+      for (int v = 0; v < VW; ++v) fa[s][g * VW + v] = As[buf][kk][g * DY * VW + ty * VW + v];
 #pragma unroll
     for (int g = 0; g < GN; ++g)
 #pragma unroll
-      for (int v = 0; v < VW; ++v) bv[g * VW + v] = Bs[buf][kk][g * DX * VW + tx * VW + v];
+      for (int v = 0; v < VW; ++v) fb[s][g * VW + v] = Bs[buf][kk][g * DX * VW + tx * VW + v];
+  };
+  // one k step of the register tile (the very first k initialises)
+  auto kstep = [&](int s, bool first) {
     if (first) {
 #pragma unroll
       for (int ii = 0; ii < TM; ++ii)
 #pragma unroll
-        for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = A::mul(a[ii], bv[jj]);
+        for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = A::mul(fa[s][ii], fb[s][jj]);
     } else {
 #pragma unroll
       for (int ii = 0; ii < TM; ++ii)
 #pragma unroll
-        for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = Mac<TIn, TAcc>::step(acc[ii][jj], a[ii], bv[jj]);
+        for (int jj = 0; jj < TN; ++jj) acc[ii][jj] = Mac<TIn, TAcc>::step(acc[ii][jj], fa[s][ii], fb[s][jj]);
     }
   };
   const int ktiles = (K + BK - 1) / BK;
@@ -187,9 +199,22 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     const int buf = kt & 1;
     if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
     const int kmax = min(BK, K - kt * BK);
+    if constexpr (kPipeFrag) {
+      load_frag(buf, 0, 0);
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk)
-      if (kk < kmax) kstep(buf, kk, kt == 0 && kk == 0);
+      for (int kk = 0; kk < BK; ++kk) {
+        if (kk + 1 < BK) load_frag(buf, kk + 1, (kk + 1) & 1);
+        if (kk < kmax) kstep(kk & 1, kt == 0 && kk == 0);
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        if (kk < kmax) {
+          load_frag(buf, kk, 0);
+          kstep(0, kt == 0 && kk == 0);
+        }
+      }
+    }
     if (kt + 1 < ktiles) {
       store_tile(buf ^ 1);
       __syncthreads();
@@ -444,6 +469,13 @@ cudaError_t run_tiled(int64_t batch, int64_t M, int64_t K, int64_t N, const void
   const int tiles_m = (int)((M + BM - 1) / BM);
   const int tiles_n = (int)((N + BN - 1) / BN);
   constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr size_t smem = sizeof(TAcc) * 2 * BK * ((BM + 16 / sizeof(TAcc)) + BN);
+  if (smem > 48 * 1024) {
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        leaf_tiled_kernel<TIn, TAcc, BM, BN, BK, TM, TN>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (attr != cudaSuccess) return attr;
+  }
   for (int64_t b0 = 0; b0 < batch; b0 += (int64_t)65535 * 65535) {
     const int64_t nb = batch - b0 < (int64_t)65535 * 65535 ? batch - b0 : (int64_t)65535 * 65535;
     const unsigned gy = (unsigned)(nb < 65535 ? nb : 65535);
@@ -453,14 +485,14 @@ cudaError_t run_tiled(int64_t batch, int64_t M, int64_t K, int64_t N, const void
     const int64_t full = (nb / 65535) * 65535;
     if (full > 0) {
       dim3 grid(tiles_m * tiles_n, 65535, (unsigned)(full / 65535));
-      leaf_tiled_kernel<TIn, TAcc, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(
+      leaf_tiled_kernel<TIn, TAcc, BM, BN, BK, TM, TN><<<grid, NT, smem, st>>>(
           (int)M, (int)K, (int)N, (const TIn*)x + b0 * xs, xs, (const TIn*)y + b0 * ys, ys,
           (TAcc*)out + b0 * M * N, tiles_n);
     }
     if (nb > full) {
       dim3 grid(tiles_m * tiles_n, (unsigned)(nb - full), 1);
       const int64_t bb = b0 + full;
-      leaf_tiled_kernel<TIn, TAcc, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(
+      leaf_tiled_kernel<TIn, TAcc, BM, BN, BK, TM, TN><<<grid, NT, smem, st>>>(
           (int)M, (int)K, (int)N, (const TIn*)x + bb * xs, xs, (const TIn*)y + bb * ys, ys,
           (TAcc*)out + bb * M * N, tiles_n);
     }
@@ -513,7 +545,10 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
   if (forced == 32 && M >= 32 && N >= 32)
     return run_tiled<TIn, TAcc, 32, 32, 8, 2, 2>(batch, M, K, N, x, xs, y, ys, out, st);
   if (forced == 1) return run_small<TIn, TAcc>(batch, M, K, N, x, xs, y, ys, out, st);
-  // binary64: 64x128 tiles of 4x8 outputs per thread (ncu: DP pipe ~72% busy)
+  // binary64: 128x64 tiles of 8x4 outputs per thread (truth 243: 15.3 vs
+  // 14.5 TFLOP/s for 64x128, 13.9 for 64x64; tools/leaf_bench.py)
+  if (sizeof(TAcc) == 8 && M >= 128 && N >= 64)
+    return run_tiled<TIn, TAcc, 128, 64, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
   if (sizeof(TAcc) == 8 && M >= 64 && N >= 128)
     return run_tiled<TIn, TAcc, 64, 128, 8, 4, 8>(batch, M, K, N, x, xs, y, ys, out, st);
   if (M >= 128 && N >= 128 && sizeof(TAcc) <= 4)

@@ -86,6 +86,24 @@ __global__ void __launch_bounds__(256) ffma_kernel(float* out, float seed) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void __launch_bounds__(256) dfma_kernel(double* out, float seed) {
+  double acc[kChains], a[kChains];
+  const double b = seed * 1e-3;
+#pragma unroll
+  for (int i = 0; i < kChains; ++i) {
+    acc[i] = 0.0;
+    a[i] = 1.0 + threadIdx.x * 1e-3 + i * 1e-4;
+  }
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) acc[i] = __fma_rn(acc[i], b, a[i]);
+  }
+  double s = acc[0];
+#pragma unroll
+  for (int i = 1; i < kChains; ++i) s += acc[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <class K>
 double time_kernel(K launch, int reps) {
   cudaEvent_t e0, e1;
@@ -117,18 +135,19 @@ int main() {
   double f64 = time_kernel([&] { mac_kernel<double><<<blocks, threads>>>((double*)buf, 1.f); }, 5);
   double f16 = time_kernel([&] { mac_kernel<__half2><<<blocks, threads>>>((__half2*)buf, 1.f); }, 5);
   double fma = time_kernel([&] { ffma_kernel<<<blocks, threads>>>((float*)buf, 1.f); }, 5);
+  double dfma = time_kernel([&] { dfma_kernel<<<blocks, threads>>>((double*)buf, 1.f); }, 5);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "CUDA error %s\n", cudaGetErrorString(e));
     return 1;
   }
   printf("{\"f32_tflops\": %.3f, \"f64_tflops\": %.3f, \"f16_tflops\": %.3f, "
-         "\"ffma_f32_tflops\": %.3f, \"sms\": %d, "
+         "\"ffma_f32_tflops\": %.3f, \"dfma_f64_tflops\": %.3f, \"sms\": %d, "
          "\"how\": \"tools/fp_peak.cu: %d x 256 threads, 16 independent acc=add(acc,mul(a,b)) chains "
          "with separately rounded multiply and add (half2 counts 4 flops), best of 5, CUDA events\"}\n",
          ops * Ops<float>::flops_per_op / (f32 * 1e-3) / 1e12,
          ops * Ops<double>::flops_per_op / (f64 * 1e-3) / 1e12,
          ops * Ops<__half2>::flops_per_op / (f16 * 1e-3) / 1e12, ops * 2.0 / (fma * 1e-3) / 1e12,
-         sms, blocks);
+         ops * 2.0 / (dfma * 1e-3) / 1e12, sms, blocks);
   return 0;
 }
