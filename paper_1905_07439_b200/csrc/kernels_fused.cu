@@ -673,21 +673,53 @@ struct SubtreeReg {
   static constexpr size_t header() {
     return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 3 * sizeof(GatherTab<n>);
   }
-  // level-q0 blocks of the next subtree(s), prefetched with cp.async (4-byte
-  // elements only): [2 buffers][SUB][X, Y][s0 * s0]
-  static constexpr bool kStage = STG && sizeof(T) == 4;
-  static constexpr int stage_elems = kStage ? 2 * SUB * 2 * s0 * s0 : 0;
+  // level-q0 blocks of the next subtree, prefetched by TMA bulk copies into
+  // [2 buffers][X, Y][span] (4-byte elements, one subtree per step): each
+  // block is copied as the 16-byte-aligned span that encloses it
+  static constexpr bool kStage = STG && sizeof(T) == 4 && SUB == 1;
+  static constexpr int spanE = ((s0 * s0 + 4) + 3) / 4 * 4;
+  static constexpr int stage_elems = kStage ? 2 * 2 * spanE : 0;
   static constexpr size_t smem_bytes() {
-    return header() + sizeof(T) * ((size_t)SUB * slot + stage_elems);
+    return header() + sizeof(T) * ((size_t)SUB * slot + stage_elems) + (kStage ? 16 : 0);
   }
 };
 
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+// global -> shared bulk copy (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// 16-byte span enclosing [p, p + bytes): start and length
+__device__ __forceinline__ const void* span_start(const void* p) {
+  return reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15);
+}
+__device__ __forceinline__ unsigned span_bytes(const void* p, unsigned bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  return (unsigned)(((a + bytes + 15) & ~(uintptr_t)15) - (a & ~(uintptr_t)15));
+}
 
 template <class T>
 __device__ __forceinline__ T shfl_val(T v, int src) {
@@ -811,6 +843,14 @@ subtree_reg_kernel(
 
   const int kbeg = blockIdx.x * kchunk;
   const int kend = kbeg + kchunk < K0 ? kbeg + kchunk : K0;
+  unsigned ctr = 0;  // staged steps consumed (buffer ctr & 1, phase (ctr >> 1) & 1)
+  if (S::kStage && threadIdx.x == 0) {
+    uint64_t* mb = reinterpret_cast<uint64_t*>(reinterpret_cast<T*>(smem_raw + S::header()) +
+                                               SUB * S::slot + S::stage_elems);
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    mbar_init_fence();
+  }
 
   for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
     __syncthreads();
@@ -866,50 +906,51 @@ subtree_reg_kernel(
       c_msk[it] = sign_mask(pl1.neg[0][hi] ^ pl1.neg[2][hj]);
     }
     bool ok = true;
-    // staged copies of the level-q0 blocks: [buf][u][X, Y][s0 * s0]
+    // staged copies of the level-q0 blocks: [buf][X, Y][spanE]
     T* stg = sm + SUB * S::slot;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(stg + S::stage_elems);
     constexpr int blkE = s0 * s0;
-    auto prefetch = [&](int kp, int buf) {
-      const int np = kend - kp < SUB ? kend - kp : SUB;
-      const int64_t blk = t * xy_tstride + (int64_t)kp * blkE;
-      T* dst = stg + buf * SUB * 2 * blkE;
-      for (int e = threadIdx.x; e < np * 2 * blkE; e += NT) {
-        const int u = e / (2 * blkE), r = e - u * 2 * blkE;
-        const int which = r >= blkE;
-        const T* src = (which ? y : x) + blk + u * blkE + (r - which * blkE);
-        cp_async4(dst + e, src);
-      }
-      cp_async_commit();
+    auto issue = [&](int kp, unsigned bsel) {  // one thread
+      const T* gx = x + t * xy_tstride + (int64_t)kp * blkE;
+      const T* gy = y + t * xy_tstride + (int64_t)kp * blkE;
+      const unsigned nx = span_bytes(gx, blkE * sizeof(T)), ny = span_bytes(gy, blkE * sizeof(T));
+      T* d = stg + bsel * 2 * S::spanE;
+      fence_proxy_async();
+      mbar_expect_tx(&mbar[bsel], nx + ny);
+      bulk_g2s(d, span_start(gx), nx, &mbar[bsel]);
+      bulk_g2s(d + S::spanE, span_start(gy), ny, &mbar[bsel]);
     };
-    if (S::kStage && kbeg < kend) prefetch(kbeg, 0);
-    int buf = 0;
+    if (S::kStage && threadIdx.x == 0 && kbeg < kend) issue(kbeg, ctr & 1);
 
-    for (int k0 = kbeg; k0 < kend; k0 += SUB, buf ^= 1) {
+    for (int k0 = kbeg; k0 < kend; k0 += SUB, ++ctr) {
       const int nsub = kend - k0 < SUB ? kend - k0 : SUB;  // live subtree slots
-      if (S::kStage) cp_async_wait_all();
+      if (S::kStage) mbar_wait(&mbar[ctr & 1], (ctr >> 1) & 1);
       __syncthreads();
       // ---- stage A: level q0 -> q0+1, level-q0 blocks -> X1 / Y1 (base order, signed)
       {
-        const T* xsrc = S::kStage ? stg + buf * SUB * 2 * blkE : x + t * xy_tstride + (int64_t)k0 * blkE;
-        const T* ysrc = S::kStage ? xsrc + blkE : y + t * xy_tstride + (int64_t)k0 * blkE;
-        // staged: slot u of X at u * 2 * blkE, Y right after it
-        constexpr int ustride = S::kStage ? 2 * blkE : blkE;
+        const T* gx = x + t * xy_tstride + (int64_t)k0 * blkE;
+        const T* gy = y + t * xy_tstride + (int64_t)k0 * blkE;
+        const T* xsrc = gx;
+        const T* ysrc = gy;
+        if (S::kStage) {
+          const T* d = stg + (ctr & 1) * 2 * S::spanE;
+          xsrc = d + ((reinterpret_cast<uintptr_t>(gx) & 15) / sizeof(T));
+          ysrc = d + S::spanE + ((reinterpret_cast<uintptr_t>(gy) & 15) / sizeof(T));
+        }
 #pragma unroll
         for (int it = 0; it < S::IA; ++it) {
           const int e = threadIdx.x + it * NT;
           if (e < nsub * 2 * kids1) {
-            const int u = e / (2 * kids1);
-            const int which = (e - u * 2 * kids1) >= kids1;
-            const int so = a_src[it] + u * (ustride - blkE);
+            const int which = (e - (e / (2 * kids1)) * 2 * kids1) >= kids1;
             if (which)
-              expand_to_children<F, T, 1>(ysrc + so, load_tab(tabs[1]), sm + a_dst[it], a_msk[it]);
+              expand_to_children<F, T, 1>(ysrc + a_src[it], load_tab(tabs[1]), sm + a_dst[it], a_msk[it]);
             else
-              expand_to_children<F, T, 0>(xsrc + so, load_tab(tabs[0]), sm + a_dst[it], a_msk[it]);
+              expand_to_children<F, T, 0>(xsrc + a_src[it], load_tab(tabs[0]), sm + a_dst[it], a_msk[it]);
           }
         }
       }
       __syncthreads();
-      if (S::kStage && k0 + SUB < kend) prefetch(k0 + SUB, buf ^ 1);
+      if (S::kStage && threadIdx.x == 0 && k0 + SUB < kend) issue(k0 + SUB, (ctr + 1) & 1);
 
       // ---- stage B: level q0+1 -> leaves -> level q0+1, in registers
       {
@@ -1002,9 +1043,237 @@ cudaError_t launch_subtree_reg_v(const void* x, const void* y, int64_t xy_tstrid
   return cudaGetLastError();
 }
 
+// ---- exchange-free variant: one lane per leaf ELEMENT -------------------------
+// Lane (r1, i, j) holds the X row-i fiber (X[i, k], k < M, of all n*n
+// sub-blocks of level-(q0+1) block r1), the Y column-j fiber (Y[k, j]) and
+// the Z element fiber (Z(I, J)[i, j]).  Every grandchild's leaf entry
+// M[i, j] = sum_k X[i, k] Y[k, j] (k ascending) is then lane-local: no
+// shuffles.  The price is redundant expansion work (each X row is expanded
+// by the M lanes j, each Y column by the M lanes i).  Lanes are independent,
+// so they pack densely (R * M * M per subtree).  Stages A and C and the
+// shared layout are those of subtree_reg_kernel, plus a separate Z1 buffer
+// (lanes of one row read the columns their neighbours write).
+template <class F, class T, int M, int SUB>
+struct SubtreeLane {
+  static constexpr int n = F::n;
+  static constexpr int R = F::R;
+  static constexpr int s1 = M * n;
+  static constexpr int s0 = s1 * n;
+  static constexpr int kids1 = s1 * s1;
+  static constexpr int LPC = M * M;                  // lanes per level-1 block
+  static constexpr int units = SUB * R * LPC;
+  static constexpr int NT = (units + 31) / 32 * 32;
+  static constexpr int IA = (SUB * 2 * kids1 + NT - 1) / NT;
+  static constexpr int IC = (SUB * kids1 + NT - 1) / NT;
+  static constexpr int RP = (F::R == 23 && M == 3) ? 26 : R + (R & 1);
+  static constexpr int slot = 3 * kids1 * RP;       // X1, Y1, Z1 of one subtree
+  static constexpr size_t header() {
+    return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 3 * sizeof(GatherTab<n>);
+  }
+  static constexpr size_t smem_bytes() { return header() + sizeof(T) * (size_t)SUB * slot; }
+};
+
+template <class F, class T, int M, int SUB>
+__global__ void __launch_bounds__(SubtreeLane<F, T, M, SUB>::NT) subtree_lane_kernel(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0, int kchunk,
+    T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
+    int64_t ntr, uint8_t* __restrict__ nonfinite) {
+  using S = SubtreeLane<F, T, M, SUB>;
+  using P = Pack<T, M>;
+  using P1 = Pack<T, 1>;
+  using A = Arith<T>;
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  constexpr int s0 = S::s0, s1 = S::s1, kids1 = S::kids1, RP = S::RP, NT = S::NT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
+  GatherTab<n>* tabs =
+      reinterpret_cast<GatherTab<n>*>(smem_raw + ((sizeof(PlanLevel) * 2 + 15) / 16) * 16);
+  T* sm = reinterpret_cast<T*>(smem_raw + S::header());
+
+  // stage-B role: unit -> (subtree slot bu, level-1 block r1, leaf element (i, j))
+  const bool unit_live = threadIdx.x < S::units;
+  const int uc = unit_live ? threadIdx.x : S::units - 1;
+  const int bu = uc / (R * S::LPC);
+  const int rem = uc - bu * (R * S::LPC);
+  const int r1 = rem / S::LPC;
+  const int le = rem - r1 * S::LPC;
+  const int li = le / M, lj = le - (le / M) * M;
+  const int fib = bu * S::slot + r1;
+
+  const int kbeg = blockIdx.x * kchunk;
+  const int kend = kbeg + kchunk < K0 ? kbeg + kchunk : K0;
+
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    __syncthreads();
+    {
+      constexpr int kWords = (int)(sizeof(PlanLevel) / 4) * 2;
+      const int* src = reinterpret_cast<const int*>(plans + t * plan_tstride + q0);
+      if (threadIdx.x < kWords) reinterpret_cast<int*>(spl)[threadIdx.x] = src[threadIdx.x];
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      GatherTab<n> tab;
+      switch (threadIdx.x) {
+        case 0: make_gather<n, 0>(spl[0], s0, tab); break;
+        case 1: make_gather<n, 1>(spl[0], s0, tab); break;
+        default: make_scatter<n>(spl[0], s1, tab); break;
+      }
+      tabs[threadIdx.x] = tab;
+    }
+    const PlanLevel& pl1 = spl[1];
+    int a_src[S::IA], a_dst[S::IA];
+    uint32_t a_msk[S::IA];
+#pragma unroll
+    for (int it = 0; it < S::IA; ++it) {
+      const int e0 = threadIdx.x + it * NT;
+      const int e = e0 < SUB * 2 * kids1 ? e0 : 0;
+      const int u = e / (2 * kids1);
+      const int eu = e - u * 2 * kids1;
+      const int which = eu >= kids1;
+      const int pos = eu - which * kids1;
+      const int row = pos / s1, col = pos - (pos / s1) * s1;
+      const int hk = row / M, hl = col / M;
+      const int ri = which ? 1 : 0, ci = which ? 2 : 1;
+      a_src[it] = u * s0 * s0 + row * s0 + col;
+      a_dst[it] = u * S::slot + which * kids1 * RP +
+                  ((pl1.perm[ri][hk] * M + (row - hk * M)) * s1 + pl1.perm[ci][hl] * M +
+                   (col - hl * M)) * RP;
+      a_msk[it] = sign_mask(pl1.neg[ri][hk] ^ pl1.neg[ci][hl]);
+    }
+    int c_src[S::IC];
+    uint32_t c_msk[S::IC];
+#pragma unroll
+    for (int it = 0; it < S::IC; ++it) {
+      const int e0 = threadIdx.x + it * NT;
+      const int e = e0 < SUB * kids1 ? e0 : 0;
+      const int u = e / kids1;
+      const int pos = e - u * kids1;
+      const int row = pos / s1, col = pos - (pos / s1) * s1;
+      const int hi = row / M, hj = col / M;
+      c_src[it] = u * S::slot + 2 * kids1 * RP +
+                  ((pl1.perm[0][hi] * M + (row - hi * M)) * s1 + pl1.perm[2][hj] * M +
+                   (col - hj * M)) * RP;
+      c_msk[it] = sign_mask(pl1.neg[0][hi] ^ pl1.neg[2][hj]);
+    }
+    bool ok = true;
+
+    for (int k0 = kbeg; k0 < kend; k0 += SUB) {
+      const int nsub = kend - k0 < SUB ? kend - k0 : SUB;
+      __syncthreads();
+      // ---- stage A: level q0 -> q0+1 (base order, signed)
+      {
+        const int64_t blk = t * xy_tstride + (int64_t)k0 * s0 * s0;
+#pragma unroll
+        for (int it = 0; it < S::IA; ++it) {
+          const int e = threadIdx.x + it * NT;
+          if (e < nsub * 2 * kids1) {
+            const int which = (e - (e / (2 * kids1)) * 2 * kids1) >= kids1;
+            if (which)
+              expand_to_children<F, T, 1>(y + blk + a_src[it], load_tab(tabs[1]), sm + a_dst[it], a_msk[it]);
+            else
+              expand_to_children<F, T, 0>(x + blk + a_src[it], load_tab(tabs[0]), sm + a_dst[it], a_msk[it]);
+          }
+        }
+      }
+      __syncthreads();
+
+      // ---- stage B: per lane, the leaf element (i, j) of all R grandchildren
+      {
+        const T* X1 = sm;
+        const T* Y1 = sm + kids1 * RP;
+        P xf[n * n], yf[n * n];
+#pragma unroll
+        for (int k = 0; k < n * n; ++k) {
+          const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
+#pragma unroll
+          for (int kk = 0; kk < M; ++kk) {
+            xf[k].v[kk] = X1[o + (li * s1 + kk) * RP];
+            yf[k].v[kk] = Y1[o + (kk * s1 + lj) * RP];
+          }
+        }
+        const int xlr = pl1.perm[0][n - 1], xlc = pl1.perm[1][n - 1];
+        const int ylr = pl1.perm[1][n - 1], ylc = pl1.perm[2][n - 1];
+        P1 z[n * n];
+#pragma unroll
+        for (int r2 = 0; r2 < R; ++r2) {
+          const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
+          const P yg = F::template expand_v1<T, M>(yf, r2, ylr, ylc);
+          P1 m;
+          T acc = A::mul(xg.v[0], yg.v[0]);
+#pragma unroll
+          for (int kk = 1; kk < M; ++kk) acc = A::add(acc, A::mul(xg.v[kk], yg.v[kk]));
+          m.v[0] = acc;
+          F::template contract_w_step<T, 1>(z, m, r2);
+        }
+        F::template contract_w_finish<T, 1>(z);
+        if (unit_live && bu < nsub) {
+          T* Z1 = sm + 2 * kids1 * RP;
+#pragma unroll
+          for (int k = 0; k < n * n; ++k)
+            Z1[((k / n) * M * s1 + (k % n) * M + li * s1 + lj) * RP + fib] = z[k].v[0];
+        }
+      }
+      __syncthreads();
+
+      // ---- stage C: level q0+1 -> q0, Z1 -> HBM (row-major)
+      {
+        const GatherTab<n> sc = load_tab(tabs[2]);
+#pragma unroll
+        for (int it = 0; it < S::IC; ++it) {
+          const int e = threadIdx.x + it * NT;
+          if (e < nsub * kids1) {
+            using O = PackOps<T, 1>;
+            const int u = e / kids1, pos = e - (e / kids1) * kids1;
+            const T* zc = sm + c_src[it];
+            P1 pr[R];
+#pragma unroll
+            for (int r = 0; r + 1 < R; r += 2) {
+              const Pack<T, 2> v = pload<T, 2>(zc + r);
+              pr[r].v[0] = flip_sign(v.v[0], c_msk[it]);
+              pr[r + 1].v[0] = flip_sign(v.v[1], c_msk[it]);
+            }
+            if (R & 1) pr[R - 1].v[0] = flip_sign(zc[R - 1], c_msk[it]);
+            P1 o[n * n];
+            F::template contract_w<T, 1>(pr, o);
+            const int row = pos / s1, col = pos - (pos / s1) * s1;
+            T* d = out + (t * K0 + k0 + u) * (int64_t)s0 * s0 + row * s0 + col;
+#pragma unroll
+            for (int k = 0; k < n * n; ++k) {
+              const P1 val = O::flip(o[k], sc.msk[k]);
+              if (nonfinite) ok = ok && O::all_finite(val);
+              pstore<T, 1>(d + sc.off[k], val);
+            }
+          }
+        }
+      }
+    }
+    if (nonfinite && !ok) nonfinite[t] = 1;
+  }
+}
+
+template <class F, class T, int M, int SUB>
+cudaError_t launch_subtree_lane_v(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
+                                  void* out, const PlanLevel* plans, int64_t pts, int q0,
+                                  int64_t ntr, uint8_t* nonfinite, cudaStream_t st, int kchunk) {
+  using S = SubtreeLane<F, T, M, SUB>;
+  const size_t smem = S::smem_bytes();
+  auto kern = subtree_lane_kernel<F, T, M, SUB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kchunk = ((kchunk + SUB - 1) / SUB) * SUB;
+  if (kchunk > K0) kchunk = (int)K0;
+  const int64_t nkc = (K0 + kchunk - 1) / kchunk;
+  dim3 grid((unsigned)nkc, (unsigned)(ntr < 65535 ? ntr : 65535));
+  kern<<<grid, S::NT, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, kchunk, (T*)out,
+                                  plans, pts, q0, ntr, nonfinite);
+  return cudaGetLastError();
+}
+
 // Tuning aids (config 2, ms per launch): RBC_SUBTREE_SUB subtrees per CTA
 // step (1: 3.28, 3: 3.82), RBC_SUBTREE_ROT=1 rotated 6-shuffle leaf (3.38),
-// RBC_SUBTREE_STAGE=1 cp.async prefetch of the level-q0 blocks (3.40),
+// RBC_SUBTREE_STAGE TMA bulk prefetch of the level-q0 blocks (default 1:
+// 3.01; 0: 3.28; per-element cp.async: 3.40),
 // RBC_SUBTREE_CHUNK subtrees per CTA (24; 8: 3.44, 48: 3.46).
 template <class F, class T, int M>
 cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
@@ -1024,10 +1293,20 @@ cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride,
   }();
   static const int stg = [] {
     const char* v = getenv("RBC_SUBTREE_STAGE");
-    return v ? atoi(v) : 0;
+    return v ? atoi(v) : 1;
   }();
   const int kchunk = kc > 0 ? kc : 24;
-#define RBC_REG(SB, RT, SG)                                                                     \
+  static const int lane = [] {
+    const char* v = getenv("RBC_SUBTREE_LANE");
+    return v ? atoi(v) : 0;
+  }();
+  if (lane == 1)
+    return launch_subtree_lane_v<F, T, M, 1>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr,
+                                             nonfinite, st, kchunk);
+  if (lane == 2)
+    return launch_subtree_lane_v<F, T, M, 2>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr,
+                                             nonfinite, st, kchunk);
+#define RBC_REG(SB, RT, SG)                                                                   \
   if (sub == SB && (rot != 0) == RT && (stg != 0) == SG)                                        \
     return launch_subtree_reg_v<F, T, M, SB, RT, SG>(x, y, xy_tstride, K0, out, plans, pts, q0, \
                                                      ntr, nonfinite, st, kchunk);
@@ -1035,7 +1314,6 @@ cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride,
   RBC_REG(1, true, false)
   RBC_REG(1, false, true)
   RBC_REG(3, false, false)
-  RBC_REG(3, false, true)
 #undef RBC_REG
   return cudaErrorInvalidValue;
 }
