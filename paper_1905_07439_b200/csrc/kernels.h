@@ -83,6 +83,13 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
                         int64_t N, const void* x, int64_t x_bstride, const void* y,
                         int64_t y_bstride, void* out, cudaStream_t st);
 
+// Binary64 product of binary64/32/16 operands on the DFMA pipe (truth.cu):
+// same contract as launch_leaf with dtype_out = f64; cudaErrorNotSupported
+// for empty shapes.
+cudaError_t launch_truth(int dtype_in, int64_t batch, int64_t M, int64_t K, int64_t N,
+                         const void* x, int64_t x_bstride, const void* y, int64_t y_bstride,
+                         void* out, cudaStream_t st);
+
 // ---- error check -----------------------------------------------------------
 // err[t] = ||widen(c[t]) - ref[t or 0]||_F / ||ref[t or 0]||_F   (binary64)
 // scratch: at least error_scratch_bytes(T) bytes of device memory.

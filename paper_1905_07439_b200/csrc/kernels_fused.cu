@@ -21,6 +21,7 @@
 
 #include "kernels.h"
 #include "plan_ops.cuh"
+#include "bulk.cuh"
 
 namespace rbc {
 
@@ -683,43 +684,6 @@ struct SubtreeReg {
     return header() + sizeof(T) * ((size_t)SUB * slot + stage_elems) + (kStage ? 16 : 0);
   }
 };
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_init_fence() {
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-// global -> shared bulk copy (16-byte aligned, size a multiple of 16)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-// 16-byte span enclosing [p, p + bytes): start and length
-__device__ __forceinline__ const void* span_start(const void* p) {
-  return reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15);
-}
-__device__ __forceinline__ unsigned span_bytes(const void* p, unsigned bytes) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  return (unsigned)(((a + bytes + 15) & ~(uintptr_t)15) - (a & ~(uintptr_t)15));
-}
 
 template <class T>
 __device__ __forceinline__ T shfl_val(T v, int src) {

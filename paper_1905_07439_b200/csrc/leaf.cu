@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.h"
 
@@ -236,6 +237,194 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), (BM / TM) * (BN / TN) >
           if (gn < N) ob[(int64_t)gm * N + gn] = acc[gi * VW + v][gj * VW + w];
         }
     }
+}
+
+// Binary64 accumulation (the truth, and binary64 leaves of 128 and up):
+// 128 x 128 x 16 tiles, 8 x 8 outputs per thread (64 independent chains),
+// one CTA of 256 threads per SM.  Warps are 4 (M) x 8 (N) threads, so every
+// 16-byte fragment load of a k step is one shared-memory wavefront (4 or 8
+// distinct 16-byte spans), i.e. 8 wavefronts per 64 DFMA warp instructions;
+// fragments are double-buffered over k.  Operands are widened to binary64 at
+// the shared-memory store (once per element per CTA), never in the k loop.
+// Every output keeps its own sequential k chain: the first product
+// initialises (a multiply, not an FMA into +0, which would lose the sign of
+// a -0 product) and K tails are skipped, not zero-padded (fl(-0 + 0*0) = +0).
+template <class TIn, int BM, int BN, int BK, int TM, int TN, bool PIPE, int MINB>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
+    truth_tiled_kernel(int M, int K, int N, const TIn* __restrict__ x, int64_t xs,
+                       const TIn* __restrict__ y, int64_t ys, double* __restrict__ out,
+                       int tiles_n) {
+  constexpr int VW = 2;           // doubles per 16-byte fragment load
+  constexpr int DY = BM / TM;     // thread rows
+  constexpr int DX = BN / TN;     // thread columns
+  constexpr int NT = DY * DX;
+  constexpr int GM = TM / VW, GN = TN / VW;
+  constexpr int A_PER = BM * BK / NT, B_PER = BK * BN / NT;
+  constexpr int WX = 8, WY = 4;   // warp shape (threads along N, M)
+  static_assert(NT % 32 == 0 && DX % WX == 0 && DY % WY == 0, "warp tiling");
+  static_assert(BM * BK % NT == 0 && BK * BN % NT == 0, "tile/threads");
+  constexpr int APAD = 2, BPAD = 2;
+  using Acc = Arith<double>;
+  extern __shared__ __align__(16) unsigned char leaf_smem[];
+  auto As = reinterpret_cast<double(*)[BK][BM + APAD]>(leaf_smem);
+  auto Bs = reinterpret_cast<double(*)[BK][BN + BPAD]>(leaf_smem + sizeof(double) * 2 * BK * (BM + APAD));
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  constexpr int WPX = DX / WX;  // warps along N
+  const int tx = (warp % WPX) * WX + (lane % WX);
+  const int ty = (warp / WPX) * WY + (lane / WX);
+  const int64_t b = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  const int tm = blockIdx.x / tiles_n;
+  const int tn = blockIdx.x - tm * tiles_n;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const TIn* xb = x + b * xs;
+  const TIn* yb = y + b * ys;
+
+  TIn ra[A_PER], rb[B_PER];
+  auto load_tile = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < A_PER; ++q) {
+      const int e = tid + q * NT;
+      const int mm = e / BK, kk = e % BK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      ra[q] = (gm < M && gk < K) ? xb[(int64_t)gm * K + gk] : TIn(0.0f);
+    }
+#pragma unroll
+    for (int q = 0; q < B_PER; ++q) {
+      const int e = tid + q * NT;
+      const int kk = e / BN, nn = e % BN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      rb[q] = (gk < K && gn < N) ? yb[(int64_t)gk * N + gn] : TIn(0.0f);
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < A_PER; ++q) {
+      const int e = tid + q * NT;
+      As[buf][e % BK][e / BK] = widen_to<TIn, double>(ra[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < B_PER; ++q) {
+      const int e = tid + q * NT;
+      Bs[buf][e / BN][e % BN] = widen_to<TIn, double>(rb[q]);
+    }
+  };
+
+  double acc[TM][TN];
+  double fa[PIPE ? 2 : 1][TM], fb[PIPE ? 2 : 1][TN];
+  auto load_frag = [&](int buf, int kk, int s) {
+#pragma unroll
+    for (int g = 0; g < GM; ++g) {
+      const double2 v = *reinterpret_cast<const double2*>(&As[buf][kk][g * DY * VW + ty * VW]);
+      fa[s][g * VW] = v.x;
+      fa[s][g * VW + 1] = v.y;
+    }
+#pragma unroll
+    for (int g = 0; g < GN; ++g) {
+      const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][kk][g * DX * VW + tx * VW]);
+      fb[s][g * VW] = v.x;
+      fb[s][g * VW + 1] = v.y;
+    }
+  };
+  auto kstep = [&](int s) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = Mac<TIn, double>::step(acc[i][j], fa[s][i], fb[s][j]);
+  };
+
+  const int ktiles = (K + BK - 1) / BK;
+  load_tile(0);
+  store_tile(0);
+  __syncthreads();
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
+    const int kmax = min(BK, K - kt * BK);
+    load_frag(buf, 0, 0);
+    if (kt == 0) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = Acc::mul(fa[0][i], fb[0][j]);
+    }
+    if (kmax == BK) {
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        if constexpr (PIPE) {
+          if (kk + 1 < BK) load_frag(buf, kk + 1, (kk + 1) & 1);
+          if (kk > 0 || kt > 0) kstep(kk & 1);
+        } else {
+          if (kk > 0) load_frag(buf, kk, 0);
+          if (kk > 0 || kt > 0) kstep(0);
+        }
+      }
+    } else {
+      // K tail: same chain, fewer steps
+#pragma unroll 1
+      for (int kk = 0; kk < kmax; ++kk) {
+        load_frag(buf, kk, 0);
+        if (kk > 0 || kt > 0) kstep(0);
+      }
+    }
+    if (kt + 1 < ktiles) {
+      store_tile(buf ^ 1);
+      __syncthreads();
+    }
+  }
+
+  double* ob = out + b * (int64_t)M * N;
+#pragma unroll
+  for (int gi = 0; gi < GM; ++gi)
+#pragma unroll
+    for (int v = 0; v < VW; ++v) {
+      const int gm = m0 + gi * DY * VW + ty * VW + v;
+      if (gm >= M) continue;
+#pragma unroll
+      for (int gj = 0; gj < GN; ++gj) {
+        const int gn = n0 + gj * DX * VW + tx * VW;
+        double* o = ob + (int64_t)gm * N + gn;
+        if (gn + 1 < N && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+          *reinterpret_cast<double2*>(o) = make_double2(acc[gi * VW + v][gj * VW], acc[gi * VW + v][gj * VW + 1]);
+        } else {
+          if (gn < N) o[0] = acc[gi * VW + v][gj * VW];
+          if (gn + 1 < N) o[1] = acc[gi * VW + v][gj * VW + 1];
+        }
+      }
+    }
+}
+
+template <class TIn, int BM, int BN, int BK, int TM, int TN, bool PIPE = true, int MINB = 1>
+cudaError_t run_truth(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
+                      const void* y, int64_t ys, void* out, cudaStream_t st) {
+  const int tiles_m = (int)((M + BM - 1) / BM);
+  const int tiles_n = (int)((N + BN - 1) / BN);
+  constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr size_t smem = sizeof(double) * 2 * BK * ((BM + 2) + (BN + 2));
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      truth_tiled_kernel<TIn, BM, BN, BK, TM, TN, PIPE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)smem);
+  if (attr != cudaSuccess) return attr;
+  for (int64_t b0 = 0; b0 < batch;) {
+    const int64_t nb = std::min<int64_t>(batch - b0, (int64_t)65535 * 65535);
+    const int64_t full = (nb / 65535) * 65535;
+    if (full > 0) {
+      dim3 grid(tiles_m * tiles_n, 65535, (unsigned)(full / 65535));
+      truth_tiled_kernel<TIn, BM, BN, BK, TM, TN, PIPE, MINB><<<grid, NT, smem, st>>>(
+          (int)M, (int)K, (int)N, (const TIn*)x + b0 * xs, xs, (const TIn*)y + b0 * ys, ys,
+          (double*)out + b0 * M * N, tiles_n);
+    }
+    if (nb > full) {
+      dim3 grid(tiles_m * tiles_n, (unsigned)(nb - full), 1);
+      const int64_t bb = b0 + full;
+      truth_tiled_kernel<TIn, BM, BN, BK, TM, TN, PIPE, MINB><<<grid, NT, smem, st>>>(
+          (int)M, (int)K, (int)N, (const TIn*)x + bb * xs, xs, (const TIn*)y + bb * ys, ys,
+          (double*)out + bb * M * N, tiles_n);
+    }
+    b0 += nb;
+  }
+  return cudaGetLastError();
 }
 
 // Small square leaves (M x M, M below a tile): one CTA stages LPB whole
@@ -545,6 +734,31 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
   if (forced == 32 && M >= 32 && N >= 32)
     return run_tiled<TIn, TAcc, 32, 32, 8, 2, 2>(batch, M, K, N, x, xs, y, ys, out, st);
   if (forced == 1) return run_small<TIn, TAcc>(batch, M, K, N, x, xs, y, ys, out, st);
+  if constexpr (sizeof(TAcc) == 8) {
+    // binary64 accumulation: from 512 up the widen pass + bulk-copy pipeline
+    // (truth.cu; 8192: 28.8 vs 24.9 TFLOP/s); below it the widen pass costs
+    // more than it saves (243 x 200: 15.8 vs 17.6) and the register-staged
+    // tile runs (tools/leaf_bench.py)
+    if (forced == 0 && M >= 512 && N >= 512 && K >= 1) {
+      const cudaError_t e = launch_truth(std::is_same<TIn, double>::value ? kF64
+                                         : std::is_same<TIn, float>::value ? kF32 : kF16,
+                                         batch, M, K, N, x, xs, y, ys, out, st);
+      if (e != cudaErrorNotSupported) return e;
+      return run_truth<TIn, 128, 128, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
+    }
+    if ((forced == 0 || forced == 302) && M >= 128 && N >= 128 && K >= 1)
+      return run_truth<TIn, 128, 128, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (forced == 303 && M >= 128 && N >= 128 && K >= 1)  // bulk kernel at any size
+      return launch_truth(std::is_same<TIn, double>::value ? kF64
+                          : std::is_same<TIn, float>::value ? kF32 : kF16,
+                          batch, M, K, N, x, xs, y, ys, out, st);
+    if (forced == 300 && M >= 128 && N >= 128 && K >= 1)
+      return run_truth<TIn, 128, 128, 16, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (forced == 301 && M >= 128 && N >= 128 && K >= 1)
+      return run_truth<TIn, 128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (forced == 306 && M >= 128 && N >= 128 && K >= 1)
+      return run_truth<TIn, 128, 128, 32, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+  }
   // binary64: 128x64 tiles of 8x4 outputs per thread (truth 243: 15.3 vs
   // 14.5 TFLOP/s for 64x128, 13.9 for 64x64; tools/leaf_bench.py)
   if (sizeof(TAcc) == 8 && M >= 128 && N >= 64)

@@ -53,7 +53,8 @@ def test_error_trials_match_oracle(name, N, Q, T):
         np.testing.assert_allclose(got["err_" + key][ok], want["err_" + key][ok], rtol=1e-12, atol=0)
 
 
-@pytest.mark.parametrize("label,N", [("f32", 243), ("f32", 256), ("f16", 200), ("f32", 37)])
+@pytest.mark.parametrize("label,N", [("f32", 243), ("f32", 256), ("f16", 200), ("f32", 37),
+                                     ("f64", 260), ("f32", 520), ("f16", 640)])
 def test_truth_bitwise(label, N):
     """The binary64 truth of narrow operands uses DFMA, which is exact here
     because every product of two widened f32/f16 values is exact in binary64:
@@ -76,6 +77,31 @@ def test_truth_bitwise(label, N):
     for t in range(3):
         want = oracle.standard_multiply(A[t].astype(np.float64), B[t].astype(np.float64))
         assert got[t].tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("tile", ["0", "303"])
+@pytest.mark.parametrize("shape", [(2, 130, 70, 257), (3, 128, 1, 128), (1, 300, 17, 140),
+                                   (2, 129, 300, 131), (1, 515, 40, 600)])
+def test_binary64_leaf_tiles_bitwise(shape, tile, monkeypatch):
+    """binary64 leaves of 128 and up run on the binary64 tile kernels with
+    DMUL + DADD (tile "303" forces the bulk-copy kernel at every size): ragged
+    M/N (pad rows never stored), K tails shorter than a k tile, K = 1 (the
+    initialising multiply only), broadcast operands."""
+    monkeypatch.setenv("RBC_LEAF_TILE", tile)
+    from paper_1905_07439_b200 import engine
+    from paper_1905_07439_b200.precision import DOUBLE
+
+    T, M, K, N = shape
+    g = np.random.default_rng(M * K + N)
+    x = g.standard_normal((T, M, K))
+    y = g.standard_normal((T, K, N))
+    x[0, :3, :] = -0.0  # products of -0 keep their sign on the first term
+    got = engine.leaf_matmul(x, y, DOUBLE)
+    want = oracle.leaf(x, y)
+    assert got.tobytes() == want.tobytes()
+    got_b = engine.leaf_matmul(x[:1], y, DOUBLE)  # x broadcast over the batch
+    want_b = oracle.leaf(x[:1], y)
+    assert got_b.tobytes() == want_b.tobytes()
 
 
 def test_device_runner_matches_host_call():

@@ -19,6 +19,9 @@ CASES = [  # (label, dtype_in, dtype_out, batch, m)
     ("truth f64<-f32 243", 1, 0, 200, 243),
     ("truth f64<-f32 2048", 1, 0, 2, 2048),
     ("truth f64<-f16 2048", 2, 0, 2, 2048),
+    ("truth f64<-f16 2048x16", 2, 0, 16, 2048),
+    ("truth f64<-f32 8192", 1, 0, 1, 8192),
+    ("truth f64<-f64 729", 0, 0, 8, 729),
     ("c3 leaf f64 27", 0, 0, 12167 * 16, 27),
 ]
 TORCH = {0: torch.float64, 1: torch.float32, 2: torch.float16}
