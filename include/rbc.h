@@ -155,6 +155,28 @@ int rbc_sum_trials_async(int dtype, int64_t T, int64_t N, const void* x, double*
 int rbc_nonfinite_async(int dtype, int64_t T, int64_t N, const void* x, uint8_t* nonfinite,
                         void* stream);
 
+/* ---- seeded test matrices on the device -------------
+ * Reference matgen.generate (pkg/src/randbc/matgen.py:55-97) over derive_rng
+ * (rng.py:20-23): out[c] (n x n, dtype, device) is bit-identical to the
+ * host draw of matrix `which[c]` (0 = A from derive_rng(mseed, 0), 1 = B from
+ * derive_rng(mseed, 1)) rounded into the mode, given the Philox key of that
+ * stream (keys[2c], keys[2c+1] = Philox(SeedSequence(..)).state key, host
+ * array).  kind: RBC_MAT_* (reference MATRIX_KINDS order, then the builder
+ * kinds).  nonfinite (device, optional, count bytes) gets 1 where the
+ * rounding into the mode overflowed (ScalarMode.array raises OverflowError).
+ * Synchronises `stream` (the ziggurat tail is evaluated on the host with the
+ * C library's log1p, as numpy does).  count <= 65535. */
+#define RBC_MAT_GAUSSIAN 0
+#define RBC_MAT_UNIFORM 1
+#define RBC_MAT_ADV1 2
+#define RBC_MAT_ADV2 3
+#define RBC_MAT_ADV3 4
+#define RBC_MAT_HILBERT 5
+#define RBC_MAT_UNIFORM_PM1 6
+#define RBC_MAT_QUADRANT100 7
+int rbc_matgen(int kind, int dtype, int64_t count, int64_t n, const uint64_t* keys,
+               const int32_t* which, void* out, uint8_t* nonfinite, void* stream);
+
 /* ---- error trials: the per-pair work of the distribution experiments ----
  * (experiments.py:248-261, 327-379): for each trial t with operands
  * (a[t], b[t]) in the mode, ref_t = binary64 inner-product truth, then the

@@ -50,6 +50,7 @@ EXPORTS = (
     "rbc_average_trials_workspace_bytes",
     "rbc_average_trials_async",
     "rbc_sum_trials_async",
+    "rbc_matgen",
 )
 
 _lock = threading.Lock()
@@ -102,6 +103,7 @@ def _declare(lib):
         "rbc_rel_errors_async": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
         "rbc_nonfinite_async": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp]),
         "rbc_sum_trials_async": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp]),
+        "rbc_matgen": (c_int, [c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
         "rbc_error_trials": (
             c_int,
             [c_int, c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp],

@@ -101,6 +101,21 @@ def get_config(name: str) -> TrialConfig:
         raise ValueError(f"unknown config {name!r}; choose from {sorted(CONFIGS)}") from None
 
 
+def pair_seeds(cfg: TrialConfig, first: int, count: int):
+    """Matrix seeds mseed of pairs first..first+count-1 (experiments.py:237-239)."""
+    return [derive_seed(cfg.seed, ROLE_MATRIX, p, kind_index(cfg.kind))
+            for p in range(first, first + count)]
+
+
+def make_pairs_device(cfg: TrialConfig, first: int, count: int, device="cuda:0"):
+    """Device twin of :func:`make_pairs`: (A, B) torch tensors (count, N, N)
+    in the mode dtype on ``device``, bit-identical to make_pairs (the matrices
+    are drawn on the GPU from the same Philox streams)."""
+    from .matgen import generate_device
+
+    return generate_device(cfg.kind, cfg.N, pair_seeds(cfg, first, count), cfg.mode, device)
+
+
 def make_pairs(cfg: TrialConfig, first: int, count: int, workers: int = 1):
     """(count, N, N) stacks of pairs first..first+count-1, mode dtype."""
     ids = list(range(first, first + count))

@@ -48,11 +48,6 @@ int fail_cuda(cudaError_t e, const char* expr, const char* file, int line) {
                    cudaGetErrorString(e), file, line, expr);
 }
 
-#define CUDA_TRY(expr)                                                      \
-  do {                                                                      \
-    cudaError_t _e = (expr);                                                \
-    if (_e != cudaSuccess) return fail_cuda(_e, #expr, __FILE__, __LINE__); \
-  } while (0)
 
 #define RBC_TRY(expr)          \
   do {                         \
@@ -560,6 +555,22 @@ int rbc_truth_async(int dtype_in, int64_t T, int64_t N, const void* a, const voi
                               (cudaStream_t)stream);
   if (e != cudaSuccess) return fail_cuda(e, "truth", __FILE__, __LINE__);
   return RBC_OK;
+}
+
+int rbc_matgen(int kind, int dtype, int64_t count, int64_t n, const uint64_t* keys,
+               const int32_t* which, void* out, uint8_t* nonfinite, void* stream) {
+  if (kind < kMatGaussian || kind > kMatQuadrant100)
+    return set_error(RBC_EVALUE, "unknown matrix kind %d", kind);
+  if (dtype != kF64 && dtype != kF32 && dtype != kF16)
+    return set_error(RBC_EVALUE, "unknown dtype %d", dtype);
+  if (count < 0 || n < 0 || count > 65535)
+    return set_error(RBC_EVALUE, "matrix count %lld / size %lld out of range", (long long)count,
+                     (long long)n);
+  if (count == 0 || n == 0) return RBC_OK;
+  if (n > (int64_t)1 << 24) return set_error(RBC_EVALUE, "matrix size %lld too large", (long long)n);
+  for (int64_t c = 0; c < count; ++c)
+    if (which[c] != 0 && which[c] != 1) return set_error(RBC_EVALUE, "which must be 0 (A) or 1 (B)");
+  return matgen(kind, dtype, count, n, keys, which, out, nonfinite, (cudaStream_t)stream);
 }
 
 size_t rbc_rel_errors_scratch_bytes(int64_t T) { return error_scratch_bytes(T); }

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "rbc.h"
 
 namespace rbc {
 
@@ -16,6 +17,14 @@ inline size_t dtype_size(int dt) { return dt == kF64 ? 8 : dt == kF32 ? 4 : 2; }
 
 // Records a CUDA failure as the thread's last error; returns RBC_ERUNTIME.
 int fail_cuda(cudaError_t e, const char* expr, const char* file, int line);
+
+#ifndef CUDA_TRY
+#define CUDA_TRY(expr)                                                      \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) return fail_cuda(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+#endif
 
 // ---- stage profiler (rbc_profile_enable) ------------------------------------
 // When enabled, Stage records a CUDA event pair around a launch on its stream,
@@ -89,6 +98,20 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
 cudaError_t launch_truth(int dtype_in, int64_t batch, int64_t M, int64_t K, int64_t N,
                          const void* x, int64_t x_bstride, const void* y, int64_t y_bstride,
                          void* out, cudaStream_t st);
+
+// ---- seeded test matrices (matgen.cu) -----------------------------------
+// Matrix families, in the order of reference MATRIX_KINDS (matgen.py:21)
+// followed by the builder kinds.
+enum MatgenKind : int {
+  kMatGaussian = 0, kMatUniform = 1, kMatAdv1 = 2, kMatAdv2 = 3, kMatAdv3 = 4, kMatHilbert = 5,
+  kMatUniformPm1 = 6, kMatQuadrant100 = 7
+};
+// out[c] (n x n, dtype) = the family's matrix drawn from the Philox stream
+// with key keys[2c], keys[2c+1] (host array), which[c] = 0 for A, 1 for B
+// (host array); flags (device, optional) set to 1 for non-finite results.
+// Synchronises the stream (the tail of the normal ziggurat runs on the host).
+int matgen(int kind, int dtype, int64_t count, int64_t n, const uint64_t* keys, const int* which,
+           void* out, uint8_t* flags, cudaStream_t st);
 
 // ---- error check -----------------------------------------------------------
 // err[t] = ||widen(c[t]) - ref[t or 0]||_F / ||ref[t or 0]||_F   (binary64)

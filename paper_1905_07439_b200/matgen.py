@@ -20,7 +20,8 @@ import numpy as np
 
 from .rng import derive_rng
 
-__all__ = ["MATRIX_KINDS", "BUILDER_KINDS", "MatrixSpec", "generate", "kind_index"]
+__all__ = ["MATRIX_KINDS", "BUILDER_KINDS", "MatrixSpec", "generate", "kind_index",
+           "philox_key", "generate_device"]
 
 MATRIX_KINDS = ("gaussian", "uniform", "adv1", "adv2", "adv3", "hilbert")
 BUILDER_KINDS = ("uniform_pm1", "quadrant100")
@@ -86,3 +87,58 @@ def generate(spec: MatrixSpec):
         sa = np.where(band, tiny, 1.0) * ones
         sb = sa
     return ga.random(sa.shape) * sa, gb.random(sb.shape) * sb
+
+
+def philox_key(seed: int, *path: int) -> tuple[int, int]:
+    """The 128-bit Philox key of ``derive_rng(seed, *path)`` (reference
+    rng.py:20-23): numpy's SeedSequence hashing, evaluated on the host."""
+    ss = np.random.SeedSequence(int(seed), spawn_key=tuple(int(p) for p in path))
+    key = np.random.Philox(ss).state["state"]["key"]
+    return int(key[0]), int(key[1])
+
+
+def generate_device(kind: str, size: int, seeds, mode, device="cuda:0", which=(0, 1)):
+    """Device twin of :func:`generate` over many seeds: returns a tuple of
+    torch tensors, one per entry of ``which`` (0 = A, 1 = B), each
+    (len(seeds), size, size) in the mode dtype on ``device``, bit-identical to
+    ``mode.array(generate(MatrixSpec(kind, size, seed))[w])`` (librbc
+    rbc_matgen: Philox4x64-10 and numpy's ziggurat on the device, SURVEY §8f
+    rank 4).  Raises OverflowError where the rounding into the mode overflows,
+    like ``mode.array``."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .precision import dtype_code, mode_of
+
+    if kind not in MATRIX_KINDS + BUILDER_KINDS:
+        raise ValueError(f"unknown matrix kind: {kind!r}")
+    m = mode_of(mode)
+    seeds = [int(s) for s in seeds]
+    for sd in seeds:
+        MatrixSpec(kind, size, sd)  # same validation as the host path
+    tdt = {"double": torch.float64, "single": torch.float32, "half": torch.float16}[m.kind]
+    dev = torch.device(device)
+    lib = _lib.load()
+    code = (MATRIX_KINDS + BUILDER_KINDS).index(kind)
+    outs = []
+    for w in which:
+        out = torch.empty((len(seeds), size, size), dtype=tdt, device=dev)
+        flags = torch.zeros(max(1, len(seeds)), dtype=torch.uint8, device=dev)
+        for c0 in range(0, len(seeds), 65535):
+            part = seeds[c0:c0 + 65535]
+            keys = np.array([philox_key(sd, w) for sd in part], dtype=np.uint64).reshape(-1)
+            wh = np.full(len(part), w, dtype=np.int32)
+            with torch.cuda.device(dev):
+                st = torch.cuda.current_stream(dev).cuda_stream
+                rc = lib.rbc_matgen(code, dtype_code(m), len(part), size,
+                                    keys.ctypes.data_as(ctypes.c_void_p),
+                                    wh.ctypes.data_as(ctypes.c_void_p),
+                                    ctypes.c_void_p(out[c0:].data_ptr()),
+                                    ctypes.c_void_p(flags[c0:].data_ptr()), ctypes.c_void_p(st))
+            _lib.check(rc)
+        if len(seeds) and bool(flags.any()):
+            raise OverflowError(f"value outside {m.label} range")
+        outs.append(out)
+    return tuple(outs)
