@@ -528,6 +528,27 @@ class AverageWorkload:
         return ms, h2d, d2h
 
 
+def device_inputs(cfg, first, T, A, B, host_s, workers):
+    """Informational: the same operand pairs drawn on the GPU (rbc_matgen,
+    SURVEY §8f rank 4) -- time and bitwise agreement with the host draw that
+    feeds the timed region."""
+    import torch
+
+    from paper_1905_07439_b200.configs import make_pairs_device
+
+    make_pairs_device(cfg, first, min(T, 2))  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dA, dB = make_pairs_device(cfg, first, T)
+    torch.cuda.synchronize()
+    dev_s = time.perf_counter() - t0
+    same = (dA.cpu().numpy().tobytes() == A.tobytes() and dB.cpu().numpy().tobytes() == B.tobytes())
+    del dA, dB
+    return {"kind": cfg.kind, "device_matgen_ms": round(dev_s * 1e3, 2),
+            "host_numpy_ms": round(host_s * 1e3, 1), "host_workers": workers,
+            "bitwise_equal": same}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -552,7 +573,10 @@ def run_ours(args):
     first, _ = distributed.shard(rank, world, T)
     pair_ids = distributed.pair_ids(rank, world, T)
     workers = min(32, max(1, (os.cpu_count() or 2) // max(1, world)))
+    t_host = time.perf_counter()
     A, B = make_pairs(cfg, first, T, workers=workers)
+    t_host = time.perf_counter() - t_host
+    inputs = device_inputs(cfg, first, T, A, B, t_host, workers)
     kind = AverageWorkload if cfg.plans_per_pair > 1 else ErrorTrialWorkload
     wl = kind(cfg, pair_ids, A, B, dev, torch)
     stream = torch.cuda.Stream(device=dev)
@@ -614,6 +638,7 @@ def run_ours(args):
                   "at these batch sizes, so no explicit flush is used",
         },
         "gpu_launches": launches,
+        "inputs": inputs,
         "clocks": clk,
         "roofline": roofline(prof, cfg.name, cfg, T, clk.get("sm_max_mhz")),
         "errors": distributed.trial_stats(allerr[0], alldet[0], allerr[1] > 0, alldet[1] > 0),

@@ -262,7 +262,12 @@ struct NoEmit {
   __device__ void operator()(int, double) const {}
 };
 
-// per chunk: exit offset and sample count from each entry offset
+// per chunk: exit offset and sample count from each entry offset.  Entry 0
+// is parsed in full, recording which chunk positions it reads an r word at
+// (rmask) and which of those emitted a sample (emask); a parse from entry e
+// stops as soon as it reads an r word at one of those positions -- from there
+// on it is entry 0's parse -- so nearly every extra entry costs a step or two.
+static_assert(kChunk == 64, "position masks are 64-bit");
 __global__ void __launch_bounds__(256) chunk_maps_kernel(int64_t Wn, int64_t J,
                                                          const uint64_t* __restrict__ W, TailTab tt,
                                                          int* __restrict__ exits,
@@ -271,12 +276,39 @@ __global__ void __launch_bounds__(256) chunk_maps_kernel(int64_t Wn, int64_t J,
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= J) return;
   const uint64_t* w = W + (int64_t)m * Wn;
+  const int64_t base = (int64_t)m * Wn;
   const int64_t c0 = j * kChunk, end = c0 + kChunk;
   const int64_t o = ((int64_t)m * J + j) * kEntries;
-  for (int e = 0; e < kEntries; ++e) {
+  uint64_t rmask = 0, emask = 0;
+  int cnt0 = 0;
+  int64_t p = c0;
+  // entry 0, recording its r-read positions
+  while (p < end) {
+    const int at = (int)(p - c0);
+    rmask |= 1ull << at;
+    int one = 0;
+    const int64_t q = parse_words(w, base, p, p + 1, tt, one, NoEmit{});
+    if (one) emask |= 1ull << at;
+    cnt0 += one;
+    p = q;
+  }
+  const int exit0 = (int)(p - end);
+  exits[o] = exit0;
+  cnts[o] = cnt0;
+  for (int e = 1; e < kEntries; ++e) {
     int cnt = 0;
-    const int64_t p = parse_words(w, (int64_t)m * Wn, c0 + e, end, tt, cnt, NoEmit{});
-    exits[o + e] = (int)(p - end);
+    int64_t q = c0 + e;
+    bool merged = false;
+    while (q < end) {
+      const int at = (int)(q - c0);
+      if ((rmask >> at) & 1) {
+        cnt += __popcll(emask >> at);
+        merged = true;
+        break;
+      }
+      q = parse_words(w, base, q, q + 1, tt, cnt, NoEmit{});
+    }
+    exits[o + e] = merged ? exit0 : (int)(q - end);
     cnts[o + e] = cnt;
   }
 }

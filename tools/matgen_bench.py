@@ -17,7 +17,10 @@ CASES = [("c1", 100, 100), ("c2", 1000, 100), ("c3", 4, 4), ("c4", 16, 2), ("c5"
 
 
 def main():
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     for name, pairs, host_pairs in CASES:
+        if only and name != only:
+            continue
         cfg = get_config(name)
         make_pairs_device(cfg, 1, min(pairs, 2))  # warm-up
         torch.cuda.synchronize()
