@@ -221,7 +221,7 @@ def fp_peaks():
     if p.exists():
         return json.loads(p.read_text()), "measured (profiles/fp_peaks.json)"
     return {"f32_tflops": FP32_NOMINAL_TFLOPS, "f64_tflops": FP32_NOMINAL_TFLOPS / 2,
-            "f16_tflops": FP32_NOMINAL_TFLOPS * 2}, "nominal"
+            "f16_tflops": FP32_NOMINAL_TFLOPS}, "nominal (half2 issues at half the FP32 rate)"
 
 
 def ncu_traffic(stage: str, config: str):

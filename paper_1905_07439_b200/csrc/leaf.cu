@@ -625,6 +625,174 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   }
 }
 
+// binary16 leaves, issue-bound variant: exact-order HMUL2/HADD2 run at one
+// instruction per clock per SM sub-partition, so every non-FP instruction in
+// the k loop costs throughput.  A is stored in shared memory transposed and
+// pre-broadcast as (a, a) half2 pairs, so the row fragment is two 16-byte
+// loads with no per-k shuffles; each thread owns TM rows x TN columns
+// (TN/2 half2 accumulators per row) for 2*TM*TN/2 FP instructions per four
+// fragment loads.  Operand tiles move as 16-byte vectors (K, N multiples of
+// 8), double-buffered through registers.  Same per-element chains as
+// leaf_tiled_h2_kernel: k ascending, first product initialises.
+template <int BM, int BN, int BK, int TM, int TN, int MINB>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
+    leaf_h2dup_kernel(int M, int K, int N, const __half* __restrict__ x, int64_t xs,
+                      const __half* __restrict__ y, int64_t ys, __half* __restrict__ out,
+                      int tiles_n) {
+  constexpr int DY = BM / TM, DX = BN / TN;
+  constexpr int NT = DY * DX;
+  constexpr int TN2 = TN / 2;
+  constexpr int AV = BM * BK / 8 / NT;  // 16-byte A vectors per thread per tile
+  constexpr int BV = BK * BN / 8 / NT;
+  static_assert(AV >= 1 && BV >= 1 && BM * BK % (8 * NT) == 0 && BK * BN % (8 * NT) == 0, "tiles");
+  static_assert(TM % 4 == 0 && TN2 % 4 == 0, "16-byte fragments");
+  constexpr int APAD = 4;  // half2 pad per k row (bank spread of the transposed stores)
+  __shared__ __align__(16) __half2 As[2][BK][BM + APAD];
+  __shared__ __align__(16) __half Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid % DX, ty = tid / DX;
+  const int64_t b = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const __half* xb = x + b * xs;
+  const __half* yb = y + b * ys;
+  uint4 ra[AV], rb[BV];
+  auto load_tile = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < AV; ++q) {
+      const int v = tid + q * NT;
+      const int mm = v / (BK / 8), kk = (v % (BK / 8)) * 8;
+      const int gm = m0 + mm, gk = k0 + kk;
+      ra[q] = (gm < M && gk < K) ? *reinterpret_cast<const uint4*>(xb + (int64_t)gm * K + gk)
+                                 : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < BV; ++q) {
+      const int v = tid + q * NT;
+      const int kk = v / (BN / 8), nn = (v % (BN / 8)) * 8;
+      const int gk = k0 + kk, gn = n0 + nn;
+      rb[q] = (gk < K && gn < N) ? *reinterpret_cast<const uint4*>(yb + (int64_t)gk * N + gn)
+                                 : make_uint4(0, 0, 0, 0);
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < AV; ++q) {
+      const int v = tid + q * NT;
+      const int mm = v / (BK / 8), kk = (v % (BK / 8)) * 8;
+      const __half* h = reinterpret_cast<const __half*>(&ra[q]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) As[buf][kk + e][mm] = __half2half2(h[e]);
+    }
+#pragma unroll
+    for (int q = 0; q < BV; ++q) {
+      const int v = tid + q * NT;
+      const int kk = v / (BN / 8), nn = (v % (BN / 8)) * 8;
+      *reinterpret_cast<uint4*>(&Bs[buf][kk][nn]) = rb[q];
+    }
+  };
+  __half2 acc[TM][TN2];
+  auto kstep = [&](int buf, int kk, bool first) {
+    __half2 a2[TM], b2[TN2];
+#pragma unroll
+    for (int g = 0; g < TM / 4; ++g) {
+      const uint4 v = *reinterpret_cast<const uint4*>(&As[buf][kk][ty * TM + 4 * g]);
+      const __half2* p = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) a2[4 * g + e] = p[e];
+    }
+#pragma unroll
+    for (int g = 0; g < TN2 / 4; ++g) {
+      const uint4 v = *reinterpret_cast<const uint4*>(&Bs[buf][kk][tx * TN + 8 * g]);
+      const __half2* p = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) b2[4 * g + e] = p[e];
+    }
+    if (first) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN2; ++j) acc[i][j] = __hmul2_rn(a2[i], b2[j]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN2; ++j) acc[i][j] = __hadd2_rn(acc[i][j], __hmul2_rn(a2[i], b2[j]));
+    }
+  };
+  const int ktiles = (K + BK - 1) / BK;
+  load_tile(0);
+  store_tile(0);
+  __syncthreads();
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
+    if ((kt + 1) * BK <= K) {
+      if (kt == 0) {
+        kstep(buf, 0, true);
+#pragma unroll
+        for (int kk = 1; kk < BK; ++kk) kstep(buf, kk, false);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) kstep(buf, kk, false);
+      }
+    } else {
+      const int kmax = K - kt * BK;
+      for (int kk = 0; kk < kmax; ++kk) kstep(buf, kk, kt == 0 && kk == 0);
+    }
+    if (kt + 1 < ktiles) {
+      store_tile(buf ^ 1);
+      __syncthreads();
+    }
+  }
+  __half* ob = out + b * (int64_t)M * N;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int gm = m0 + ty * TM + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int g = 0; g < TN2 / 4; ++g) {
+      const int gn = n0 + tx * TN + 8 * g;
+      if (gn + 8 <= N) {
+        *reinterpret_cast<uint4*>(&ob[(int64_t)gm * N + gn]) = *reinterpret_cast<const uint4*>(&acc[i][4 * g]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (gn + 2 * e < N) ob[(int64_t)gm * N + gn + 2 * e] = __low2half(acc[i][4 * g + e]);
+          if (gn + 2 * e + 1 < N) ob[(int64_t)gm * N + gn + 2 * e + 1] = __high2half(acc[i][4 * g + e]);
+        }
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int BK, int TM, int TN, int MINB>
+cudaError_t run_h2dup(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
+                      const void* y, int64_t ys, void* out, cudaStream_t st) {
+  const int tiles_m = (int)((M + BM - 1) / BM);
+  const int tiles_n = (int)((N + BN - 1) / BN);
+  constexpr int NT = (BM / TM) * (BN / TN);
+  for (int64_t b0 = 0; b0 < batch;) {
+    const int64_t nb = std::min<int64_t>(batch - b0, (int64_t)65535 * 65535);
+    const int64_t full = (nb / 65535) * 65535;
+    if (full > 0) {
+      dim3 grid(tiles_m * tiles_n, 65535, (unsigned)(full / 65535));
+      leaf_h2dup_kernel<BM, BN, BK, TM, TN, MINB><<<grid, NT, 0, st>>>(
+          (int)M, (int)K, (int)N, (const __half*)x + b0 * xs, xs, (const __half*)y + b0 * ys, ys,
+          (__half*)out + b0 * M * N, tiles_n);
+    }
+    if (nb > full) {
+      dim3 grid(tiles_m * tiles_n, (unsigned)(nb - full), 1);
+      const int64_t bb = b0 + full;
+      leaf_h2dup_kernel<BM, BN, BK, TM, TN, MINB><<<grid, NT, 0, st>>>(
+          (int)M, (int)K, (int)N, (const __half*)x + bb * xs, xs, (const __half*)y + bb * ys, ys,
+          (__half*)out + bb * M * N, tiles_n);
+    }
+    b0 += nb;
+  }
+  return cudaGetLastError();
+}
+
 template <int BM, int BN, int BK, int TM, int TN>
 cudaError_t run_tiled_h2(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
                          const void* y, int64_t ys, void* out, cudaStream_t st) {
@@ -792,6 +960,18 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
   if (dtype_out == kF32 && dtype_in == kF32)
     return leaf_dispatch<float, float>(batch, M, K, N, x, xs, y, ys, out, st);
   if (dtype_out == kF16 && dtype_in == kF16) {
+    // 16-byte operand vectors need K, N multiples of 8 and aligned strides
+    const bool vec = K % 8 == 0 && N % 8 == 0 && (xs % 8 == 0 || batch == 1) &&
+                     (ys % 8 == 0 || batch == 1) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
+    const int forced = tile_override();
+    if (vec && M >= 128 && N >= 128 && (forced == 0 || forced == 401))
+      return run_h2dup<128, 128, 16, 8, 16, 3>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (vec && M >= 128 && N >= 128 && forced == 402)
+      return run_h2dup<128, 128, 16, 8, 16, 2>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (vec && M >= 64 && N >= 64 && forced == 403)
+      return run_h2dup<64, 64, 16, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (vec && M >= 128 && N >= 128 && forced == 404)
+      return run_h2dup<128, 64, 16, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
     if (M >= 128 && N >= 128)
       return run_tiled_h2<128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
     if (M >= 64 && N >= 64)

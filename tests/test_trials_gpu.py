@@ -104,6 +104,30 @@ def test_binary64_leaf_tiles_bitwise(shape, tile, monkeypatch):
     assert got_b.tobytes() == want_b.tobytes()
 
 
+@pytest.mark.parametrize("tile", ["0", "402", "403", "404", "999"])
+@pytest.mark.parametrize("shape", [(3, 128, 128, 128), (1, 256, 64, 136), (2, 130, 24, 200),
+                                   (1, 128, 40, 128), (1, 128, 13, 128)])
+def test_binary16_leaf_tiles_bitwise(shape, tile, monkeypatch):
+    """binary16 leaves of 128 and up (config 4's leaves): the half2 tile
+    kernels against the oracle's per-operation rounding, with ragged M/N, K
+    tails (K not a multiple of the k tile; K = 13 falls back to the scalar
+    loads), overflow to inf and signed zeros."""
+    from paper_1905_07439_b200 import engine
+    from paper_1905_07439_b200.precision import HALF
+
+    monkeypatch.setenv("RBC_LEAF_TILE", tile)
+    T, M, K, N = shape
+    g = np.random.default_rng(M + 7 * K + N)
+    x = HALF.array(g.standard_normal((T, M, K)) * 8)
+    y = HALF.array(g.standard_normal((T, K, N)) * 8)
+    x[0, :2, :] = -0.0
+    x[0, 5, :] = 200.0  # row 5 overflows to +-inf
+    with np.errstate(all="ignore"):
+        got = engine.leaf_matmul(x, y, HALF)
+        want = oracle.leaf(x, y)
+    assert got.tobytes() == want.tobytes()
+
+
 def test_device_runner_matches_host_call():
     import torch
 

@@ -15,7 +15,7 @@ from paper_1905_07439_b200 import _lib  # noqa: E402
 CASES = [  # (label, dtype_in, dtype_out, batch, m)
     ("c5 leaf f32 256", 1, 1, 2 * 1681, 256),
     ("c1 leaf f32 64", 1, 1, 49 * 400, 64),
-    ("c4 leaf f16 128", 2, 2, 2401 * 8, 128),
+    ("c4 leaf f16 128", 2, 2, 2401 * 16, 128),
     ("truth f64<-f32 243", 1, 0, 200, 243),
     ("truth f64<-f32 2048", 1, 0, 2, 2048),
     ("truth f64<-f16 2048", 2, 0, 2, 2048),
