@@ -766,6 +766,171 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
   }
 }
 
+// binary32 leaves, issue-bound like binary16 (FMUL and FADD each take an
+// issue slot): 16-byte operand vectors (K, N multiples of 4), transposed A
+// tile, float4 fragments, and a k loop with no per-step guards -- the K tail
+// of the last tile runs a separate loop.  Same chains as leaf_tiled_kernel.
+template <int BM, int BN, int BK, int TM, int TN, int MINB>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
+    leaf_f32v_kernel(int M, int K, int N, const float* __restrict__ x, int64_t xs,
+                     const float* __restrict__ y, int64_t ys, float* __restrict__ out,
+                     int tiles_n) {
+  constexpr int DY = BM / TM, DX = BN / TN;
+  constexpr int NT = DY * DX;
+  constexpr int AV = BM * BK / 4 / NT;  // float4 vectors per thread per tile
+  constexpr int BV = BK * BN / 4 / NT;
+  static_assert(AV >= 1 && BV >= 1 && BM * BK % (4 * NT) == 0 && BK * BN % (4 * NT) == 0, "tiles");
+  static_assert(TM % 4 == 0 && TN % 4 == 0, "float4 fragments");
+  constexpr int APAD = 4;
+  __shared__ __align__(16) float As[2][BK][BM + APAD];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid % DX, ty = tid / DX;
+  const int64_t b = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const float* xb = x + b * xs;
+  const float* yb = y + b * ys;
+  float4 ra[AV], rb[BV];
+  auto load_tile = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < AV; ++q) {
+      const int v = tid + q * NT;
+      const int mm = v / (BK / 4), kk = (v % (BK / 4)) * 4;
+      const int gm = m0 + mm, gk = k0 + kk;
+      ra[q] = (gm < M && gk < K) ? *reinterpret_cast<const float4*>(xb + (int64_t)gm * K + gk)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < BV; ++q) {
+      const int v = tid + q * NT;
+      const int kk = v / (BN / 4), nn = (v % (BN / 4)) * 4;
+      const int gk = k0 + kk, gn = n0 + nn;
+      rb[q] = (gk < K && gn < N) ? *reinterpret_cast<const float4*>(yb + (int64_t)gk * N + gn)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < AV; ++q) {
+      const int v = tid + q * NT;
+      const int mm = v / (BK / 4), kk = (v % (BK / 4)) * 4;
+      As[buf][kk][mm] = ra[q].x;
+      As[buf][kk + 1][mm] = ra[q].y;
+      As[buf][kk + 2][mm] = ra[q].z;
+      As[buf][kk + 3][mm] = ra[q].w;
+    }
+#pragma unroll
+    for (int q = 0; q < BV; ++q) {
+      const int v = tid + q * NT;
+      const int kk = v / (BN / 4), nn = (v % (BN / 4)) * 4;
+      *reinterpret_cast<float4*>(&Bs[buf][kk][nn]) = rb[q];
+    }
+  };
+  float acc[TM][TN];
+  auto kstep = [&](const float* arow, const float* brow, bool first) {
+    float a[TM], bb[TN];
+#pragma unroll
+    for (int g = 0; g < TM / 4; ++g) {
+      const float4 v = *reinterpret_cast<const float4*>(arow + g * DY * 4);
+      a[4 * g] = v.x; a[4 * g + 1] = v.y; a[4 * g + 2] = v.z; a[4 * g + 3] = v.w;
+    }
+#pragma unroll
+    for (int g = 0; g < TN / 4; ++g) {
+      const float4 v = *reinterpret_cast<const float4*>(brow + g * DX * 4);
+      bb[4 * g] = v.x; bb[4 * g + 1] = v.y; bb[4 * g + 2] = v.z; bb[4 * g + 3] = v.w;
+    }
+    if (first) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = __fmul_rn(a[i], bb[j]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], bb[j]));
+    }
+  };
+  const int ktiles = (K + BK - 1) / BK;
+  load_tile(0);
+  store_tile(0);
+  __syncthreads();
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
+    const float* a0 = &As[buf][0][ty * 4];
+    const float* b0 = &Bs[buf][0][tx * 4];
+    if ((kt + 1) * BK <= K) {
+      if (kt == 0) {
+        kstep(a0, b0, true);
+#pragma unroll
+        for (int kk = 1; kk < BK; ++kk) kstep(a0 + kk * (BM + APAD), b0 + kk * BN, false);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) kstep(a0 + kk * (BM + APAD), b0 + kk * BN, false);
+      }
+    } else {
+      const int kmax = K - kt * BK;
+#pragma unroll 1
+      for (int kk = 0; kk < kmax; ++kk)
+        kstep(a0 + kk * (BM + APAD), b0 + kk * BN, kt == 0 && kk == 0);
+    }
+    if (kt + 1 < ktiles) {
+      store_tile(buf ^ 1);
+      __syncthreads();
+    }
+  }
+  float* ob = out + b * (int64_t)M * N;
+#pragma unroll
+  for (int gi = 0; gi < TM / 4; ++gi)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int gm = m0 + gi * DY * 4 + ty * 4 + v;
+      if (gm >= M) continue;
+#pragma unroll
+      for (int gj = 0; gj < TN / 4; ++gj) {
+        const int gn = n0 + gj * DX * 4 + tx * 4;
+        const int i = gi * 4 + v, j = gj * 4;
+        if (gn + 4 <= N) {
+          *reinterpret_cast<float4*>(&ob[(int64_t)gm * N + gn]) =
+              make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+        } else {
+#pragma unroll
+          for (int w = 0; w < 4; ++w)
+            if (gn + w < N) ob[(int64_t)gm * N + gn + w] = acc[i][j + w];
+        }
+      }
+    }
+}
+
+template <int BM, int BN, int BK, int TM, int TN, int MINB>
+cudaError_t run_f32v(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
+                     const void* y, int64_t ys, void* out, cudaStream_t st) {
+  const int tiles_m = (int)((M + BM - 1) / BM);
+  const int tiles_n = (int)((N + BN - 1) / BN);
+  constexpr int NT = (BM / TM) * (BN / TN);
+  for (int64_t b0 = 0; b0 < batch;) {
+    const int64_t nb = std::min<int64_t>(batch - b0, (int64_t)65535 * 65535);
+    const int64_t full = (nb / 65535) * 65535;
+    if (full > 0) {
+      dim3 grid(tiles_m * tiles_n, 65535, (unsigned)(full / 65535));
+      leaf_f32v_kernel<BM, BN, BK, TM, TN, MINB><<<grid, NT, 0, st>>>(
+          (int)M, (int)K, (int)N, (const float*)x + b0 * xs, xs, (const float*)y + b0 * ys, ys,
+          (float*)out + b0 * M * N, tiles_n);
+    }
+    if (nb > full) {
+      dim3 grid(tiles_m * tiles_n, (unsigned)(nb - full), 1);
+      const int64_t bb = b0 + full;
+      leaf_f32v_kernel<BM, BN, BK, TM, TN, MINB><<<grid, NT, 0, st>>>(
+          (int)M, (int)K, (int)N, (const float*)x + bb * xs, xs, (const float*)y + bb * ys, ys,
+          (float*)out + bb * M * N, tiles_n);
+    }
+    b0 += nb;
+  }
+  return cudaGetLastError();
+}
+
 template <int BM, int BN, int BK, int TM, int TN, int MINB>
 cudaError_t run_h2dup(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
                       const void* y, int64_t ys, void* out, cudaStream_t st) {
@@ -957,8 +1122,24 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
     if (dtype_in == kF32) return leaf_dispatch<float, double>(batch, M, K, N, x, xs, y, ys, out, st);
     if (dtype_in == kF16) return leaf_dispatch<__half, double>(batch, M, K, N, x, xs, y, ys, out, st);
   }
-  if (dtype_out == kF32 && dtype_in == kF32)
+  if (dtype_out == kF32 && dtype_in == kF32) {
+    const bool vec = K % 4 == 0 && N % 4 == 0 && (xs % 4 == 0 || batch == 1) &&
+                     (ys % 4 == 0 || batch == 1) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
+    const int forced = tile_override();
+    if (vec && M >= 128 && N >= 128 && (forced == 0 || forced == 501))
+      return run_f32v<128, 128, 8, 8, 8, 2>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (vec && M >= 128 && N >= 128 && forced == 502)
+      return run_f32v<128, 128, 16, 8, 8, 2>(batch, M, K, N, x, xs, y, ys, out, st);
+    // 64-wide leaves (config 1): 4 x 8 per thread, 128 threads (26.2 vs
+    // 20.5 TFLOP/s for 8 x 8 per thread; tools/leaf_bench.py)
+    if (vec && M >= 64 && N >= 64 && (forced == 0 || forced == 504))
+      return run_f32v<64, 64, 8, 4, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (vec && M >= 64 && N >= 64 && forced == 503)
+      return run_f32v<64, 64, 16, 8, 8, 6>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (vec && M >= 64 && N >= 128 && forced == 505)
+      return run_f32v<64, 128, 8, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
     return leaf_dispatch<float, float>(batch, M, K, N, x, xs, y, ys, out, st);
+  }
   if (dtype_out == kF16 && dtype_in == kF16) {
     // 16-byte operand vectors need K, N multiples of 8 and aligned strides
     const bool vec = K % 8 == 0 && N % 8 == 0 && (xs % 8 == 0 || batch == 1) &&

@@ -104,6 +104,15 @@ def test_binary64_leaf_tiles_bitwise(shape, tile, monkeypatch):
     assert got_b.tobytes() == want_b.tobytes()
 
 
+def _same_bits_or_nan(got, want):
+    """Bitwise equality, except that NaNs (inf - inf after an overflow) only
+    need to be NaN in the same places: their sign/payload is not IEEE-defined
+    and the reference raises OverflowError before any escapes (_engine.py:147)."""
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(got), nan)
+    assert got[~nan].tobytes() == want[~nan].tobytes()
+
+
 @pytest.mark.parametrize("tile", ["0", "402", "403", "404", "999"])
 @pytest.mark.parametrize("shape", [(3, 128, 128, 128), (1, 256, 64, 136), (2, 130, 24, 200),
                                    (1, 128, 40, 128), (1, 128, 13, 128)])
@@ -125,7 +134,30 @@ def test_binary16_leaf_tiles_bitwise(shape, tile, monkeypatch):
     with np.errstate(all="ignore"):
         got = engine.leaf_matmul(x, y, HALF)
         want = oracle.leaf(x, y)
-    assert got.tobytes() == want.tobytes()
+    _same_bits_or_nan(got, want)
+
+
+@pytest.mark.parametrize("tile", ["0", "502", "504", "505", "999"])
+@pytest.mark.parametrize("shape", [(3, 128, 128, 128), (1, 256, 64, 136), (2, 130, 24, 200),
+                                   (4, 64, 64, 64), (1, 128, 13, 128), (2, 100, 36, 68)])
+def test_binary32_leaf_tiles_bitwise(shape, tile, monkeypatch):
+    """binary32 leaves (configs 1 and 5): the vector-load tile kernels against
+    the oracle, with ragged M/N, K tails, a K that is not a multiple of 4
+    (scalar fallback), overflow and signed zeros."""
+    from paper_1905_07439_b200 import engine
+    from paper_1905_07439_b200.precision import SINGLE
+
+    monkeypatch.setenv("RBC_LEAF_TILE", tile)
+    T, M, K, N = shape
+    g = np.random.default_rng(M + 11 * K + N)
+    x = SINGLE.array(g.standard_normal((T, M, K)))
+    y = SINGLE.array(g.standard_normal((T, K, N)))
+    x[0, :2, :] = -0.0
+    x[0, 5, :] = 3e38  # row 5 overflows
+    with np.errstate(all="ignore"):
+        got = engine.leaf_matmul(x, y, SINGLE)
+        want = oracle.leaf(x, y)
+    _same_bits_or_nan(got, want)
 
 
 def test_device_runner_matches_host_call():
