@@ -159,6 +159,14 @@ __global__ void __launch_bounds__(kThreads) expand_dense_staged(
   }
 }
 
+// binary64 tables of n = 3 carry fewer positions per thread: the n*n*PPT
+// accumulators plus the batched child loads must leave room for more than
+// one resident CTA per SM
+template <class T, int N>
+constexpr int contract_ppt() {
+  return sizeof(T) == 8 && N >= 3 ? 2 : kPPT;
+}
+
 template <class T, int N>
 __global__ void __launch_bounds__(kThreads) contract_dense_staged(
     const T* __restrict__ ch, int K, int mb, int R, const T* __restrict__ w, int64_t w_tstride,
@@ -166,6 +174,7 @@ __global__ void __launch_bounds__(kThreads) contract_dense_staged(
   extern __shared__ __align__(16) unsigned char sraw[];
   T* sw = reinterpret_cast<T*>(sraw);
   using A = Arith<T>;
+  constexpr int CP = contract_ppt<T, N>();
   const int s = N * mb;
   const int P = mb * mb;
   const int64_t items = (int64_t)K * P;
@@ -173,11 +182,11 @@ __global__ void __launch_bounds__(kThreads) contract_dense_staged(
     __syncthreads();
     for (int q = threadIdx.x; q < R * N * N; q += kThreads) sw[q] = w[t * w_tstride + q];
     __syncthreads();
-    int64_t cbase[kPPT], obase[kPPT];
-    bool live[kPPT];
+    int64_t cbase[CP], obase[CP];
+    bool live[CP];
 #pragma unroll
-    for (int p = 0; p < kPPT; ++p) {
-      const int64_t e = ((int64_t)blockIdx.x * kPPT + p) * kThreads + threadIdx.x;
+    for (int p = 0; p < CP; ++p) {
+      const int64_t e = ((int64_t)blockIdx.x * CP + p) * kThreads + threadIdx.x;
       live[p] = e < items;
       const int64_t ee = live[p] ? e : 0;
       const int Kp = (int)(ee / P);
@@ -186,23 +195,34 @@ __global__ void __launch_bounds__(kThreads) contract_dense_staged(
       cbase[p] = (t * K + Kp) * (int64_t)R * P + pos;
       obase[p] = (t * K + Kp) * (int64_t)s * s + (int64_t)i * s + j;
     }
-    T acc[N * N][kPPT];
-    for (int r = 0; r < R; ++r) {
-      T pr[kPPT];
+    T acc[N * N][CP];
+    // the children of kRB consecutive terms are loaded together (kRB * CP
+    // independent loads in flight), then folded in ascending r
+    constexpr int kRB = 4;
+    for (int r0 = 0; r0 < R; r0 += kRB) {
+      T pr[kRB][CP];
 #pragma unroll
-      for (int p = 0; p < kPPT; ++p) pr[p] = live[p] ? ch[cbase[p] + (int64_t)r * P] : T(0);
-      const T* wr = sw + r * N * N;
+      for (int q = 0; q < kRB; ++q)
 #pragma unroll
-      for (int ij = 0; ij < N * N; ++ij) {
-        const T c = wr[ij];
+        for (int p = 0; p < CP; ++p)
+          pr[q][p] = (live[p] && r0 + q < R) ? ch[cbase[p] + (int64_t)(r0 + q) * P] : T(0);
 #pragma unroll
-        for (int p = 0; p < kPPT; ++p)
-          acc[ij][p] = (r == 0) ? A::mul(c, pr[p]) : A::add(acc[ij][p], A::mul(c, pr[p]));
+      for (int q = 0; q < kRB; ++q) {
+        const int r = r0 + q;
+        if (r >= R) break;
+        const T* wr = sw + r * N * N;
+#pragma unroll
+        for (int ij = 0; ij < N * N; ++ij) {
+          const T c = wr[ij];
+#pragma unroll
+          for (int p = 0; p < CP; ++p)
+            acc[ij][p] = (r == 0) ? A::mul(c, pr[q][p]) : A::add(acc[ij][p], A::mul(c, pr[q][p]));
+        }
       }
     }
     bool ok = true;
 #pragma unroll
-    for (int p = 0; p < kPPT; ++p) {
+    for (int p = 0; p < CP; ++p) {
       if (!live[p]) continue;
 #pragma unroll
       for (int I = 0; I < N; ++I)
@@ -238,12 +258,13 @@ cudaError_t staged_contract_n(const void* ch, int64_t K, int64_t mb, int R, cons
                               int64_t ws, void* out, int64_t ntr, uint8_t* nf, cudaStream_t st) {
   const int64_t items = K * mb * mb;
   const size_t smem = (size_t)R * N * N * sizeof(T);
+  constexpr int CP = contract_ppt<T, N>();
   auto kern = contract_dense_staged<T, N>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid((unsigned)((items + kThreads * kPPT - 1) / (kThreads * kPPT)),
+  dim3 grid((unsigned)((items + kThreads * CP - 1) / (kThreads * CP)),
             (unsigned)(ntr < 65535 ? ntr : 65535));
   kern<<<grid, kThreads, smem, st>>>((const T*)ch, (int)K, (int)mb, R, (const T*)w, ws, (T*)out, ntr, nf);
   return cudaGetLastError();

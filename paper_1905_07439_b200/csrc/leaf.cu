@@ -69,6 +69,12 @@ struct Mac<__half, double> {
   }
 };
 
+// RBC_LEAF_TILE=<128|64|32|1> overrides the tile choice (tuning aid).
+inline int tile_override() {
+  const char* v = getenv("RBC_LEAF_TILE");
+  return v ? atoi(v) : 0;
+}
+
 template <class TIn, class TAcc>
 __global__ void __launch_bounds__(256) leaf_small_kernel(int64_t batch, int M, int K, int N,
                                                          const TIn* __restrict__ x, int64_t xs,
@@ -1035,11 +1041,6 @@ cudaError_t run_small(int64_t batch, int64_t M, int64_t K, int64_t N, const void
   return cudaGetLastError();
 }
 
-// RBC_LEAF_TILE=<128|64|32|1> overrides the tile choice (tuning aid).
-inline int tile_override() {
-  const char* v = getenv("RBC_LEAF_TILE");
-  return v ? atoi(v) : 0;
-}
 
 template <class TIn, class TAcc>
 cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x,
