@@ -168,6 +168,12 @@ static bool fusion_enabled() {
   return !(v && v[0] == '1');
 }
 
+// RBC_NO_EXPAND2=1 evaluates every expansion level in its own pass.
+static bool expand2_enabled() {
+  const char* v = getenv("RBC_NO_EXPAND2");
+  return !(v && v[0] == '1');
+}
+
 static constexpr size_t kMaxSubtreeSmem = 200 * 1024;
 
 static cudaError_t stage_done(cudaError_t e, cudaStream_t st) {
@@ -236,31 +242,50 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
       int64_t cur_ts = p.T0 == 1 ? 0 : N2;
       if (p.T0 != 1) cur = (const char*)cur + (size_t)t0 * N2 * es;
       int64_t K = 1, s = g.N;
-      for (int q = 0; q < q0; ++q) {
+      for (int q = 0; q < q0;) {
         const int n = g.lv[q].n, R = g.lv[q].R;
-        void* dst = (q == q0 - 1) ? (which == 0 ? bufX : bufY) : ((q & 1) ? pong : ping);
-        cudaError_t e;
-        const double mbq = (double)(s / n);
-        Stage stage(st, p.plan ? "expand_plan" : "expand_dense",
-                    ((cur_ts ? (double)nt : 1.0) * K * s * s + (double)nt * K * R * mbq * mbq) * es,
-                    (double)nt * K * R * mbq * mbq * n * n * 2.0);
-        if (p.plan) {
-          const int64_t pts = p.Tp == 1 ? 0 : g.Q;
-          const PlanLevel* pl = p.plans + (p.Tp == 1 ? 0 : t0 * g.Q);
-          e = launch_expand_plan(dt, p.formula, which, cur, cur_ts, K, s, dst, pl, pts, q, nt, st);
-        } else {
-          const void* c = which == 0 ? p.u[q] : p.v[q];
-          const int64_t cts = p.Tc[q] == 1 ? 0 : (int64_t)R * n * n;
-          c = (const char*)c + (size_t)(p.Tc[q] == 1 ? 0 : t0 * cts) * es;
-          e = launch_expand_dense(dt, cur, cur_ts, K, s, n, R, c, cts, dst, nt, st);
+        // plan path: two levels per pass where an instantiation exists
+        int step = (p.plan && expand2_enabled() && q + 1 < q0 &&
+                    expand2_supported(dt, p.formula)) ? 2 : 1;
+        const int qlast = q + step - 1;
+        void* dst = (qlast == q0 - 1) ? (which == 0 ? bufX : bufY) : (cur == ping ? pong : ping);
+        cudaError_t e = cudaErrorNotSupported;
+        const int64_t pts = p.Tp == 1 ? 0 : g.Q;
+        const PlanLevel* pl = p.plans + (p.Tp == 1 ? 0 : t0 * g.Q);
+        if (step == 2) {
+          const double mb2 = (double)(s / (n * n));
+          Stage stage(st, "expand2_plan",
+                      ((cur_ts ? (double)nt : 1.0) * K * s * s + (double)nt * K * R * R * mb2 * mb2) * es,
+                      (double)nt * K * R * (R + 1) * mb2 * mb2 * n * n * 2.0);
+          e = launch_expand2_plan(dt, p.formula, which, cur, cur_ts, K, s, dst, pl, pts, q, nt, st);
+          if (e == cudaErrorNotSupported) {
+            step = 1;
+            dst = (q == q0 - 1) ? (which == 0 ? bufX : bufY) : (cur == ping ? pong : ping);
+          }
+        }
+        if (step == 1) {
+          const double mbq = (double)(s / n);
+          Stage stage(st, p.plan ? "expand_plan" : "expand_dense",
+                      ((cur_ts ? (double)nt : 1.0) * K * s * s + (double)nt * K * R * mbq * mbq) * es,
+                      (double)nt * K * R * mbq * mbq * n * n * 2.0);
+          if (p.plan) {
+            e = launch_expand_plan(dt, p.formula, which, cur, cur_ts, K, s, dst, pl, pts, q, nt, st);
+          } else {
+            const void* c = which == 0 ? p.u[q] : p.v[q];
+            const int64_t cts = p.Tc[q] == 1 ? 0 : (int64_t)R * n * n;
+            c = (const char*)c + (size_t)(p.Tc[q] == 1 ? 0 : t0 * cts) * es;
+            e = launch_expand_dense(dt, cur, cur_ts, K, s, n, R, c, cts, dst, nt, st);
+          }
         }
         e = stage_done(e, st);
         if (e != cudaSuccess) return fail_cuda(e, "expand", __FILE__, __LINE__);
-        const int64_t mb = s / n;
+        for (int k = 0; k < step; ++k) {
+          s /= n;
+          K *= R;
+        }
         cur = dst;
-        cur_ts = K * R * mb * mb;
-        K *= R;
-        s = mb;
+        cur_ts = K * s * s;
+        q += step;
       }
     }
     // --- leaves (or the fused bottom subtree)

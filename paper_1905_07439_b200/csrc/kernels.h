@@ -63,6 +63,15 @@ cudaError_t launch_contract_plan(int dtype, int formula, const void* ch, int64_t
                                  void* out, const PlanLevel* plans, int64_t plan_tstride,
                                  int level, int64_t T, uint8_t* nonfinite, cudaStream_t st);
 
+// Expansion of levels `level` and `level + 1` in one pass (no level+1 array in
+// HBM): x (T or 1, K, s, s) -> out (T, K*R*R, s/n^2, s/n^2).  Same values as
+// two launch_expand_plan calls.  expand2_supported: an instantiation exists.
+cudaError_t launch_expand2_plan(int dtype, int formula, int which, const void* x,
+                                int64_t x_tstride, int64_t K, int64_t s, void* out,
+                                const PlanLevel* plans, int64_t plan_tstride, int level,
+                                int64_t ntr, cudaStream_t st);
+bool expand2_supported(int dtype, int formula);
+
 int formula_n(int formula);
 int formula_R(int formula);
 

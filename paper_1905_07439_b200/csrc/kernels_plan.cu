@@ -72,6 +72,87 @@ __global__ void __launch_bounds__(kThreads) expand_plan_kernel(
   }
 }
 
+// Two expansion levels (q, q+1) in one pass: a thread owns one position of
+// the level-(q+2) blocks under one level-q parent, loads the n^4 parent
+// elements that feed it (read exactly once per trial, coalesced along rows),
+// forms each level-(q+1) child r1 at its n*n sub-positions with the
+// single-output network (expand_u1 / expand_v1: the same per-element fold as
+// the full network), and expands those into the R grandchildren with the full
+// network.  Both plans' gathers are folded into the load addresses (level
+// q+1's permutation picks which sub-position feeds which network input; its
+// sign is applied to the child value), so every register index is static.
+// Values equal two expand_plan_kernel launches; the level-(q+1) array never
+// goes through HBM.
+template <class F, class T, int W, int WHICH>
+__global__ void __launch_bounds__(kThreads) expand2_plan_kernel(
+    const T* __restrict__ x, int64_t x_tstride, int K, int s, T* __restrict__ out,
+    const PlanLevel* __restrict__ plans, int64_t plan_tstride, int level, int64_t ntr) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  constexpr int NN = n * n;
+  const int mb1 = s / n, mb2 = mb1 / n;
+  const int P = (mb2 * mb2) / W;
+  const int64_t items = (int64_t)K * P;
+  const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (e >= items) return;
+  const int Kp = (int)(e / P);
+  const int p = (int)(e - (int64_t)Kp * P);
+  const int pos = p * W;
+  const int i = pos / mb2;
+  const int j = pos - i * mb2;
+  constexpr int ri = WHICH == 0 ? 0 : 1;
+  constexpr int ci = WHICH == 0 ? 1 : 2;
+  using O = PackOps<T, W>;
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    const PlanLevel& p0 = plans[t * plan_tstride + level];
+    const PlanLevel& p1 = plans[t * plan_tstride + level + 1];
+    const T* xb = x + t * x_tstride + (int64_t)Kp * s * s + (int64_t)i * s + j;
+    Pack<T, W> g0[NN][NN];
+    uint32_t m1[NN];
+#pragma unroll
+    for (int kb1 = 0; kb1 < n; ++kb1) {
+      const int a = p1.inv[ri][kb1];
+#pragma unroll
+      for (int lb1 = 0; lb1 < n; ++lb1) {
+        const int b = p1.inv[ci][lb1];
+        m1[kb1 * n + lb1] = sign_mask(p1.neg[ri][a] ^ p1.neg[ci][b]);
+        const T* xs = xb + (int64_t)a * mb2 * s + b * mb2;
+#pragma unroll
+        for (int kb0 = 0; kb0 < n; ++kb0) {
+          const int hk = p0.inv[ri][kb0];
+#pragma unroll
+          for (int lb0 = 0; lb0 < n; ++lb0) {
+            const int hl = p0.inv[ci][lb0];
+            const uint32_t m0 = sign_mask(p0.neg[ri][hk] ^ p0.neg[ci][hl]);
+            g0[kb1 * n + lb1][kb0 * n + lb0] =
+                O::flip(pload<T, W>(xs + (int64_t)hk * mb1 * s + hl * mb1), m0);
+          }
+        }
+      }
+    }
+    const int l0r = p0.perm[ri][n - 1], l0c = p0.perm[ci][n - 1];
+    const int l1r = p1.perm[ri][n - 1], l1c = p1.perm[ci][n - 1];
+    T* ob = out + (t * K + Kp) * (int64_t)R * R * mb2 * mb2 + pos;
+#pragma unroll
+    for (int r1 = 0; r1 < R; ++r1) {
+      Pack<T, W> g1[NN];
+#pragma unroll
+      for (int q = 0; q < NN; ++q) {
+        const Pack<T, W> v = WHICH == 0 ? F::template expand_u1<T, W>(g0[q], r1, l0r, l0c)
+                                        : F::template expand_v1<T, W>(g0[q], r1, l0r, l0c);
+        g1[q] = O::flip(v, m1[q]);
+      }
+      Pack<T, W> o[R];
+      if (WHICH == 0)
+        F::template expand_u<T, W>(g1, o, l1r, l1c);
+      else
+        F::template expand_v<T, W>(g1, o, l1r, l1c);
+#pragma unroll
+      for (int r2 = 0; r2 < R; ++r2) pstore<T, W>(ob + (int64_t)(r1 * R + r2) * mb2 * mb2, o[r2]);
+    }
+  }
+}
+
 template <class F, class T, int W>
 __global__ void __launch_bounds__(kThreads) contract_plan_kernel(
     const T* __restrict__ ch, int K, int mb, T* __restrict__ out,
@@ -133,6 +214,60 @@ cudaError_t expand_plan_w(int which, const void* x, int64_t xs, int64_t K, int64
     expand_plan_kernel<F, T, W, 1><<<grid, kThreads, 0, st>>>(
         (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
   return cudaGetLastError();
+}
+
+template <class F, class T, int W>
+cudaError_t expand2_plan_w(int which, const void* x, int64_t xs, int64_t K, int64_t s, void* out,
+                           const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
+                           cudaStream_t st) {
+  const int64_t mb2 = s / (F::n * F::n);
+  const dim3 grid = grid_for(K * (mb2 * mb2 / W), ntr);
+  if (which == 0)
+    expand2_plan_kernel<F, T, W, 0><<<grid, kThreads, 0, st>>>(
+        (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
+  else
+    expand2_plan_kernel<F, T, W, 1><<<grid, kThreads, 0, st>>>(
+        (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
+  return cudaGetLastError();
+}
+
+// n^4 live input packs per thread: binary64 Laderman (81 doubles) and wide
+// packs would spill, so those keep the two single-level launches.
+template <class F, class T>
+constexpr int expand2_max_width() {
+  constexpr int bytes = F::n * F::n * F::n * F::n * (int)sizeof(T);
+  if (F::n >= 3 && sizeof(T) != 4) return 0;  // binary16 n = 3 spills (half pack ops)
+  return bytes > 384 ? 0 : (bytes * 4 <= 384 ? 4 : bytes * 2 <= 384 ? 2 : 1);
+}
+
+template <class F, class T>
+cudaError_t expand2_plan_t(int dtype, int which, const void* x, int64_t xs, int64_t K, int64_t s,
+                           void* out, const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
+                           cudaStream_t st) {
+  constexpr int cap = expand2_max_width<F, T>();
+  if constexpr (cap == 0) {
+    return cudaErrorNotSupported;
+  } else {
+    const int W = pick_width(dtype, s / (F::n * F::n), cap);
+    switch (W) {
+      case 4: return expand2_plan_w<F, T, (cap >= 4 ? 4 : 1)>(which, x, xs, K, s, out, plans, pts, level, ntr, st);
+      case 2: return expand2_plan_w<F, T, (cap >= 2 ? 2 : 1)>(which, x, xs, K, s, out, plans, pts, level, ntr, st);
+      default: return expand2_plan_w<F, T, 1>(which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    }
+  }
+}
+
+template <class T>
+cudaError_t expand2_plan_f(int dtype, int formula, int which, const void* x, int64_t xs, int64_t K,
+                           int64_t s, void* out, const PlanLevel* plans, int64_t pts, int level,
+                           int64_t ntr, cudaStream_t st) {
+  switch (formula) {
+    case FStrassen::kId: return expand2_plan_t<FStrassen, T>(dtype, which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    case FLaderman::kId: return expand2_plan_t<FLaderman, T>(dtype, which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    case FStandard2::kId: return expand2_plan_t<FStandard2, T>(dtype, which, x, xs, K, s, out, plans, pts, level, ntr, st);
+    case FStandard3::kId: return expand2_plan_t<FStandard3, T>(dtype, which, x, xs, K, s, out, plans, pts, level, ntr, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <class F, class T, int W>
@@ -232,6 +367,37 @@ cudaError_t launch_expand_plan(int dtype, int formula, int which, const void* x,
     case kF16: return expand_plan_f<__half>(dtype, formula, which, x, x_tstride, K, s, out, plans, plan_tstride, level, ntr, st);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_expand2_plan(int dtype, int formula, int which, const void* x,
+                                int64_t x_tstride, int64_t K, int64_t s, void* out,
+                                const PlanLevel* plans, int64_t plan_tstride, int level,
+                                int64_t ntr, cudaStream_t st) {
+  switch (dtype) {
+    case kF64: return expand2_plan_f<double>(dtype, formula, which, x, x_tstride, K, s, out, plans, plan_tstride, level, ntr, st);
+    case kF32: return expand2_plan_f<float>(dtype, formula, which, x, x_tstride, K, s, out, plans, plan_tstride, level, ntr, st);
+    case kF16: return expand2_plan_f<__half>(dtype, formula, which, x, x_tstride, K, s, out, plans, plan_tstride, level, ntr, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+bool expand2_supported(int dtype, int formula) {
+  auto ok = [&](auto f) {
+    using F = decltype(f);
+    switch (dtype) {
+      case kF64: return expand2_max_width<F, double>() > 0;
+      case kF32: return expand2_max_width<F, float>() > 0;
+      case kF16: return expand2_max_width<F, __half>() > 0;
+    }
+    return false;
+  };
+  switch (formula) {
+    case FStrassen::kId: return ok(FStrassen{});
+    case FLaderman::kId: return ok(FLaderman{});
+    case FStandard2::kId: return ok(FStandard2{});
+    case FStandard3::kId: return ok(FStandard3{});
+  }
+  return false;
 }
 
 cudaError_t launch_contract_plan(int dtype, int formula, const void* ch, int64_t K, int64_t mb,
