@@ -15,7 +15,8 @@ def main():
     h = rows[1]
     idx = {k: i for i, k in enumerate(h)}
     data = rows[2:]
-    ie, ss, ex = idx["Instructions Executed"], idx["Warp Stall Sampling (All Samples)"], idx["L1 Wavefronts Shared Excessive"]
+    ie, ss = idx["Instructions Executed"], idx["Warp Stall Sampling (All Samples)"]
+    ex = idx.get("L1 Wavefronts Shared Excessive")
     tot = sum(int(r[ie] or 0) for r in data)
     samp = sum(int(r[ss] or 0) for r in data) or 1
     c, s, x = Counter(), Counter(), Counter()
@@ -27,7 +28,7 @@ def main():
         op = op.split(".")[0]
         c[op] += int(r[ie] or 0)
         s[op] += int(r[ss] or 0)
-        x[op] += int(r[ex] or 0)
+        x[op] += int(r[ex] or 0) if ex is not None else 0
     print(f"total warp instructions {tot / 1e6:.1f}M")
     for op, v in c.most_common(top):
         print(f"{op:10s} {v / 1e6:9.1f}M {100 * v / tot:5.1f}%  stall {100 * s[op] / samp:5.1f}%  excess_wf {x[op] / 1e6:.1f}M")
