@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "bulk.cuh"
 #include "kernels.h"
 
 namespace rbc {
@@ -493,11 +494,132 @@ cudaError_t run_smem(int64_t batch, const void* x, int64_t xs, const void* y, in
   return cudaGetLastError();
 }
 
+// Persistent variant for long batches of small square leaves whose operand
+// type equals the accumulation type: LPB leaves per group arrive by bulk
+// copies (the TMA engine; each leaf's X and Y are copied as the 16-byte
+// aligned spans enclosing them) into a 2-stage ring completed on mbarriers,
+// issued by one thread one group ahead -- no load instructions in the
+// threads, loads overlap the FP work inside every CTA.  Same per-element
+// chains as leaf_smem_kernel.
+template <class T, int M, int TR>
+struct SmemBulk {
+  static constexpr int TPL = (M / TR) * (M / TR);
+  static constexpr int LPB = 256 / TPL;
+  static constexpr int E = M * M;
+  static constexpr int SPAN = ((E * (int)sizeof(T) + 16) + 15) / 16 * 16;  // bytes per operand slot
+  static constexpr size_t stage_bytes = (size_t)LPB * 2 * SPAN;
+  static constexpr size_t smem = 2 * stage_bytes + 2 * sizeof(uint64_t);
+};
+
+template <class T, int M, int TR>
+__global__ void __launch_bounds__(256) leaf_smem_bulk_kernel(int64_t batch, const T* __restrict__ x,
+                                                             int64_t xs, const T* __restrict__ y,
+                                                             int64_t ys, T* __restrict__ out) {
+  using S = SmemBulk<T, M, TR>;
+  constexpr int TPL = S::TPL, LPB = S::LPB, E = S::E;
+  using A = Arith<T>;
+  extern __shared__ __align__(128) unsigned char bulk_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(bulk_smem + 2 * S::stage_bytes);
+  const int64_t groups = (batch + LPB - 1) / LPB;
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  // operand slot (stage, leaf, which) and the element offset of the block in it
+  auto slot = [&](int stg, int l, int which) {
+    return bulk_smem + (size_t)stg * S::stage_bytes + (size_t)(l * 2 + which) * S::SPAN;
+  };
+  auto issue = [&](int64_t g, int stg) {  // one thread
+    const int64_t b0 = g * LPB;
+    const int nl = batch - b0 < LPB ? (int)(batch - b0) : LPB;
+    unsigned bytes = 0;
+    for (int l = 0; l < nl; ++l) {
+      bytes += span_bytes(x + (b0 + l) * xs, E * sizeof(T));
+      bytes += span_bytes(y + (b0 + l) * ys, E * sizeof(T));
+    }
+    fence_proxy_async();
+    mbar_expect_tx(&full[stg], bytes);
+    for (int l = 0; l < nl; ++l) {
+      const T* gx = x + (b0 + l) * xs;
+      const T* gy = y + (b0 + l) * ys;
+      bulk_g2s(slot(stg, l, 0), span_start(gx), span_bytes(gx, E * sizeof(T)), &full[stg]);
+      bulk_g2s(slot(stg, l, 1), span_start(gy), span_bytes(gy, E * sizeof(T)), &full[stg]);
+    }
+  };
+  const int l = threadIdx.x / TPL;
+  const int r = threadIdx.x - l * TPL;
+  const int ti = (r / (M / TR)) * TR, tj = (r % (M / TR)) * TR;
+  int64_t g = blockIdx.x;
+  if (threadIdx.x == 0 && g < groups) issue(g, 0);
+  for (int it = 0; g < groups; g += gridDim.x, ++it) {
+    const int stg = it & 1;
+    if (threadIdx.x == 0 && g + gridDim.x < groups) issue(g + gridDim.x, stg ^ 1);
+    mbar_wait(&full[stg], (unsigned)((it >> 1) & 1));
+    const int64_t b0 = g * LPB;
+    const int nl = batch - b0 < LPB ? (int)(batch - b0) : LPB;
+    if (l < nl) {
+      const T* gx = x + (b0 + l) * xs;
+      const T* gy = y + (b0 + l) * ys;
+      const T* Xs = reinterpret_cast<const T*>(slot(stg, l, 0) + (reinterpret_cast<uintptr_t>(gx) & 15));
+      const T* Ys = reinterpret_cast<const T*>(slot(stg, l, 1) + (reinterpret_cast<uintptr_t>(gy) & 15));
+      T acc[TR][TR];
+#pragma unroll
+      for (int i = 0; i < TR; ++i)
+#pragma unroll
+        for (int j = 0; j < TR; ++j) acc[i][j] = A::mul(Xs[(ti + i) * M], Ys[tj + j]);
+#pragma unroll 3
+      for (int k = 1; k < M; ++k) {
+        T a[TR], bb[TR];
+#pragma unroll
+        for (int i = 0; i < TR; ++i) a[i] = Xs[(ti + i) * M + k];
+#pragma unroll
+        for (int j = 0; j < TR; ++j) bb[j] = Ys[k * M + tj + j];
+#pragma unroll
+        for (int i = 0; i < TR; ++i)
+#pragma unroll
+          for (int j = 0; j < TR; ++j) acc[i][j] = A::add(acc[i][j], A::mul(a[i], bb[j]));
+      }
+      T* o = out + (b0 + l) * (int64_t)E;
+#pragma unroll
+      for (int i = 0; i < TR; ++i)
+#pragma unroll
+        for (int j = 0; j < TR; ++j) o[(ti + i) * M + tj + j] = acc[i][j];
+    }
+    __syncthreads();  // stage stg is refilled next iteration (issued above it)
+  }
+}
+
+template <class T, int M, int TR>
+cudaError_t run_smem_bulk(int64_t batch, const void* x, int64_t xs, const void* y, int64_t ys,
+                          void* out, cudaStream_t st) {
+  using S = SmemBulk<T, M, TR>;
+  auto kern = leaf_smem_bulk_kernel<T, M, TR>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem);
+  if (attr != cudaSuccess) return attr;
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, S::smem);
+  if (e != cudaSuccess) return e;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t groups = (batch + S::LPB - 1) / S::LPB;
+  const int64_t blocks = std::min<int64_t>(groups, (int64_t)sms * std::max(1, per_sm));
+  kern<<<(unsigned)blocks, 256, S::smem, st>>>(batch, (const T*)x, xs, (const T*)y, ys, (T*)out);
+  return cudaGetLastError();
+}
+
 // Square small leaves with a shared-memory kernel instantiation; returns
 // cudaErrorNotSupported when none applies.
 template <class TIn, class TAcc>
 cudaError_t small_square(int64_t batch, int64_t M, const void* x, int64_t xs, const void* y,
                          int64_t ys, void* out, cudaStream_t st) {
+  if constexpr (std::is_same<TIn, TAcc>::value && sizeof(TIn) >= 4) {
+    const int f = tile_override();
+    if (M == 27 && batch >= 2048 && (f == 0 || f == 210))
+      return run_smem_bulk<TIn, 27, 3>(batch, x, xs, y, ys, out, st);
+  }
   switch (M) {
     case 27: return run_smem<TIn, TAcc, 27, 3>(batch, x, xs, y, ys, out, st);
     case 24: return run_smem<TIn, TAcc, 24, 3>(batch, x, xs, y, ys, out, st);

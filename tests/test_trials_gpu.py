@@ -160,6 +160,28 @@ def test_binary32_leaf_tiles_bitwise(shape, tile, monkeypatch):
     _same_bits_or_nan(got, want)
 
 
+@pytest.mark.parametrize("label", ["f64", "f32"])
+@pytest.mark.parametrize("tile", ["0", "205"])
+def test_small_square_leaves_bitwise(label, tile, monkeypatch):
+    """27x27 leaves in long batches (config 3's leaves) run on the bulk-copy
+    persistent kernel (tile "0") or the single-shot shared-memory kernel
+    ("205"): both equal the oracle; the batch is odd so groups end ragged and
+    leaves sit at 8-byte offsets."""
+    from paper_1905_07439_b200 import engine
+    from paper_1905_07439_b200.precision import parse_precision
+
+    monkeypatch.setenv("RBC_LEAF_TILE", tile)
+    mode = parse_precision(label)
+    g = np.random.default_rng(27)
+    T = 4099
+    x = mode.array(g.standard_normal((T, 27, 27)))
+    y = mode.array(g.standard_normal((T, 27, 27)))
+    x[7, :2, :] = -0.0
+    got = engine.leaf_matmul(x, y, mode)
+    want = oracle.leaf(x, y)
+    assert got.tobytes() == want.tobytes()
+
+
 def test_device_runner_matches_host_call():
     import torch
 
