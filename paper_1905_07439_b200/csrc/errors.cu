@@ -8,6 +8,8 @@
 // (The reference's numpy pairwise/BLAS sums use another order; the two
 // agree to a few ulp of binary64, far inside the 1e-12 golden tolerance.)
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace rbc {
@@ -41,8 +43,24 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(int64_t N2, const T* __
   const T* ct = c + t * N2;
   const double* rt = ref + t * ref_tstride;
   double num = 0.0, den = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < N2;
-       i += (int64_t)gridDim.x * kThreads) {
+  // four independent loads in flight per thread per round
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  for (; i + 3 * stride < N2; i += 4 * stride) {
+    double r[4], cv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      r[q] = rt[i + q * stride];
+      cv[q] = Arith<T>::widen(ct[i + q * stride]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double d = cv[q] - r[q];
+      num += d * d;
+      den += r[q] * r[q];
+    }
+  }
+  for (; i < N2; i += stride) {
     const double r = rt[i];
     const double d = Arith<T>::widen(ct[i]) - r;
     num += d * d;
@@ -83,16 +101,18 @@ __global__ void __launch_bounds__(kThreads) nonfinite_kernel(int64_t N2, const T
 template <class T>
 cudaError_t rel_errors_t(int64_t ntr, int64_t N2, const void* c, const double* ref, int64_t rts,
                          double* err, void* scratch, cudaStream_t st) {
+  // blocks per trial: about 16 elements per thread, at most kBlocksPerTrial
+  // (a function of N2 only, so the summation order is fixed)
+  const int nb = (int)std::min<int64_t>(kBlocksPerTrial, std::max<int64_t>(1, (N2 + 4095) / 4096));
   double* pn = (double*)scratch;
   double* pd = pn + ntr * kBlocksPerTrial;
   for (int64_t t0 = 0; t0 < ntr; t0 += 65535) {
     const int64_t nt = ntr - t0 < 65535 ? ntr - t0 : 65535;
-    dim3 grid(kBlocksPerTrial, (unsigned)nt);
+    dim3 grid(nb, (unsigned)nt);
     sumsq_kernel<T><<<grid, kThreads, 0, st>>>(N2, (const T*)c + t0 * N2, ref + t0 * rts, rts,
-                                                pn + t0 * kBlocksPerTrial,
-                                                pd + t0 * kBlocksPerTrial);
+                                                pn + t0 * nb, pd + t0 * nb);
   }
-  finish_kernel<<<(unsigned)((ntr + 127) / 128), 128, 0, st>>>(ntr, kBlocksPerTrial, pn, pd, err);
+  finish_kernel<<<(unsigned)((ntr + 127) / 128), 128, 0, st>>>(ntr, nb, pn, pd, err);
   return cudaGetLastError();
 }
 
