@@ -111,14 +111,26 @@ __global__ void __launch_bounds__(kMeanThreads) running_mean_kernel(
     const double r = ref[e];
     double total = 0.0;
     int c = 0;
-    for (int t = 0; t < G; ++t) {
-      total = __dadd_rn(total, rbc::Arith<T>::widen(C[(int64_t)t * N2 + e]));
-      if (c < cp.n && t + 1 == cp.at[c]) {
-        const double d = __dsub_rn(__ddiv_rn(total, (double)(t + 1)), r);
+    // the products of kBatch plans are loaded together (independent loads in
+    // flight), then added in plan order
+    constexpr int kBatch = 8;
+    for (int t0 = 0; t0 < G; t0 += kBatch) {
+      T v[kBatch];
 #pragma unroll
-        for (int k = 0; k < kMaxCheckpoints; ++k)
-          if (k == c) s[k] += d * d;
-        ++c;
+      for (int q = 0; q < kBatch; ++q)
+        v[q] = t0 + q < G ? C[(int64_t)(t0 + q) * N2 + e] : T(0);
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q) {
+        const int t = t0 + q;
+        if (t >= G) break;
+        total = __dadd_rn(total, rbc::Arith<T>::widen(v[q]));
+        if (c < cp.n && t + 1 == cp.at[c]) {
+          const double d = __dsub_rn(__ddiv_rn(total, (double)(t + 1)), r);
+#pragma unroll
+          for (int k = 0; k < kMaxCheckpoints; ++k)
+            if (k == c) s[k] += d * d;
+          ++c;
+        }
       }
     }
     s[kMaxCheckpoints] += r * r;
