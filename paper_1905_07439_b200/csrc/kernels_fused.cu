@@ -670,7 +670,11 @@ struct SubtreeReg {
   static constexpr int RP = (F::R == 23 && M == 3) ? 26 : R + (R & 1);
   static constexpr int slot = 2 * kids1 * RP;             // X1 + Y1 of one subtree
   // resident CTAs per SM the register budget aims at (about 128 registers a thread)
-  static constexpr int kMinBlocks = 65536 / (128 * NT) > 0 ? 65536 / (128 * NT) : 1;
+#ifndef RBC_SUBTREE_REGS
+#define RBC_SUBTREE_REGS 128
+#endif
+  static constexpr int kMinBlocks =
+      65536 / (RBC_SUBTREE_REGS * NT) > 0 ? 65536 / (RBC_SUBTREE_REGS * NT) : 1;
   static constexpr size_t header() {
     return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 3 * sizeof(GatherTab<n>);
   }
