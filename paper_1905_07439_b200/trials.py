@@ -126,6 +126,17 @@ class DeviceAverageTrials:
             out.append(tuple(self.torch.from_numpy(t).to(self.device) for t in (u, v, w)))
         return out
 
+    def capture(self, a, b, tables, with_det: bool = True):
+        """One pass as a CUDA graph (see DeviceErrorTrials.capture)."""
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.graph(g, stream=s):
+            self.run(a, b, tables, with_det, stream=s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return g
+
     def run(self, a, b, tables, with_det: bool = True, stream=None):
         torch = self.torch
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -201,6 +212,21 @@ class DeviceErrorTrials:
         self.err_det = torch.empty(T, dtype=torch.float64, device=self.device)
         self.nf_rand = torch.empty(T, dtype=torch.uint8, device=self.device)
         self.nf_det = torch.empty(T, dtype=torch.uint8, device=self.device)
+
+    def capture(self, a, b, plans, with_det: bool = True):
+        """Capture one pass (every launch of the truth, both products, the
+        forked lanes and the errors) into a CUDA graph; ``graph.replay()``
+        re-runs it on the same tensors without per-launch host overhead.
+        Run the pass eagerly once first (kernel attributes are set on first
+        use, outside capture)."""
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.graph(g, stream=s):
+            self.run(a, b, plans, with_det, stream=s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return g
 
     def run(self, a, b, plans, with_det: bool = True, stream=None):
         """Enqueue one pass on ``stream`` (default: torch's current stream)."""

@@ -211,3 +211,41 @@ def test_device_runner_matches_host_call():
     torch.cuda.synchronize()
     assert np.array_equal(r.err_rand.cpu().numpy(), host["err_rand"])
     assert np.array_equal(r.err_det.cpu().numpy(), host["err_det"])
+
+
+@pytest.mark.parametrize("name,N,Q,T", [("c1", 256, 2, 5), ("c2", 243, 4, 3), ("c5", 1024, 3, 2)])
+def test_graph_replay_matches_eager(name, N, Q, T):
+    """The error-trial step captured as one CUDA graph (forked lanes, the
+    stream-ordered scratch of the binary64 truth) replays to the same
+    errors as eager launches, on fresh inputs written between replays."""
+    import torch
+    from dataclasses import replace
+
+    from paper_1905_07439_b200.configs import get_config, make_pairs
+    from paper_1905_07439_b200.randomize import pack_recursive_plans
+    from paper_1905_07439_b200.trials import DeviceErrorTrials
+
+    cfg = replace(get_config(name), N=N, Q=Q)
+    f = cfg.formula_obj()
+    dev = torch.device("cuda:0")
+    A, B = make_pairs(cfg, 1, 2 * T)
+    packed = pack_recursive_plans([cfg.plan(p) for p in range(1, 2 * T + 1)], cfg.Q, cfg.n)
+    r = DeviceErrorTrials(f, cfg.Q, cfg.N, cfg.mode, T, device=dev)
+    a = torch.from_numpy(A[:T]).to(dev)
+    b = torch.from_numpy(B[:T]).to(dev)
+    pl = torch.from_numpy(packed[:T]).to(dev)
+    r.run(a, b, pl)
+    torch.cuda.synchronize()
+    g = r.capture(a, b, pl)
+    for sl in (slice(T, 2 * T), slice(0, T)):
+        a.copy_(torch.from_numpy(A[sl]))
+        b.copy_(torch.from_numpy(B[sl]))
+        pl.copy_(torch.from_numpy(packed[sl]))
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        got = (r.err_rand.cpu().numpy().copy(), r.err_det.cpu().numpy().copy())
+        r.run(a, b, pl)
+        torch.cuda.synchronize()
+        assert np.array_equal(got[0], r.err_rand.cpu().numpy())
+        assert np.array_equal(got[1], r.err_det.cpu().numpy())
