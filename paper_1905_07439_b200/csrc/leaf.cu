@@ -1202,6 +1202,10 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
       if (e != cudaErrorNotSupported) return e;
       return run_truth<TIn, 128, 128, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
     }
+    // ragged sizes (config 2: 243) do better with 128 x 64 tiles and 128-thread
+    // CTAs (19.5 vs 18.0 TFLOP/s); whole 128-multiples with 128 x 128
+    if (forced == 0 && M >= 128 && N >= 128 && K >= 1 && (M % 128 || N % 128))
+      return run_truth<TIn, 128, 64, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
     if ((forced == 0 || forced == 302) && M >= 128 && N >= 128 && K >= 1)
       return run_truth<TIn, 128, 128, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
     if (forced == 303 && M >= 128 && N >= 128 && K >= 1)  // bulk kernel at any size
@@ -1212,6 +1216,10 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
       return run_truth<TIn, 128, 128, 16, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
     if (forced == 301 && M >= 128 && N >= 128 && K >= 1)
       return run_truth<TIn, 128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (forced == 304 && M >= 128 && N >= 64 && K >= 1)  // half the register file per CTA
+      return run_truth<TIn, 128, 64, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (forced == 305 && M >= 64 && N >= 64 && K >= 1)
+      return run_truth<TIn, 64, 64, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
     if (forced == 306 && M >= 128 && N >= 128 && K >= 1)
       return run_truth<TIn, 128, 128, 32, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
   }

@@ -17,6 +17,8 @@ CASES = [  # (label, dtype_in, dtype_out, batch, m)
     ("c1 leaf f32 64", 1, 1, 49 * 400, 64),
     ("c4 leaf f16 128", 2, 2, 2401 * 16, 128),
     ("truth f64<-f32 243", 1, 0, 200, 243),
+    ("truth f64<-f32 256", 1, 0, 100, 256),
+    ("truth f64<-f64 256", 0, 0, 100, 256),
     ("truth f64<-f32 2048", 1, 0, 2, 2048),
     ("truth f64<-f16 2048", 2, 0, 2, 2048),
     ("truth f64<-f16 2048x16", 2, 0, 16, 2048),
