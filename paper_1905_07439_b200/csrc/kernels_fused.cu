@@ -678,11 +678,12 @@ struct SubtreeReg {
   static constexpr size_t header() {
     return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 3 * sizeof(GatherTab<n>);
   }
-  // level-q0 blocks of the next subtree, prefetched by TMA bulk copies into
-  // [2 buffers][X, Y][span] (4-byte elements, one subtree per step): each
-  // block is copied as the 16-byte-aligned span that encloses it
-  static constexpr bool kStage = STG && sizeof(T) == 4 && SUB == 1;
-  static constexpr int spanE = ((s0 * s0 + 4) + 3) / 4 * 4;
+  // level-q0 blocks of the next step's SUB subtrees (consecutive in HBM),
+  // prefetched by TMA bulk copies into [2 buffers][X, Y][span] (4-byte
+  // elements): each operand's blocks are copied as the 16-byte-aligned span
+  // that encloses them
+  static constexpr bool kStage = STG && sizeof(T) == 4;
+  static constexpr int spanE = ((SUB * s0 * s0 + 4) + 3) / 4 * 4;  // SUB consecutive blocks
   static constexpr int stage_elems = kStage ? 2 * 2 * spanE : 0;
   static constexpr size_t smem_bytes() {
     return header() + sizeof(T) * ((size_t)SUB * slot + stage_elems) + (kStage ? 16 : 0);
@@ -881,7 +882,8 @@ subtree_reg_kernel(
     auto issue = [&](int kp, unsigned bsel) {  // one thread
       const T* gx = x + t * xy_tstride + (int64_t)kp * blkE;
       const T* gy = y + t * xy_tstride + (int64_t)kp * blkE;
-      const unsigned nx = span_bytes(gx, blkE * sizeof(T)), ny = span_bytes(gy, blkE * sizeof(T));
+      const unsigned nb = (unsigned)(kend - kp < SUB ? kend - kp : SUB) * blkE * sizeof(T);
+      const unsigned nx = span_bytes(gx, nb), ny = span_bytes(gy, nb);
       T* d = stg + bsel * 2 * S::spanE;
       fence_proxy_async();
       mbar_expect_tx(&mbar[bsel], nx + ny);
@@ -1282,6 +1284,8 @@ cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride,
   RBC_REG(1, true, false)
   RBC_REG(1, false, true)
   RBC_REG(3, false, false)
+  RBC_REG(2, false, true)
+  RBC_REG(3, false, true)
 #undef RBC_REG
   return cudaErrorInvalidValue;
 }

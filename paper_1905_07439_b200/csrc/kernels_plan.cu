@@ -22,6 +22,8 @@
 #include "formulas_gen.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace rbc {
 
 namespace {
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) expand_plan_kernel(
 // sign is applied to the child value), so every register index is static.
 // Values equal two expand_plan_kernel launches; the level-(q+1) array never
 // goes through HBM.
-template <class F, class T, int W, int WHICH>
+template <class F, class T, int W, int WHICH, bool SYNC>
 __global__ void __launch_bounds__(kThreads) expand2_plan_kernel(
     const T* __restrict__ x, int64_t x_tstride, int K, int s, T* __restrict__ out,
     const PlanLevel* __restrict__ plans, int64_t plan_tstride, int level, int64_t ntr) {
@@ -93,8 +95,10 @@ __global__ void __launch_bounds__(kThreads) expand2_plan_kernel(
   const int mb1 = s / n, mb2 = mb1 / n;
   const int P = (mb2 * mb2) / W;
   const int64_t items = (int64_t)K * P;
-  const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (e >= items) return;
+  int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const bool live = e < items;
+  if (!SYNC && !live) return;
+  if (!live) e = items - 1;  // SYNC: idle lanes mirror the last item, stores masked
   const int Kp = (int)(e / P);
   const int p = (int)(e - (int64_t)Kp * P);
   const int pos = p * W;
@@ -147,8 +151,13 @@ __global__ void __launch_bounds__(kThreads) expand2_plan_kernel(
         F::template expand_u<T, W>(g1, o, l1r, l1c);
       else
         F::template expand_v<T, W>(g1, o, l1r, l1c);
+      if (live) {
 #pragma unroll
-      for (int r2 = 0; r2 < R; ++r2) pstore<T, W>(ob + (int64_t)(r1 * R + r2) * mb2 * mb2, o[r2]);
+        for (int r2 = 0; r2 < R; ++r2) pstore<T, W>(ob + (int64_t)(r1 * R + r2) * mb2 * mb2, o[r2]);
+      }
+      // SYNC: the CTA writes the grandchildren of r1 together, so each output
+      // block's lines are completed in one short window (write locality)
+      if (SYNC) __syncthreads();
     }
   }
 }
@@ -222,11 +231,28 @@ cudaError_t expand2_plan_w(int which, const void* x, int64_t xs, int64_t K, int6
                            cudaStream_t st) {
   const int64_t mb2 = s / (F::n * F::n);
   const dim3 grid = grid_for(K * (mb2 * mb2 / W), ntr);
-  if (which == 0)
-    expand2_plan_kernel<F, T, W, 0><<<grid, kThreads, 0, st>>>(
+  // Lockstep (a CTA barrier after each r1) when the grandchild blocks are
+  // small: a thread writes R^2 blocks, so without it each output line
+  // collects its pieces from drifting warps over the whole launch and L2
+  // evicts to scattered DRAM pages (config 2, 27x27 binary32 blocks: 0.534 ->
+  // 0.332 ms/launch).  Large blocks have whole lines per warp store, where the
+  // barrier only costs (config 5: 0.68 vs 0.73).  RBC_EXPAND2_SYNC=0/1 forces.
+  static const int forced = [] {
+    const char* v = getenv("RBC_EXPAND2_SYNC");
+    return v ? atoi(v) : -1;
+  }();
+  const bool sync = forced >= 0 ? forced != 0 : mb2 * mb2 * (int64_t)sizeof(T) < (64 << 10);
+  if (which == 0 && sync)
+    expand2_plan_kernel<F, T, W, 0, true><<<grid, kThreads, 0, st>>>(
+        (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
+  else if (which == 0)
+    expand2_plan_kernel<F, T, W, 0, false><<<grid, kThreads, 0, st>>>(
+        (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
+  else if (sync)
+    expand2_plan_kernel<F, T, W, 1, true><<<grid, kThreads, 0, st>>>(
         (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
   else
-    expand2_plan_kernel<F, T, W, 1><<<grid, kThreads, 0, st>>>(
+    expand2_plan_kernel<F, T, W, 1, false><<<grid, kThreads, 0, st>>>(
         (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
   return cudaGetLastError();
 }
