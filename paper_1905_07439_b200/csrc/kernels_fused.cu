@@ -1286,6 +1286,8 @@ cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride,
   RBC_REG(3, false, false)
   RBC_REG(2, false, true)
   RBC_REG(3, false, true)
+  RBC_REG(1, true, true)
+  RBC_REG(2, true, true)
 #undef RBC_REG
   return cudaErrorInvalidValue;
 }

@@ -501,9 +501,10 @@ cudaError_t run_smem(int64_t batch, const void* x, int64_t xs, const void* y, in
 // issued by one thread one group ahead -- no load instructions in the
 // threads, loads overlap the FP work inside every CTA.  Same per-element
 // chains as leaf_smem_kernel.
-template <class T, int M, int TR>
+template <class T, int M, int TM, int TN>
 struct SmemBulk {
-  static constexpr int TPL = (M / TR) * (M / TR);
+  static_assert(M % TM == 0 && M % TN == 0, "leaf tiling");
+  static constexpr int TPL = (M / TM) * (M / TN);
   static constexpr int LPB = 256 / TPL;
   static constexpr int E = M * M;
   static constexpr int SPAN = ((E * (int)sizeof(T) + 16) + 15) / 16 * 16;  // bytes per operand slot
@@ -511,11 +512,11 @@ struct SmemBulk {
   static constexpr size_t smem = 2 * stage_bytes + 2 * sizeof(uint64_t);
 };
 
-template <class T, int M, int TR>
+template <class T, int M, int TM, int TN>
 __global__ void __launch_bounds__(256) leaf_smem_bulk_kernel(int64_t batch, const T* __restrict__ x,
                                                              int64_t xs, const T* __restrict__ y,
                                                              int64_t ys, T* __restrict__ out) {
-  using S = SmemBulk<T, M, TR>;
+  using S = SmemBulk<T, M, TM, TN>;
   constexpr int TPL = S::TPL, LPB = S::LPB, E = S::E;
   using A = Arith<T>;
   extern __shared__ __align__(128) unsigned char bulk_smem[];
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(256) leaf_smem_bulk_kernel(int64_t batch, cons
   };
   const int l = threadIdx.x / TPL;
   const int r = threadIdx.x - l * TPL;
-  const int ti = (r / (M / TR)) * TR, tj = (r % (M / TR)) * TR;
+  const int ti = (r / (M / TN)) * TM, tj = (r % (M / TN)) * TN;
   int64_t g = blockIdx.x;
   if (threadIdx.x == 0 && g < groups) issue(g, 0);
   for (int it = 0; g < groups; g += gridDim.x, ++it) {
@@ -564,38 +565,43 @@ __global__ void __launch_bounds__(256) leaf_smem_bulk_kernel(int64_t batch, cons
       const T* gy = y + (b0 + l) * ys;
       const T* Xs = reinterpret_cast<const T*>(slot(stg, l, 0) + (reinterpret_cast<uintptr_t>(gx) & 15));
       const T* Ys = reinterpret_cast<const T*>(slot(stg, l, 1) + (reinterpret_cast<uintptr_t>(gy) & 15));
-      T acc[TR][TR];
+      // operands of step k + 1 are loaded while step k multiplies (k fully
+      // unrolled); every output keeps its sequential k chain
+      T acc[TM][TN], a[2][TM], bb[2][TN];
 #pragma unroll
-      for (int i = 0; i < TR; ++i)
+      for (int i = 0; i < TM; ++i) a[0][i] = Xs[(ti + i) * M];
 #pragma unroll
-        for (int j = 0; j < TR; ++j) acc[i][j] = A::mul(Xs[(ti + i) * M], Ys[tj + j]);
-#pragma unroll 3
-      for (int k = 1; k < M; ++k) {
-        T a[TR], bb[TR];
+      for (int j = 0; j < TN; ++j) bb[0][j] = Ys[tj + j];
 #pragma unroll
-        for (int i = 0; i < TR; ++i) a[i] = Xs[(ti + i) * M + k];
+      for (int k = 0; k < M; ++k) {
+        const int c = k & 1;
+        if (k + 1 < M) {
 #pragma unroll
-        for (int j = 0; j < TR; ++j) bb[j] = Ys[k * M + tj + j];
+          for (int i = 0; i < TM; ++i) a[c ^ 1][i] = Xs[(ti + i) * M + k + 1];
 #pragma unroll
-        for (int i = 0; i < TR; ++i)
+          for (int j = 0; j < TN; ++j) bb[c ^ 1][j] = Ys[(k + 1) * M + tj + j];
+        }
 #pragma unroll
-          for (int j = 0; j < TR; ++j) acc[i][j] = A::add(acc[i][j], A::mul(a[i], bb[j]));
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j)
+            acc[i][j] = k == 0 ? A::mul(a[c][i], bb[c][j]) : A::add(acc[i][j], A::mul(a[c][i], bb[c][j]));
       }
       T* o = out + (b0 + l) * (int64_t)E;
 #pragma unroll
-      for (int i = 0; i < TR; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TR; ++j) o[(ti + i) * M + tj + j] = acc[i][j];
+        for (int j = 0; j < TN; ++j) o[(ti + i) * M + tj + j] = acc[i][j];
     }
     __syncthreads();  // stage stg is refilled next iteration (issued above it)
   }
 }
 
-template <class T, int M, int TR>
+template <class T, int M, int TM, int TN>
 cudaError_t run_smem_bulk(int64_t batch, const void* x, int64_t xs, const void* y, int64_t ys,
                           void* out, cudaStream_t st) {
-  using S = SmemBulk<T, M, TR>;
-  auto kern = leaf_smem_bulk_kernel<T, M, TR>;
+  using S = SmemBulk<T, M, TM, TN>;
+  auto kern = leaf_smem_bulk_kernel<T, M, TM, TN>;
   static const cudaError_t attr =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem);
   if (attr != cudaSuccess) return attr;
@@ -617,8 +623,15 @@ cudaError_t small_square(int64_t batch, int64_t M, const void* x, int64_t xs, co
                          int64_t ys, void* out, cudaStream_t st) {
   if constexpr (std::is_same<TIn, TAcc>::value && sizeof(TIn) >= 4) {
     const int f = tile_override();
+    // 3 x 3 outputs per thread, 3 leaves per 243-thread CTA, 3 CTAs per SM
+    // (c3: 0.884 ms/launch).  3 x 9 ("211": 12 loads per 27 multiply-adds
+    // instead of 6 per 9) fits one CTA per SM and runs slower (1.13)
     if (M == 27 && batch >= 2048 && (f == 0 || f == 210))
-      return run_smem_bulk<TIn, 27, 3>(batch, x, xs, y, ys, out, st);
+      return run_smem_bulk<TIn, 27, 3, 3>(batch, x, xs, y, ys, out, st);
+    if (M == 27 && batch >= 2048 && f == 211)
+      return run_smem_bulk<TIn, 27, 3, 9>(batch, x, xs, y, ys, out, st);
+    if (M == 27 && batch >= 2048 && f == 212)
+      return run_smem_bulk<TIn, 27, 9, 3>(batch, x, xs, y, ys, out, st);
   }
   switch (M) {
     case 27: return run_smem<TIn, TAcc, 27, 3>(batch, x, xs, y, ys, out, st);

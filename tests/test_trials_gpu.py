@@ -161,12 +161,13 @@ def test_binary32_leaf_tiles_bitwise(shape, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("label", ["f64", "f32"])
-@pytest.mark.parametrize("tile", ["0", "205"])
+@pytest.mark.parametrize("tile", ["0", "205", "210", "211", "212"])
 def test_small_square_leaves_bitwise(label, tile, monkeypatch):
     """27x27 leaves in long batches (config 3's leaves) run on the bulk-copy
-    persistent kernel (tile "0") or the single-shot shared-memory kernel
-    ("205"): both equal the oracle; the batch is odd so groups end ragged and
-    leaves sit at 8-byte offsets."""
+    persistent kernel (tile "0" = "210": 3 x 3 outputs per thread; "211"
+    3 x 9, "212" 9 x 3) or the single-shot shared-memory kernel ("205"): all equal the
+    oracle; the batch is odd so groups end ragged and leaves sit at 8-byte
+    offsets."""
     from paper_1905_07439_b200 import engine
     from paper_1905_07439_b200.precision import parse_precision
 
