@@ -654,7 +654,12 @@ cudaError_t launch_subtree2w(const void* x, const void* y, int64_t xy_tstride, i
 // flips each child before contracting -- the same values the breadth-first
 // kernels produce.  Z overwrites X1 in place: a lane writes exactly the rows
 // {k*M + i} of block r1 it read.
-template <class F, class T, int M, int SUB, bool STG = false>
+// STG: 0 = operands read straight from HBM in stage A; 1 = the next step's
+// level-q0 blocks prefetched by TMA bulk copies into two staging buffers;
+// 2 = one staging buffer and two X1/Y1 slots, so the contraction of step k
+// (stage C) and the expansion of step k + 1 (stage A) share one phase between
+// two CTA barriers (2 barriers per step instead of 3).
+template <class F, class T, int M, int SUB, int STG = 0>
 struct SubtreeReg {
   static constexpr int n = F::n;
   static constexpr int R = F::R;
@@ -678,15 +683,18 @@ struct SubtreeReg {
   static constexpr size_t header() {
     return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 3 * sizeof(GatherTab<n>);
   }
-  // level-q0 blocks of the next step's SUB subtrees (consecutive in HBM),
-  // prefetched by TMA bulk copies into [2 buffers][X, Y][span] (4-byte
-  // elements): each operand's blocks are copied as the 16-byte-aligned span
-  // that encloses them
-  static constexpr bool kStage = STG && sizeof(T) == 4;
+  // level-q0 blocks of a step's SUB subtrees (consecutive in HBM), prefetched
+  // by TMA bulk copies into [buffers][X, Y][span] (4-byte elements): each
+  // operand's blocks are copied as the 16-byte-aligned span that encloses them
+  static constexpr bool kStage = STG != 0 && sizeof(T) == 4;
+  static constexpr bool kPipe = kStage && STG == 2;
+  static constexpr int kBufs = kPipe ? 1 : 2;   // staging buffers
+  static constexpr int kBanks = kPipe ? 2 : 1;  // X1/Y1 slot sets
   static constexpr int spanE = ((SUB * s0 * s0 + 4) + 3) / 4 * 4;  // SUB consecutive blocks
-  static constexpr int stage_elems = kStage ? 2 * 2 * spanE : 0;
+  static constexpr int stage_elems = kStage ? kBufs * 2 * spanE : 0;
+  static constexpr int bank = SUB * slot;
   static constexpr size_t smem_bytes() {
-    return header() + sizeof(T) * ((size_t)SUB * slot + stage_elems) + (kStage ? 16 : 0);
+    return header() + sizeof(T) * ((size_t)kBanks * bank + stage_elems) + (kStage ? 16 : 0);
   }
 };
 
@@ -777,7 +785,7 @@ __device__ __forceinline__ Pack<T, M> leaf_row(const Pack<T, M>& xg, const Pack<
   return m;
 }
 
-template <class F, class T, int M, int SUB, bool ROT, bool STG>
+template <class F, class T, int M, int SUB, bool ROT, int STG>
 __global__ void __launch_bounds__(SubtreeReg<F, T, M, SUB, STG>::NT, SubtreeReg<F, T, M, SUB, STG>::kMinBlocks)
 subtree_reg_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0, int kchunk,
@@ -793,6 +801,9 @@ subtree_reg_kernel(
   GatherTab<n>* tabs =
       reinterpret_cast<GatherTab<n>*>(smem_raw + ((sizeof(PlanLevel) * 2 + 15) / 16) * 16);
   T* sm = reinterpret_cast<T*>(smem_raw + S::header());
+  // staged copies of the level-q0 blocks: [buf][X, Y][spanE]
+  T* stg = sm + S::kBanks * S::bank;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stg + S::stage_elems);
 
   // stage-B role of this lane: group -> (subtree slot u, level-1 block r1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -812,14 +823,12 @@ subtree_reg_kernel(
 
   const int kbeg = blockIdx.x * kchunk;
   const int kend = kbeg + kchunk < K0 ? kbeg + kchunk : K0;
-  unsigned ctr = 0;  // staged steps consumed (buffer ctr & 1, phase (ctr >> 1) & 1)
+  unsigned ctr = 0;  // staged copies consumed (buffer ctr % kBufs, phase (ctr / kBufs) & 1)
   if (S::kStage && threadIdx.x == 0) {
-    uint64_t* mb = reinterpret_cast<uint64_t*>(reinterpret_cast<T*>(smem_raw + S::header()) +
-                                               SUB * S::slot + S::stage_elems);
-    mbar_init(&mb[0], 1);
-    mbar_init(&mb[1], 1);
+    for (int b = 0; b < S::kBufs; ++b) mbar_init(&mbar[b], 1);
     mbar_init_fence();
   }
+  constexpr int blkE = s0 * s0;
 
   for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
     __syncthreads();
@@ -875,10 +884,6 @@ subtree_reg_kernel(
       c_msk[it] = sign_mask(pl1.neg[0][hi] ^ pl1.neg[2][hj]);
     }
     bool ok = true;
-    // staged copies of the level-q0 blocks: [buf][X, Y][spanE]
-    T* stg = sm + SUB * S::slot;
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(stg + S::stage_elems);
-    constexpr int blkE = s0 * s0;
     auto issue = [&](int kp, unsigned bsel) {  // one thread
       const T* gx = x + t * xy_tstride + (int64_t)kp * blkE;
       const T* gy = y + t * xy_tstride + (int64_t)kp * blkE;
@@ -890,112 +895,144 @@ subtree_reg_kernel(
       bulk_g2s(d, span_start(gx), nx, &mbar[bsel]);
       bulk_g2s(d + S::spanE, span_start(gy), ny, &mbar[bsel]);
     };
-    if (S::kStage && threadIdx.x == 0 && kbeg < kend) issue(kbeg, ctr & 1);
-
-    for (int k0 = kbeg; k0 < kend; k0 += SUB, ++ctr) {
-      const int nsub = kend - k0 < SUB ? kend - k0 : SUB;  // live subtree slots
-      if (S::kStage) mbar_wait(&mbar[ctr & 1], (ctr >> 1) & 1);
-      __syncthreads();
-      // ---- stage A: level q0 -> q0+1, level-q0 blocks -> X1 / Y1 (base order, signed)
-      {
-        const T* gx = x + t * xy_tstride + (int64_t)k0 * blkE;
-        const T* gy = y + t * xy_tstride + (int64_t)k0 * blkE;
-        const T* xsrc = gx;
-        const T* ysrc = gy;
-        if (S::kStage) {
-          const T* d = stg + (ctr & 1) * 2 * S::spanE;
-          xsrc = d + ((reinterpret_cast<uintptr_t>(gx) & 15) / sizeof(T));
-          ysrc = d + S::spanE + ((reinterpret_cast<uintptr_t>(gy) & 15) / sizeof(T));
-        }
+    // ---- stage A: level q0 -> q0+1, level-q0 blocks -> X1 / Y1 (base order, signed)
+    auto stage_a = [&](int k0, const T* buf, T* dst) {
+      const int nsub = kend - k0 < SUB ? kend - k0 : SUB;
+      const T* gx = x + t * xy_tstride + (int64_t)k0 * blkE;
+      const T* gy = y + t * xy_tstride + (int64_t)k0 * blkE;
+      const T* xsrc = gx;
+      const T* ysrc = gy;
+      if (S::kStage) {
+        xsrc = buf + ((reinterpret_cast<uintptr_t>(gx) & 15) / sizeof(T));
+        ysrc = buf + S::spanE + ((reinterpret_cast<uintptr_t>(gy) & 15) / sizeof(T));
+      }
 #pragma unroll
-        for (int it = 0; it < S::IA; ++it) {
-          const int e = threadIdx.x + it * NT;
-          if (e < nsub * 2 * kids1) {
-            const int which = (e - (e / (2 * kids1)) * 2 * kids1) >= kids1;
-            if (which)
-              expand_to_children<F, T, 1>(ysrc + a_src[it], load_tab(tabs[1]), sm + a_dst[it], a_msk[it]);
-            else
-              expand_to_children<F, T, 0>(xsrc + a_src[it], load_tab(tabs[0]), sm + a_dst[it], a_msk[it]);
-          }
+      for (int it = 0; it < S::IA; ++it) {
+        const int e = threadIdx.x + it * NT;
+        if (e < nsub * 2 * kids1) {
+          const int which = (e - (e / (2 * kids1)) * 2 * kids1) >= kids1;
+          if (which)
+            expand_to_children<F, T, 1>(ysrc + a_src[it], load_tab(tabs[1]), dst + a_dst[it], a_msk[it]);
+          else
+            expand_to_children<F, T, 0>(xsrc + a_src[it], load_tab(tabs[0]), dst + a_dst[it], a_msk[it]);
         }
       }
-      __syncthreads();
-      if (S::kStage && threadIdx.x == 0 && k0 + SUB < kend) issue(k0 + SUB, (ctr + 1) & 1);
-
-      // ---- stage B: level q0+1 -> leaves -> level q0+1, in registers
-      {
-        const T* X1 = sm;
-        const T* Y1 = sm + kids1 * RP;
-        P xf[n * n], yf[n * n];
+    };
+    // ---- stage B: level q0+1 -> leaves -> level q0+1, in registers
+    auto stage_b = [&](int k0, T* base) {
+      const int nsub = kend - k0 < SUB ? kend - k0 : SUB;
+      const T* X1 = base;
+      const T* Y1 = base + kids1 * RP;
+      P xf[n * n], yf[n * n];
+#pragma unroll
+      for (int k = 0; k < n * n; ++k) {
+        const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          xf[k].v[j] = X1[o + (ROT ? col_of[j] : j) * RP];
+          yf[k].v[j] = Y1[o + j * RP];
+        }
+      }
+      const int xlr = pl1.perm[0][n - 1], xlc = pl1.perm[1][n - 1];
+      const int ylr = pl1.perm[1][n - 1], ylc = pl1.perm[2][n - 1];
+      P z[n * n];
+#pragma unroll
+      for (int r2 = 0; r2 < R; ++r2) {
+        const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
+        const P yg = F::template expand_v1<T, M>(yf, r2, ylr, ylc);
+        const P m = leaf_row<T, M, ROT>(xg, yg, gbase, gbase + rowA, gbase + rowB, li == 2);
+        F::template contract_w_step<T, M>(z, m, r2);
+      }
+      F::template contract_w_finish<T, M>(z);
+      if (in_range && bu < nsub) {
+        T* Z1 = base;
 #pragma unroll
         for (int k = 0; k < n * n; ++k) {
           const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
 #pragma unroll
-          for (int j = 0; j < M; ++j) {
-            xf[k].v[j] = X1[o + (ROT ? col_of[j] : j) * RP];
-            yf[k].v[j] = Y1[o + j * RP];
-          }
+          for (int j = 0; j < M; ++j) Z1[o + j * RP] = z[k].v[j];
         }
-        const int xlr = pl1.perm[0][n - 1], xlc = pl1.perm[1][n - 1];
-        const int ylr = pl1.perm[1][n - 1], ylc = pl1.perm[2][n - 1];
-        P z[n * n];
+      }
+    };
+    // ---- stage C: level q0+1 -> q0, Z1 -> HBM (row-major)
+    auto stage_c = [&](int k0, const T* base) {
+      const int nsub = kend - k0 < SUB ? kend - k0 : SUB;
+      const GatherTab<n> sc = load_tab(tabs[2]);
 #pragma unroll
-        for (int r2 = 0; r2 < R; ++r2) {
-          const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
-          const P yg = F::template expand_v1<T, M>(yf, r2, ylr, ylc);
-          const P m = leaf_row<T, M, ROT>(xg, yg, gbase, gbase + rowA, gbase + rowB, li == 2);
-          F::template contract_w_step<T, M>(z, m, r2);
-        }
-        F::template contract_w_finish<T, M>(z);
-        if (in_range && bu < nsub) {
-          T* Z1 = sm;
+      for (int it = 0; it < S::IC; ++it) {
+        const int e = threadIdx.x + it * NT;
+        if (e < nsub * kids1) {
+          using O = PackOps<T, 1>;
+          const int u = e / kids1, pos = e - (e / kids1) * kids1;
+          const T* zc = base + c_src[it];
+          Pack<T, 1> pr[R];
+#pragma unroll
+          for (int r = 0; r + 1 < R; r += 2) {
+            const Pack<T, 2> v = pload<T, 2>(zc + r);
+            pr[r].v[0] = flip_sign(v.v[0], c_msk[it]);
+            pr[r + 1].v[0] = flip_sign(v.v[1], c_msk[it]);
+          }
+          if (R & 1) pr[R - 1].v[0] = flip_sign(zc[R - 1], c_msk[it]);
+          Pack<T, 1> o[n * n];
+          F::template contract_w<T, 1>(pr, o);
+          const int row = pos / s1, col = pos - (pos / s1) * s1;
+          T* d = out + (t * K0 + k0 + u) * (int64_t)s0 * s0 + row * s0 + col;
 #pragma unroll
           for (int k = 0; k < n * n; ++k) {
-            const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
-#pragma unroll
-            for (int j = 0; j < M; ++j) Z1[o + j * RP] = z[k].v[j];
+            const Pack<T, 1> val = O::flip(o[k], sc.msk[k]);
+            if (nonfinite) ok = ok && O::all_finite(val);
+            pstore<T, 1>(d + sc.off[k], val);
           }
         }
       }
-      __syncthreads();
+    };
 
-      // ---- stage C: level q0+1 -> q0, Z1 -> HBM (row-major)
-      {
-        const GatherTab<n> sc = load_tab(tabs[2]);
-#pragma unroll
-        for (int it = 0; it < S::IC; ++it) {
-          const int e = threadIdx.x + it * NT;
-          if (e < nsub * kids1) {
-            using O = PackOps<T, 1>;
-            const int u = e / kids1, pos = e - (e / kids1) * kids1;
-            const T* zc = sm + c_src[it];
-            Pack<T, 1> pr[R];
-#pragma unroll
-            for (int r = 0; r + 1 < R; r += 2) {
-              const Pack<T, 2> v = pload<T, 2>(zc + r);
-              pr[r].v[0] = flip_sign(v.v[0], c_msk[it]);
-              pr[r + 1].v[0] = flip_sign(v.v[1], c_msk[it]);
-            }
-            if (R & 1) pr[R - 1].v[0] = flip_sign(zc[R - 1], c_msk[it]);
-            Pack<T, 1> o[n * n];
-            F::template contract_w<T, 1>(pr, o);
-            const int row = pos / s1, col = pos - (pos / s1) * s1;
-            T* d = out + (t * K0 + k0 + u) * (int64_t)s0 * s0 + row * s0 + col;
-#pragma unroll
-            for (int k = 0; k < n * n; ++k) {
-              const Pack<T, 1> val = O::flip(o[k], sc.msk[k]);
-              if (nonfinite) ok = ok && O::all_finite(val);
-              pstore<T, 1>(d + sc.off[k], val);
-            }
+    if constexpr (S::kPipe) {
+      // B(k) | barrier | C(k) + A(k+1) | barrier ...; one staging buffer,
+      // refilled as soon as stage A has consumed it (B of the next step
+      // covers the copy)
+      if (kbeg < kend) {
+        if (threadIdx.x == 0) issue(kbeg, 0);
+        __syncthreads();  // tables
+        mbar_wait(&mbar[0], ctr & 1);
+        ++ctr;
+        stage_a(kbeg, stg, sm);
+        __syncthreads();
+        if (threadIdx.x == 0 && kbeg + SUB < kend) issue(kbeg + SUB, 0);
+        int bsel = 0;
+        for (int k0 = kbeg; k0 < kend; k0 += SUB, bsel ^= 1) {
+          T* cur = sm + bsel * S::bank;
+          stage_b(k0, cur);
+          __syncthreads();
+          const bool next = k0 + SUB < kend;
+          if (next) {
+            mbar_wait(&mbar[0], ctr & 1);
+            ++ctr;
           }
+          stage_c(k0, cur);
+          if (next) stage_a(k0 + SUB, stg, sm + (bsel ^ 1) * S::bank);
+          __syncthreads();
+          if (threadIdx.x == 0 && k0 + 2 * SUB < kend) issue(k0 + 2 * SUB, 0);
         }
+      }
+    } else {
+      if (S::kStage && threadIdx.x == 0 && kbeg < kend) issue(kbeg, ctr & 1);
+      for (int k0 = kbeg; k0 < kend; k0 += SUB, ++ctr) {
+        if (S::kStage) mbar_wait(&mbar[ctr & 1], (ctr >> 1) & 1);
+        __syncthreads();
+        stage_a(k0, stg + (ctr & 1) * 2 * S::spanE, sm);
+        __syncthreads();
+        if (S::kStage && threadIdx.x == 0 && k0 + SUB < kend) issue(k0 + SUB, (ctr + 1) & 1);
+        stage_b(k0, sm);
+        __syncthreads();
+        stage_c(k0, sm);
       }
     }
     if (nonfinite && !ok) nonfinite[t] = 1;
   }
 }
 
-template <class F, class T, int M, int SUB, bool ROT, bool STG>
+template <class F, class T, int M, int SUB, bool ROT, int STG>
 cudaError_t launch_subtree_reg_v(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
                                  void* out, const PlanLevel* plans, int64_t pts, int q0,
                                  int64_t ntr, uint8_t* nonfinite, cudaStream_t st, int kchunk) {
@@ -1243,7 +1280,10 @@ cudaError_t launch_subtree_lane_v(const void* x, const void* y, int64_t xy_tstri
 // Tuning aids (config 2, ms per launch): RBC_SUBTREE_SUB subtrees per CTA
 // step (1: 3.28, 3: 3.82), RBC_SUBTREE_ROT=1 rotated 6-shuffle leaf (3.38),
 // RBC_SUBTREE_STAGE TMA bulk prefetch of the level-q0 blocks (default 1:
-// 3.01; 0: 3.28; per-element cp.async: 3.40),
+// 3.01; 0: 3.28; per-element cp.async: 3.40; 2 = one staging buffer and
+// double-buffered X1/Y1, stage C(k) sharing a phase with stage A(k+1), two
+// barriers per step: 3.01 -- barriers are not what bounds the kernel;
+// SUB 2 + STAGE 2: 3.64, five CTAs per SM no longer fit),
 // RBC_SUBTREE_CHUNK subtrees per CTA (24; 8: 3.44, 48: 3.46).
 template <class F, class T, int M>
 cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
@@ -1277,17 +1317,16 @@ cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride,
     return launch_subtree_lane_v<F, T, M, 2>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr,
                                              nonfinite, st, kchunk);
 #define RBC_REG(SB, RT, SG)                                                                   \
-  if (sub == SB && (rot != 0) == RT && (stg != 0) == SG)                                        \
+  if (sub == SB && (rot != 0) == RT && stg == SG)                                               \
     return launch_subtree_reg_v<F, T, M, SB, RT, SG>(x, y, xy_tstride, K0, out, plans, pts, q0, \
                                                      ntr, nonfinite, st, kchunk);
-  RBC_REG(1, false, false)
-  RBC_REG(1, true, false)
-  RBC_REG(1, false, true)
-  RBC_REG(3, false, false)
-  RBC_REG(2, false, true)
-  RBC_REG(3, false, true)
-  RBC_REG(1, true, true)
-  RBC_REG(2, true, true)
+  RBC_REG(1, false, 0)
+  RBC_REG(1, true, 0)
+  RBC_REG(1, false, 1)
+  RBC_REG(1, false, 2)
+  RBC_REG(2, false, 1)
+  RBC_REG(2, false, 2)
+  RBC_REG(3, false, 1)
 #undef RBC_REG
   return cudaErrorInvalidValue;
 }
