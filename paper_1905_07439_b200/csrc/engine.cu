@@ -313,22 +313,42 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
       e = stage_done(e, st);
       if (e != cudaSuccess) return fail_cuda(e, "leaf", __FILE__, __LINE__);
     }
-    // --- contractions, innermost level first
+    // --- contractions, innermost level first (plan path: two levels per pass
+    // where an instantiation exists, the mirror of the expansions)
     const void* cur = ping;
     int64_t K = K_q0, mb = s_q0;
-    for (int q = q0 - 1; q >= 0; --q) {
+    for (int q = q0 - 1; q >= 0;) {
       const int n = g.lv[q].n, R = g.lv[q].R;
+      const int64_t pts = p.Tp == 1 ? 0 : g.Q;
+      const PlanLevel* pl = p.plans + (p.Tp == 1 ? 0 : t0 * g.Q);
+      cudaError_t e = cudaErrorNotSupported;
+      if (p.plan && expand2_enabled() && q >= 1 && expand2_supported(dt, p.formula)) {
+        const int64_t K2 = K / R / g.lv[q - 1].R;  // level-(q-1) parents per trial
+        void* dst = q == 1 ? (char*)p.out + (size_t)t0 * N2 * es : (cur == ping ? pong : ping);
+        uint8_t* nf = (q == 1 && p.nonfinite) ? p.nonfinite + t0 : nullptr;
+        const double sq = (double)(mb * n * n);
+        Stage stage(st, "contract2_plan",
+                    ((double)nt * K * mb * mb + (double)nt * K2 * sq * sq) * es,
+                    (double)nt * K * mb * mb * (R + 1) * n * n * 2.0);
+        e = launch_contract2_plan(dt, p.formula, cur, K2, mb, dst, pl, pts, q - 1, nt, nf, st);
+        if (e != cudaErrorNotSupported) {
+          e = stage_done(e, st);
+          if (e != cudaSuccess) return fail_cuda(e, "contract2", __FILE__, __LINE__);
+          K = K2;
+          cur = dst;
+          mb *= n * n;
+          q -= 2;
+          continue;
+        }
+      }
       K /= R;
       void* dst = q == 0 ? (char*)p.out + (size_t)t0 * N2 * es : (cur == ping ? pong : ping);
       uint8_t* nf = (q == 0 && p.nonfinite) ? p.nonfinite + t0 : nullptr;
-      cudaError_t e;
       const double sq = (double)(mb * n);
       Stage stage(st, p.plan ? "contract_plan" : "contract_dense",
                   ((double)nt * K * R * mb * mb + (double)nt * K * sq * sq) * es,
                   (double)nt * K * sq * sq * R * 2.0);
       if (p.plan) {
-        const int64_t pts = p.Tp == 1 ? 0 : g.Q;
-        const PlanLevel* pl = p.plans + (p.Tp == 1 ? 0 : t0 * g.Q);
         e = launch_contract_plan(dt, p.formula, cur, K, mb, dst, pl, pts, q, nt, nf, st);
       } else {
         const int64_t cts = p.Tc[q] == 1 ? 0 : (int64_t)R * n * n;
@@ -339,6 +359,7 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
       if (e != cudaSuccess) return fail_cuda(e, "contract", __FILE__, __LINE__);
       cur = dst;
       mb *= n;
+      --q;
     }
   }
   return RBC_OK;

@@ -59,6 +59,12 @@ cudaError_t launch_expand_plan(int dtype, int formula, int which, const void* x,
 
 // Contraction of one level: ch (T, K, R, mb, mb) -> out (T, K, n*mb, n*mb).
 // nonfinite (optional, T bytes) gets 1 for trials with a non-finite output.
+// Two contraction levels (level + 1 into level) in one pass; `ch` holds the
+// level-(level + 2) blocks (K * R * R per trial, side mb2).  Same support as
+// expand2 (expand2_supported); cudaErrorNotSupported otherwise.
+cudaError_t launch_contract2_plan(int dtype, int formula, const void* ch, int64_t K, int64_t mb2,
+                                  void* out, const PlanLevel* plans, int64_t plan_tstride,
+                                  int level, int64_t ntr, uint8_t* nonfinite, cudaStream_t st);
 cudaError_t launch_contract_plan(int dtype, int formula, const void* ch, int64_t K, int64_t mb,
                                  void* out, const PlanLevel* plans, int64_t plan_tstride,
                                  int level, int64_t T, uint8_t* nonfinite, cudaStream_t st);

@@ -205,6 +205,85 @@ __global__ void __launch_bounds__(kThreads) contract_plan_kernel(
   }
 }
 
+// Two contraction levels (q+1, q) in one pass, the mirror of
+// expand2_plan_kernel: a thread owns one position of the level-(q+2) product
+// blocks under one level-q parent.  For each level-(q+1) block r1 (ascending)
+// it loads the R grandchildren at its position, contracts them with the
+// network (contract_w: the level-(q+1) value at the n*n sub-positions, base
+// coordinates), applies the level-(q+1) plan's sign, and folds that value into
+// the level-q accumulators of those sub-positions with contract_w_step (the
+// reference's r-ascending fold, _engine.py:104-112, streamed over r1).  The
+// level-(q+1) array never goes through HBM; values equal two
+// contract_plan_kernel launches.
+template <class F, class T, int W, bool SYNC>
+__global__ void __launch_bounds__(kThreads) contract2_plan_kernel(
+    const T* __restrict__ ch, int K, int mb2, T* __restrict__ out,
+    const PlanLevel* __restrict__ plans, int64_t plan_tstride, int level, int64_t ntr,
+    uint8_t* __restrict__ nonfinite) {
+  constexpr int n = F::n;
+  constexpr int R = F::R;
+  constexpr int NN = n * n;
+  const int mb1 = n * mb2, s = n * mb1;
+  const int P = (mb2 * mb2) / W;
+  const int64_t items = (int64_t)K * P;
+  int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const bool live = e < items;
+  if (!SYNC && !live) return;
+  if (!live) e = items - 1;  // SYNC: idle lanes mirror the last item, stores masked
+  const int Kp = (int)(e / P);
+  const int p = (int)(e - (int64_t)Kp * P);
+  const int pos = p * W;
+  const int i = pos / mb2;
+  const int j = pos - i * mb2;
+  const int64_t blk2 = (int64_t)mb2 * mb2;
+  using O = PackOps<T, W>;
+  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
+    const PlanLevel& p0 = plans[t * plan_tstride + level];
+    const PlanLevel& p1 = plans[t * plan_tstride + level + 1];
+    // level-(q+1) base sub-block q1 = (I1, J1) sits at hatted (inv0, inv2), signed
+    uint32_t m1[NN];
+#pragma unroll
+    for (int I = 0; I < n; ++I)
+#pragma unroll
+      for (int J = 0; J < n; ++J)
+        m1[I * n + J] = sign_mask(p1.neg[0][p1.inv[0][I]] ^ p1.neg[2][p1.inv[2][J]]);
+    const T* cb = ch + (t * K + Kp) * (int64_t)R * R * blk2 + pos;
+    Pack<T, W> acc[NN][NN];  // [level-(q+1) sub-position q1][level-q base block]
+#pragma unroll
+    for (int r1 = 0; r1 < R; ++r1) {
+      Pack<T, W> pr[R];
+#pragma unroll
+      for (int r2 = 0; r2 < R; ++r2) pr[r2] = pload<T, W>(cb + (int64_t)(r1 * R + r2) * blk2);
+      Pack<T, W> o1[NN];
+      F::template contract_w<T, W>(pr, o1);
+#pragma unroll
+      for (int q = 0; q < NN; ++q) F::template contract_w_step<T, W>(acc[q], O::flip(o1[q], m1[q]), r1);
+      // SYNC: the CTA reads the grandchildren of r1 together (read locality of
+      // small blocks, as in expand2_plan_kernel)
+      if (SYNC) __syncthreads();
+    }
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < NN; ++q) {
+      F::template contract_w_finish<T, W>(acc[q]);
+      const int hi1 = p1.inv[0][q / n], hj1 = p1.inv[2][q % n];
+      T* ob = out + (t * K + Kp) * (int64_t)s * s + (int64_t)(hi1 * mb2 + i) * s + hj1 * mb2 + j;
+#pragma unroll
+      for (int I = 0; I < n; ++I) {
+        const int hi = p0.inv[0][I];
+#pragma unroll
+        for (int J = 0; J < n; ++J) {
+          const int hj = p0.inv[2][J];
+          const Pack<T, W> val = O::flip(acc[q][I * n + J], sign_mask(p0.neg[0][hi] ^ p0.neg[2][hj]));
+          if (nonfinite) ok = ok && O::all_finite(val);
+          if (live) pstore<T, W>(ob + (int64_t)hi * mb1 * s + hj * mb1, val);
+        }
+      }
+    }
+    if (nonfinite && live && !ok) nonfinite[t] = 1;
+  }
+}
+
 inline dim3 grid_for(int64_t items, int64_t ntr) {
   const int64_t bx = (items + kThreads - 1) / kThreads;
   return dim3((unsigned)bx, (unsigned)(ntr < 65535 ? ntr : 65535), 1);
@@ -304,6 +383,61 @@ cudaError_t contract_plan_w(const void* ch, int64_t K, int64_t mb, void* out,
   contract_plan_kernel<F, T, W><<<grid, kThreads, 0, st>>>(
       (const T*)ch, (int)K, (int)mb, (T*)out, plans, pts, level, ntr, nonfinite);
   return cudaGetLastError();
+}
+
+template <class F, class T, int W>
+cudaError_t contract2_plan_w(const void* ch, int64_t K, int64_t mb2, void* out,
+                             const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
+                             uint8_t* nonfinite, cudaStream_t st) {
+  const dim3 grid = grid_for(K * (mb2 * mb2 / W), ntr);
+  // lockstep for small blocks, as in expand2_plan_w (RBC_EXPAND2_SYNC forces)
+  static const int forced = [] {
+    const char* v = getenv("RBC_EXPAND2_SYNC");
+    return v ? atoi(v) : -1;
+  }();
+  const bool sync = forced >= 0 ? forced != 0 : mb2 * mb2 * (int64_t)sizeof(T) < (64 << 10);
+  // (n = 2 formulas read R^2 = 49 blocks per thread: no lockstep variant,
+  // its unrolled barrier loop costs 255 registers)
+  if constexpr (F::R > 8) {
+    if (sync) {
+      contract2_plan_kernel<F, T, W, true><<<grid, kThreads, 0, st>>>(
+          (const T*)ch, (int)K, (int)mb2, (T*)out, plans, pts, level, ntr, nonfinite);
+      return cudaGetLastError();
+    }
+  }
+    contract2_plan_kernel<F, T, W, false><<<grid, kThreads, 0, st>>>(
+        (const T*)ch, (int)K, (int)mb2, (T*)out, plans, pts, level, ntr, nonfinite);
+  return cudaGetLastError();
+}
+
+template <class F, class T>
+cudaError_t contract2_plan_t(int dtype, const void* ch, int64_t K, int64_t mb2, void* out,
+                             const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
+                             uint8_t* nonfinite, cudaStream_t st) {
+  constexpr int cap = expand2_max_width<F, T>();  // n^4 live accumulator packs, as expand2
+  if constexpr (cap == 0) {
+    return cudaErrorNotSupported;
+  } else {
+    const int W = pick_width(dtype, mb2, cap);
+    switch (W) {
+      case 4: return contract2_plan_w<F, T, (cap >= 4 ? 4 : 1)>(ch, K, mb2, out, plans, pts, level, ntr, nonfinite, st);
+      case 2: return contract2_plan_w<F, T, (cap >= 2 ? 2 : 1)>(ch, K, mb2, out, plans, pts, level, ntr, nonfinite, st);
+      default: return contract2_plan_w<F, T, 1>(ch, K, mb2, out, plans, pts, level, ntr, nonfinite, st);
+    }
+  }
+}
+
+template <class T>
+cudaError_t contract2_plan_f(int dtype, int formula, const void* ch, int64_t K, int64_t mb2,
+                             void* out, const PlanLevel* plans, int64_t pts, int level,
+                             int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
+  switch (formula) {
+    case FStrassen::kId: return contract2_plan_t<FStrassen, T>(dtype, ch, K, mb2, out, plans, pts, level, ntr, nonfinite, st);
+    case FLaderman::kId: return contract2_plan_t<FLaderman, T>(dtype, ch, K, mb2, out, plans, pts, level, ntr, nonfinite, st);
+    case FStandard2::kId: return contract2_plan_t<FStandard2, T>(dtype, ch, K, mb2, out, plans, pts, level, ntr, nonfinite, st);
+    case FStandard3::kId: return contract2_plan_t<FStandard3, T>(dtype, ch, K, mb2, out, plans, pts, level, ntr, nonfinite, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 // Width dispatch.  Large-R formulas (Laderman: 23 live packs) cap the width
@@ -424,6 +558,17 @@ bool expand2_supported(int dtype, int formula) {
     case FStandard3::kId: return ok(FStandard3{});
   }
   return false;
+}
+
+cudaError_t launch_contract2_plan(int dtype, int formula, const void* ch, int64_t K, int64_t mb2,
+                                  void* out, const PlanLevel* plans, int64_t plan_tstride,
+                                  int level, int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
+  switch (dtype) {
+    case kF64: return contract2_plan_f<double>(dtype, formula, ch, K, mb2, out, plans, plan_tstride, level, ntr, nonfinite, st);
+    case kF32: return contract2_plan_f<float>(dtype, formula, ch, K, mb2, out, plans, plan_tstride, level, ntr, nonfinite, st);
+    case kF16: return contract2_plan_f<__half>(dtype, formula, ch, K, mb2, out, plans, plan_tstride, level, ntr, nonfinite, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_contract_plan(int dtype, int formula, const void* ch, int64_t K, int64_t mb,

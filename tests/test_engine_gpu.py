@@ -152,15 +152,19 @@ def test_fused_subtree_vs_breadth_first_and_oracle(eng, monkeypatch, label, fnam
     "label,fname,Q,N,T,T0",
     [
         ("f32", "laderman", 3, 243, 2, 2),   # expand2 (levels 0-1) then the fused subtree
+        ("f32", "laderman", 4, 243, 2, 2),   # config 2's schedule at two trials
         ("f32", "strassen", 5, 512, 2, 1),   # expand2 twice, then one single level
         ("f16", "strassen", 4, 256, 2, 2),
         ("f64", "strassen", 3, 96, 3, 1),
         ("f64", "laderman", 3, 81, 2, 2),    # no binary64 n=3 instantiation: single levels
     ],
 )
-def test_two_level_expansion_vs_single_levels(eng, monkeypatch, label, fname, Q, N, T, T0):
-    """expand2_plan_kernel (two expansion levels per pass) equals the
-    one-level-per-pass schedule and the oracle."""
+@pytest.mark.parametrize("fusion", ["1", "0"])
+def test_two_level_expansion_vs_single_levels(eng, monkeypatch, label, fname, Q, N, T, T0, fusion):
+    """expand2_plan_kernel / contract2_plan_kernel (two expansion and two
+    contraction levels per pass) equal the one-level-per-pass schedule and the
+    oracle, with and without the fused bottom subtree (the contraction pairs
+    then start at different levels)."""
     import paper_1905_07439_b200 as rbc
     from paper_1905_07439_b200.randomize import pack_recursive_plans, plan_formula_id
 
@@ -172,7 +176,8 @@ def test_two_level_expansion_vs_single_levels(eng, monkeypatch, label, fname, Q,
     rplans = [rbc.draw_recursive_plan(f.n, Q, rbc.derive_rng(94, t)) for t in range(T)]
     packed = pack_recursive_plans(rplans, Q, f.n)
     fid = plan_formula_id(f)
-    monkeypatch.setenv("RBC_NO_FUSION", "1")
+    if fusion == "0":
+        monkeypatch.setenv("RBC_NO_FUSION", "1")
     two = eng.apply_plans(fid, Q, packed, a, b, mode)
     monkeypatch.setenv("RBC_NO_EXPAND2", "1")
     one = eng.apply_plans(fid, Q, packed, a, b, mode)
