@@ -790,9 +790,9 @@ static cudaStream_t make_stream() {
   return x;
 }
 
-static cudaStream_t host_stream() {
-  static cudaStream_t s = make_stream();
-  return s;
+static cudaStream_t host_stream(int i = 0) {
+  static cudaStream_t s[2] = {make_stream(), make_stream()};
+  return s[i];
 }
 
 static cudaStream_t copy_stream() {
@@ -801,15 +801,17 @@ static cudaStream_t copy_stream() {
 }
 
 static cudaEvent_t pipe_event(int i) {
-  static cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  static cudaEvent_t ev[16] = {nullptr};
   if (!ev[i]) cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
   return ev[i];
 }
 
 // Host-buffer error trials, pipelined: trials are cut into chunks; chunk k+1
-// is copied host->device on a copy stream (into the other of two input
-// slots) while chunk k is computed on the compute stream.  With pinned host
-// buffers the PCIe transfer hides behind the kernels.
+// is copied host->device on a copy stream (into a ring of three input slots)
+// while chunks k and k-1 compute on two alternating compute streams with
+// their own workspaces, so the small per-chunk grids of consecutive chunks
+// share the GPU.  With pinned host buffers the PCIe transfer hides behind the
+// kernels.
 int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
                      const void* b, const void* rand_plans, int with_det, double* err_rand,
                      double* err_det, uint8_t* nf_rand, uint8_t* nf_det) {
@@ -833,8 +835,9 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   const size_t db = (size_t)Q * RBC_PLAN_BYTES;
   std::lock_guard<std::mutex> lock(arena().mu);
   // chunk size: ~8 chunks, shrunk until two input slots + workspace fit
-  // pipeline chunks: about 16 MB of operands per chunk, at most 32 (measured
-  // on config 2: 4 chunks 18.0 ms, 8: 17.0, 16: 16.8, 32: 16.4 ms per call);
+  // pipeline chunks: about 8 MB of operands per chunk, at most 16 (config 2
+  // with two compute streams: 12 chunks 11.21 ms per call, 16: 11.20, 32:
+  // 11.4 -- the PCIe copies, 472 MB at 44-52 GB/s, are the critical path);
   // RBC_E2E_CHUNKS overrides
   static const int forced_chunks = [] {
     const char* v = getenv("RBC_E2E_CHUNKS");
@@ -842,14 +845,24 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   }();
   int64_t nchunks = forced_chunks > 0
                         ? forced_chunks
-                        : std::min<int64_t>(32, std::max<int64_t>(
+                        : std::min<int64_t>(16, std::max<int64_t>(
                                                     1, (int64_t)(2 * T * N2 * es >> 23)));
   int64_t C = std::max<int64_t>(1, (T + nchunks - 1) / nchunks);
   if (C > 8) C = (C + 7) / 8 * 8;  // whole multiples of 8 trials keep grids regular
+  // Two compute streams pay off for many small chunks (config 2: 1000 pairs
+  // of 243); products of 512 and up are whole-GPU jobs per chunk, and their
+  // truth scratch comes from the stream-ordered pool, which two streams
+  // fragment (config 4 calls went from 24 to 24-80 ms): one stream there.
+  static const int forced_streams = [] {  // RBC_E2E_STREAMS=1/2 (tuning aid)
+    const char* v = getenv("RBC_E2E_STREAMS");
+    return v ? atoi(v) : 0;
+  }();
+  const bool two = forced_streams ? forced_streams == 2 : N < 512;
+  constexpr int kSlots = 3;  // input slots: one being copied, two computing
   auto need = [&](int64_t c) {
     const size_t slot = 2 * align_up(c * N2 * es) + align_up(c * Q * RBC_PLAN_BYTES);
-    return 2 * slot + align_up(db) + 2 * align_up(T * 8) + 2 * align_up(T) + 4096 +
-           rbc_error_trials_workspace_bytes(dtype, formula, Q, c, N);
+    return kSlots * slot + align_up(db) + 2 * align_up(T * 8) + 2 * align_up(T) + 4096 +
+           (two ? 2 : 1) * align_up(rbc_error_trials_workspace_bytes(dtype, formula, Q, c, N));
   };
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -858,10 +871,10 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   if (need(C) > budget) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
   RBC_TRY(arena().reserve(need(C) + 256));
   Arena& A = arena();
-  void* da[2];
-  void* dbb[2];
-  void* dpl[2];
-  for (int k = 0; k < 2; ++k) {
+  void* da[kSlots];
+  void* dbb[kSlots];
+  void* dpl[kSlots];
+  for (int k = 0; k < kSlots; ++k) {
     da[k] = A.take(C * N2 * es);
     dbb[k] = A.take(C * N2 * es);
     dpl[k] = A.take(C * Q * RBC_PLAN_BYTES);
@@ -872,8 +885,9 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   uint8_t* dnf_r = (uint8_t*)A.take(T);
   uint8_t* dnf_d = (uint8_t*)A.take(T);
   const size_t ws = rbc_error_trials_workspace_bytes(dtype, formula, Q, C, N);
-  void* dws = A.take(ws);
-  cudaStream_t sc = host_stream();
+  void* dws[2] = {A.take(ws), two ? A.take(ws) : nullptr};
+  cudaStream_t scs[2] = {host_stream(0), host_stream(1)};
+  cudaStream_t sc = scs[0];
   cudaStream_t sx = copy_stream();
   std::vector<PlanLevel> ident(Q);
   for (int q = 0; q < Q; ++q) {
@@ -882,12 +896,42 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
       for (int j = 0; j < n; ++j) ident[q].perm[i][j] = ident[q].inv[i][j] = (int8_t)j;
   }
   CUDA_TRY(cudaMemcpyAsync(ddet, ident.data(), db, cudaMemcpyHostToDevice, sc));
+  CUDA_TRY(cudaEventRecord(pipe_event(15), sc));
+  CUDA_TRY(cudaStreamWaitEvent(scs[1], pipe_event(15), 0));
+  static const bool trace = [] {
+    const char* v = getenv("RBC_E2E_TRACE");
+    return v && v[0] == '1';
+  }();
+  cudaEvent_t tr0 = nullptr;
+  std::vector<cudaEvent_t> tr_copy, tr_comp;
+  if (trace) {
+    cudaEventCreate(&tr0);
+    cudaEventRecord(tr0, sx);
+  }
   int64_t k = 0;
-  for (int64_t t0 = 0; t0 < T; t0 += C, ++k) {
-    const int64_t nt = std::min(C, T - t0);
-    const int slot = (int)(k & 1);
-    cudaEvent_t copied = pipe_event(slot), computed = pipe_event(2 + slot);
-    if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(sx, computed, 0));  // slot free again
+  // Chunk sizes: C, ..., C, then the remainder cut in halves (multiples of
+  // 8): the copies are the critical path (PCIe), so after the last copy only
+  // a small chunk is left to compute.
+  std::vector<int64_t> sizes;
+  {
+    int64_t rem = T;
+    while (rem > C) {
+      sizes.push_back(C);
+      rem -= C;
+    }
+    while (rem > 8) {
+      const int64_t c = ((rem + 1) / 2 + 7) / 8 * 8;
+      sizes.push_back(std::min(c, rem));
+      rem -= std::min(c, rem);
+    }
+    if (rem > 0) sizes.push_back(rem);
+  }
+  for (int64_t t0 = 0; k < (int64_t)sizes.size(); t0 += sizes[k], ++k) {
+    const int64_t nt = sizes[k];
+    const int slot = (int)(k % kSlots);
+    cudaStream_t sk = scs[two ? (k & 1) : 0];
+    cudaEvent_t copied = pipe_event(slot), computed = pipe_event(kSlots + slot);
+    if (k >= kSlots) CUDA_TRY(cudaStreamWaitEvent(sx, computed, 0));  // slot free again
     CUDA_TRY(cudaMemcpyAsync(da[slot], (const char*)a + t0 * N2 * es, nt * N2 * es,
                              cudaMemcpyHostToDevice, sx));
     CUDA_TRY(cudaMemcpyAsync(dbb[slot], (const char*)b + t0 * N2 * es, nt * N2 * es,
@@ -896,11 +940,36 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
       CUDA_TRY(cudaMemcpyAsync(dpl[slot], (const char*)rand_plans + t0 * Q * RBC_PLAN_BYTES,
                                nt * Q * RBC_PLAN_BYTES, cudaMemcpyHostToDevice, sx));
     CUDA_TRY(cudaEventRecord(copied, sx));
-    CUDA_TRY(cudaStreamWaitEvent(sc, copied, 0));
+    if (trace) {
+      tr_copy.emplace_back();
+      cudaEventCreate(&tr_copy.back());
+      cudaEventRecord(tr_copy.back(), sx);
+    }
+    CUDA_TRY(cudaStreamWaitEvent(sk, copied, 0));
     RBC_TRY(rbc_error_trials_async(dtype, formula, Q, nt, N, da[slot], dbb[slot],
                                    rand_plans ? dpl[slot] : nullptr, with_det ? ddet : nullptr,
-                                   derr_r + t0, derr_d + t0, dnf_r + t0, dnf_d + t0, dws, ws, sc));
-    CUDA_TRY(cudaEventRecord(computed, sc));
+                                   derr_r + t0, derr_d + t0, dnf_r + t0, dnf_d + t0,
+                                   dws[two ? (k & 1) : 0], ws, sk));
+    CUDA_TRY(cudaEventRecord(computed, sk));
+    if (trace) {
+      tr_comp.emplace_back();
+      cudaEventCreate(&tr_comp.back());
+      cudaEventRecord(tr_comp.back(), sk);
+    }
+  }
+  CUDA_TRY(cudaEventRecord(pipe_event(15), scs[1]));
+  CUDA_TRY(cudaStreamWaitEvent(sc, pipe_event(15), 0));
+  if (trace) {  // RBC_E2E_TRACE=1: per-chunk copy / compute completion times
+    CUDA_TRY(cudaStreamSynchronize(sc));
+    for (size_t i = 0; i < tr_copy.size(); ++i) {
+      float c = 0.f, g = 0.f;
+      cudaEventElapsedTime(&c, tr0, tr_copy[i]);
+      cudaEventElapsedTime(&g, tr0, tr_comp[i]);
+      fprintf(stderr, "e2e chunk %zu: copied %.3f ms, computed %.3f ms\n", i, c, g);
+      cudaEventDestroy(tr_copy[i]);
+      cudaEventDestroy(tr_comp[i]);
+    }
+    cudaEventDestroy(tr0);
   }
   if (rand_plans) {
     CUDA_TRY(cudaMemcpyAsync(err_rand, derr_r, T * 8, cudaMemcpyDeviceToHost, sc));

@@ -1284,7 +1284,8 @@ cudaError_t launch_subtree_lane_v(const void* x, const void* y, int64_t xy_tstri
 // double-buffered X1/Y1, stage C(k) sharing a phase with stage A(k+1), two
 // barriers per step: 3.01 -- barriers are not what bounds the kernel;
 // SUB 2 + STAGE 2: 3.64, five CTAs per SM no longer fit),
-// RBC_SUBTREE_CHUNK subtrees per CTA (24; 8: 3.44, 48: 3.46).
+// RBC_SUBTREE_CHUNK subtrees per CTA (default about 24, balanced; 8: 3.44,
+// 48: 3.46).
 template <class F, class T, int M>
 cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
                                void* out, const PlanLevel* plans, int64_t pts, int q0,
@@ -1305,7 +1306,13 @@ cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride,
     const char* v = getenv("RBC_SUBTREE_STAGE");
     return v ? atoi(v) : 1;
   }();
-  const int kchunk = kc > 0 ? kc : 24;
+  // about 24 subtrees per CTA, balanced so no CTA gets a short tail chunk
+  // (config 2: 529 blocks -> 23 x 23 instead of 22 x 24 + 1: 3.02 -> 2.98 ms)
+  int kchunk = kc;
+  if (kchunk <= 0) {
+    const int64_t nchunks = (K0 + 23) / 24;
+    kchunk = (int)((K0 + nchunks - 1) / nchunks);
+  }
   static const int lane = [] {
     const char* v = getenv("RBC_SUBTREE_LANE");
     return v ? atoi(v) : 0;

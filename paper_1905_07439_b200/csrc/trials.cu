@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/rbc.h"
@@ -62,26 +63,36 @@ struct AuxStreams {
   cudaEvent_t fork, join[3], truth_done, lane_done[2];
 };
 
-AuxStreams* aux_streams() {
-  static AuxStreams* per_dev[64] = {nullptr};
+// One lane set per (device, caller stream): two passes issued on different
+// caller streams (the host-buffer pipeline's two compute streams) must not
+// queue behind each other on shared lanes.
+AuxStreams* aux_streams(cudaStream_t caller) {
+  struct Entry {
+    int dev;
+    cudaStream_t caller;
+    AuxStreams* ax;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> sets;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!per_dev[dev]) {
-    AuxStreams* a = new AuxStreams;
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    for (int i = 0; i < 3; ++i) {
-      // the truth lane (FP64 pipe) gets the highest priority so its CTAs
-      // interleave with the shared-memory-bound product kernels
-      cudaStreamCreateWithPriority(&a->s[i], cudaStreamNonBlocking, i == 0 ? hi : lo);
-      cudaEventCreateWithFlags(&a->join[i], cudaEventDisableTiming);
-    }
-    cudaEventCreateWithFlags(&a->fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&a->truth_done, cudaEventDisableTiming);
-    for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&a->lane_done[i], cudaEventDisableTiming);
-    per_dev[dev] = a;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Entry& e : sets)
+    if (e.dev == dev && e.caller == caller) return e.ax;
+  AuxStreams* a = new AuxStreams;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  for (int i = 0; i < 3; ++i) {
+    // the truth lane (FP64 pipe) gets the highest priority so its CTAs
+    // interleave with the shared-memory-bound product kernels
+    cudaStreamCreateWithPriority(&a->s[i], cudaStreamNonBlocking, i == 0 ? hi : lo);
+    cudaEventCreateWithFlags(&a->join[i], cudaEventDisableTiming);
   }
-  return per_dev[dev];
+  cudaEventCreateWithFlags(&a->fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&a->truth_done, cudaEventDisableTiming);
+  for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&a->lane_done[i], cudaEventDisableTiming);
+  sets.push_back({dev, caller, a});
+  return a;
 }
 
 }  // namespace
@@ -200,7 +211,7 @@ int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, 
     return v && v[0] == '1';
   }();
   const bool conc = !prof_on() && !serial_env;
-  AuxStreams* ax = aux_streams();
+  AuxStreams* ax = aux_streams(st);
   cudaStream_t lanes[3] = {st, st, st};
   if (conc) {
     for (int i = 0; i < 3; ++i) lanes[i] = ax->s[i];

@@ -8,4 +8,5 @@ for c in c1 c3 c4 c5; do timeout 900 python bench.py --config $c > gpurun_out/be
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_c2.json 2> gpurun_out/bench_ref_c2.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:subtree -s 2 -c 1 -o gpurun_out/subtree_c2 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:contract2 -s 2 -c 1 -o gpurun_out/contract2_c2 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_full2.log 2>&1
 exit 0
