@@ -41,6 +41,7 @@ an all-gather of per-trial error statistics (a few KB, NCCL).
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -467,6 +468,24 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ ours ----
+@contextlib.contextmanager
+def no_gc():
+    """The host-buffer calls are timed by wall clock: a full collection of the
+    harness's own Python objects (plans, records) inside the timed loop is a
+    harness artefact (seen as 20-100 ms outliers), so collect first and pause
+    the collector while timing."""
+    import gc
+
+    gc.collect()
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        yield
+    finally:
+        if was:
+            gc.enable()
+
+
 class ErrorTrialWorkload:
     """c1, c2, c4, c5: 2 products per pair (plan path, packed plans)."""
 
@@ -518,12 +537,13 @@ class ErrorTrialWorkload:
         for _ in range(max(0, warmup - 1)):
             error_trials(*args, packed=pn)
         self.e2e_calls = []
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            t1 = time.perf_counter()
-            error_trials(*args, packed=pn)
-            self.e2e_calls.append((time.perf_counter() - t1) * 1e3)
-        ms = (time.perf_counter() - t0) / steps * 1e3
+        with no_gc():
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                t1 = time.perf_counter()
+                error_trials(*args, packed=pn)
+                self.e2e_calls.append((time.perf_counter() - t1) * 1e3)
+            ms = (time.perf_counter() - t0) / steps * 1e3
         h2d = self.A.nbytes + self.B.nbytes + self.packed.nbytes
         d2h = 2 * len(err_r) * 9
         return ms, h2d, d2h
@@ -579,10 +599,11 @@ class AverageWorkload:
             raise SystemExit("e2e errors differ from the device-resident run")
         for _ in range(max(0, warmup - 1)):
             average_trials(*args)
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            average_trials(*args)
-        ms = (time.perf_counter() - t0) / steps * 1e3
+        with no_gc():
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                average_trials(*args)
+            ms = (time.perf_counter() - t0) / steps * 1e3
         es = np.dtype(self.cfg.mode.dtype).itemsize
         h2d = self.A.nbytes + self.B.nbytes + sum(
             3 * len(self.rplans) * self.cfg.rank * self.cfg.n ** 2 * es for _ in range(self.cfg.Q))

@@ -795,9 +795,9 @@ static cudaStream_t host_stream(int i = 0) {
   return s[i];
 }
 
-static cudaStream_t copy_stream() {
-  static cudaStream_t s = make_stream();
-  return s;
+static cudaStream_t copy_stream(int i = 0) {
+  static cudaStream_t s[2] = {make_stream(), make_stream()};
+  return s[i];
 }
 
 static cudaEvent_t pipe_event(int i) {
@@ -888,7 +888,13 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   void* dws[2] = {A.take(ws), two ? A.take(ws) : nullptr};
   cudaStream_t scs[2] = {host_stream(0), host_stream(1)};
   cudaStream_t sc = scs[0];
-  cudaStream_t sx = copy_stream();
+  cudaStream_t sx = copy_stream(0);
+  // RBC_E2E_COPY_STREAMS=2: B (and plans) on a second copy stream (tuning aid)
+  static const bool two_copy = [] {
+    const char* v = getenv("RBC_E2E_COPY_STREAMS");
+    return v && atoi(v) == 2;
+  }();
+  cudaStream_t sx2 = two_copy ? copy_stream(1) : sx;
   std::vector<PlanLevel> ident(Q);
   for (int q = 0; q < Q; ++q) {
     memset(&ident[q], 0, sizeof(PlanLevel));
@@ -931,14 +937,21 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
     const int slot = (int)(k % kSlots);
     cudaStream_t sk = scs[two ? (k & 1) : 0];
     cudaEvent_t copied = pipe_event(slot), computed = pipe_event(kSlots + slot);
-    if (k >= kSlots) CUDA_TRY(cudaStreamWaitEvent(sx, computed, 0));  // slot free again
+    if (k >= kSlots) {  // slot free again
+      CUDA_TRY(cudaStreamWaitEvent(sx, computed, 0));
+      if (two_copy) CUDA_TRY(cudaStreamWaitEvent(sx2, computed, 0));
+    }
     CUDA_TRY(cudaMemcpyAsync(da[slot], (const char*)a + t0 * N2 * es, nt * N2 * es,
                              cudaMemcpyHostToDevice, sx));
     CUDA_TRY(cudaMemcpyAsync(dbb[slot], (const char*)b + t0 * N2 * es, nt * N2 * es,
-                             cudaMemcpyHostToDevice, sx));
+                             cudaMemcpyHostToDevice, sx2));
     if (rand_plans)
       CUDA_TRY(cudaMemcpyAsync(dpl[slot], (const char*)rand_plans + t0 * Q * RBC_PLAN_BYTES,
-                               nt * Q * RBC_PLAN_BYTES, cudaMemcpyHostToDevice, sx));
+                               nt * Q * RBC_PLAN_BYTES, cudaMemcpyHostToDevice, sx2));
+    if (two_copy) {
+      CUDA_TRY(cudaEventRecord(pipe_event(14), sx2));
+      CUDA_TRY(cudaStreamWaitEvent(sx, pipe_event(14), 0));
+    }
     CUDA_TRY(cudaEventRecord(copied, sx));
     if (trace) {
       tr_copy.emplace_back();
