@@ -1278,7 +1278,9 @@ cudaError_t launch_subtree_lane_v(const void* x, const void* y, int64_t xy_tstri
 }
 
 // Tuning aids (config 2, ms per launch): RBC_SUBTREE_SUB subtrees per CTA
-// step (1: 3.28, 3: 3.82), RBC_SUBTREE_ROT=1 rotated 6-shuffle leaf (3.38),
+// step (1: 3.28, 3: 3.82), RBC_SUBTREE_ROT=1 rotated 6-shuffle leaf (3.38;
+// a shuffle-free leaf where every lane expands the whole Y fiber measured
+// 8.5: 3x the Y network adds and 255 registers),
 // RBC_SUBTREE_STAGE TMA bulk prefetch of the level-q0 blocks (default 1:
 // 3.01; 0: 3.28; per-element cp.async: 3.40; 2 = one staging buffer and
 // double-buffered X1/Y1, stage C(k) sharing a phase with stage A(k+1), two

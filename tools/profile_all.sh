@@ -14,6 +14,7 @@ cap() {  # name config kernel-regex skip   (summaries only: reports stay on the 
 }
 cap c2_subtree c2 subtree 2
 cap c2_expand2 c2 expand2 2
+cap c2_contract2 c2 contract2 2
 cap c2_truth c2 truth_tiled 1
 cap c5_truth c5 truth_bulk 1
 cap c5_leaf c5 leaf_f32v 1
