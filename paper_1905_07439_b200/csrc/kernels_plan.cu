@@ -29,6 +29,13 @@ namespace rbc {
 namespace {
 
 constexpr int kThreads = 256;
+// CTA size of the lockstep (SYNC) two-level kernels (compile-time tuning knob;
+// c2 expand2 at 128 threads: 0.415 vs 0.332 ms -- a bigger lockstep group
+// writes longer runs of each output block)
+#ifndef RBC_SYNC_THREADS
+#define RBC_SYNC_THREADS 256
+#endif
+constexpr int kSyncThreads = RBC_SYNC_THREADS;
 
 template <class F, class T, int W, int WHICH>
 __global__ void __launch_bounds__(kThreads) expand_plan_kernel(
@@ -86,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) expand_plan_kernel(
 // Values equal two expand_plan_kernel launches; the level-(q+1) array never
 // goes through HBM.
 template <class F, class T, int W, int WHICH, bool SYNC>
-__global__ void __launch_bounds__(kThreads) expand2_plan_kernel(
+__global__ void __launch_bounds__(SYNC ? kSyncThreads : kThreads) expand2_plan_kernel(
     const T* __restrict__ x, int64_t x_tstride, int K, int s, T* __restrict__ out,
     const PlanLevel* __restrict__ plans, int64_t plan_tstride, int level, int64_t ntr) {
   constexpr int n = F::n;
@@ -95,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) expand2_plan_kernel(
   const int mb1 = s / n, mb2 = mb1 / n;
   const int P = (mb2 * mb2) / W;
   const int64_t items = (int64_t)K * P;
-  int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  int64_t e = (int64_t)blockIdx.x * (SYNC ? kSyncThreads : kThreads) + threadIdx.x;
   const bool live = e < items;
   if (!SYNC && !live) return;
   if (!live) e = items - 1;  // SYNC: idle lanes mirror the last item, stores masked
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) contract_plan_kernel(
 // level-(q+1) array never goes through HBM; values equal two
 // contract_plan_kernel launches.
 template <class F, class T, int W, bool SYNC>
-__global__ void __launch_bounds__(kThreads) contract2_plan_kernel(
+__global__ void __launch_bounds__(SYNC ? kSyncThreads : kThreads) contract2_plan_kernel(
     const T* __restrict__ ch, int K, int mb2, T* __restrict__ out,
     const PlanLevel* __restrict__ plans, int64_t plan_tstride, int level, int64_t ntr,
     uint8_t* __restrict__ nonfinite) {
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(kThreads) contract2_plan_kernel(
   const int mb1 = n * mb2, s = n * mb1;
   const int P = (mb2 * mb2) / W;
   const int64_t items = (int64_t)K * P;
-  int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  int64_t e = (int64_t)blockIdx.x * (SYNC ? kSyncThreads : kThreads) + threadIdx.x;
   const bool live = e < items;
   if (!SYNC && !live) return;
   if (!live) e = items - 1;  // SYNC: idle lanes mirror the last item, stores masked
@@ -284,8 +291,8 @@ __global__ void __launch_bounds__(kThreads) contract2_plan_kernel(
   }
 }
 
-inline dim3 grid_for(int64_t items, int64_t ntr) {
-  const int64_t bx = (items + kThreads - 1) / kThreads;
+inline dim3 grid_for(int64_t items, int64_t ntr, int nt = kThreads) {
+  const int64_t bx = (items + nt - 1) / nt;
   return dim3((unsigned)bx, (unsigned)(ntr < 65535 ? ntr : 65535), 1);
 }
 
@@ -321,14 +328,15 @@ cudaError_t expand2_plan_w(int which, const void* x, int64_t xs, int64_t K, int6
     return v ? atoi(v) : -1;
   }();
   const bool sync = forced >= 0 ? forced != 0 : mb2 * mb2 * (int64_t)sizeof(T) < (64 << 10);
+  const dim3 gs = grid_for(K * (mb2 * mb2 / W), ntr, kSyncThreads);
   if (which == 0 && sync)
-    expand2_plan_kernel<F, T, W, 0, true><<<grid, kThreads, 0, st>>>(
+    expand2_plan_kernel<F, T, W, 0, true><<<gs, kSyncThreads, 0, st>>>(
         (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
   else if (which == 0)
     expand2_plan_kernel<F, T, W, 0, false><<<grid, kThreads, 0, st>>>(
         (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
   else if (sync)
-    expand2_plan_kernel<F, T, W, 1, true><<<grid, kThreads, 0, st>>>(
+    expand2_plan_kernel<F, T, W, 1, true><<<gs, kSyncThreads, 0, st>>>(
         (const T*)x, xs, (int)K, (int)s, (T*)out, plans, pts, level, ntr);
   else
     expand2_plan_kernel<F, T, W, 1, false><<<grid, kThreads, 0, st>>>(
@@ -396,11 +404,12 @@ cudaError_t contract2_plan_w(const void* ch, int64_t K, int64_t mb2, void* out,
     return v ? atoi(v) : -1;
   }();
   const bool sync = forced >= 0 ? forced != 0 : mb2 * mb2 * (int64_t)sizeof(T) < (64 << 10);
+  const dim3 gs = grid_for(K * (mb2 * mb2 / W), ntr, kSyncThreads);
   // (n = 2 formulas read R^2 = 49 blocks per thread: no lockstep variant,
   // its unrolled barrier loop costs 255 registers)
   if constexpr (F::R > 8) {
     if (sync) {
-      contract2_plan_kernel<F, T, W, true><<<grid, kThreads, 0, st>>>(
+      contract2_plan_kernel<F, T, W, true><<<gs, kSyncThreads, 0, st>>>(
           (const T*)ch, (int)K, (int)mb2, (T*)out, plans, pts, level, ntr, nonfinite);
       return cudaGetLastError();
     }
