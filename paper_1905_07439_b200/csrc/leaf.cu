@@ -507,7 +507,12 @@ struct SmemBulk {
   static constexpr int TPL = (M / TM) * (M / TN);
   static constexpr int LPB = 256 / TPL;
   static constexpr int E = M * M;
-  static constexpr int SPAN = ((E * (int)sizeof(T) + 16) + 15) / 16 * 16;  // bytes per operand slot
+  static constexpr int SPAN0 = ((E * (int)sizeof(T) + 16) + 15) / 16 * 16;
+  // bytes per operand slot, padded to 4 (mod 16) words for binary64: the
+  // same operand of consecutive leaves then sits 8 banks apart, so a warp
+  // that straddles two leaves reads their A rows without bank conflicts
+  static constexpr int SPAN =
+      sizeof(T) == 8 ? SPAN0 + ((4 - (SPAN0 / 4) % 16 + 16) % 16) * 4 : SPAN0;
   static constexpr size_t stage_bytes = (size_t)LPB * 2 * SPAN;
   static constexpr size_t smem = 2 * stage_bytes + 2 * sizeof(uint64_t);
 };
