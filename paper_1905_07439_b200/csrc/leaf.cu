@@ -288,34 +288,47 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
   const TIn* xb = x + b * xs;
   const TIn* yb = y + b * ys;
 
+  // Per-thread load geometry, fixed across k tiles (NT divides BK * BN and
+  // BM * BK): A element (m0 + a_m + q * AR, k0 + a_k), B element
+  // (k0 + b_k + q * BR, n0 + b_n).  Interior k tiles skip the K checks, rows
+  // and columns past M / N are masked once per thread.
+  static_assert(NT % BK == 0 && NT % BN == 0, "load geometry");
+  constexpr int AR = NT / BK, BR = NT / BN;
+  static_assert(A_PER <= 32, "row mask");
+  const int a_k = tid % BK, a_m = tid / BK;
+  const int b_n = tid % BN, b_k = tid / BN;
+  const TIn* pa = xb + (int64_t)(m0 + a_m) * K + a_k;
+  const TIn* pb = yb + (int64_t)b_k * N + n0 + b_n;
+  const int64_t sa = (int64_t)AR * K, sb = (int64_t)BR * N;
+  uint32_t a_rows = 0;
+#pragma unroll
+  for (int q = 0; q < A_PER; ++q) a_rows |= (m0 + a_m + q * AR < M ? 1u : 0u) << q;
+  const bool b_col = n0 + b_n < N;
   TIn ra[A_PER], rb[B_PER];
   auto load_tile = [&](int k0) {
+    const TIn* p = pa + k0;
+    const TIn* r = pb + (int64_t)k0 * N;
+    if (k0 + BK <= K) {
 #pragma unroll
-    for (int q = 0; q < A_PER; ++q) {
-      const int e = tid + q * NT;
-      const int mm = e / BK, kk = e % BK;
-      const int gm = m0 + mm, gk = k0 + kk;
-      ra[q] = (gm < M && gk < K) ? xb[(int64_t)gm * K + gk] : TIn(0.0f);
-    }
+      for (int q = 0; q < A_PER; ++q) ra[q] = ((a_rows >> q) & 1) ? p[q * sa] : TIn(0.0f);
 #pragma unroll
-    for (int q = 0; q < B_PER; ++q) {
-      const int e = tid + q * NT;
-      const int kk = e / BN, nn = e % BN;
-      const int gk = k0 + kk, gn = n0 + nn;
-      rb[q] = (gk < K && gn < N) ? yb[(int64_t)gk * N + gn] : TIn(0.0f);
+      for (int q = 0; q < B_PER; ++q) rb[q] = b_col ? r[q * sb] : TIn(0.0f);
+    } else {
+      const bool ak = k0 + a_k < K;
+#pragma unroll
+      for (int q = 0; q < A_PER; ++q) ra[q] = (ak && ((a_rows >> q) & 1)) ? p[q * sa] : TIn(0.0f);
+#pragma unroll
+      for (int q = 0; q < B_PER; ++q)
+        rb[q] = (b_col && k0 + b_k + q * BR < K) ? r[q * sb] : TIn(0.0f);
     }
   };
   auto store_tile = [&](int buf) {
+    double* da = &As[buf][a_k][a_m];
+    double* db = &Bs[buf][b_k][b_n];
 #pragma unroll
-    for (int q = 0; q < A_PER; ++q) {
-      const int e = tid + q * NT;
-      As[buf][e % BK][e / BK] = widen_to<TIn, double>(ra[q]);
-    }
+    for (int q = 0; q < A_PER; ++q) da[q * AR] = widen_to<TIn, double>(ra[q]);
 #pragma unroll
-    for (int q = 0; q < B_PER; ++q) {
-      const int e = tid + q * NT;
-      Bs[buf][e / BN][e % BN] = widen_to<TIn, double>(rb[q]);
-    }
+    for (int q = 0; q < B_PER; ++q) db[q * BR * (BN + BPAD)] = widen_to<TIn, double>(rb[q]);
   };
 
   double acc[TM][TN];
