@@ -92,8 +92,13 @@ __global__ void __launch_bounds__(kThreads) expand_plan_kernel(
 // sign is applied to the child value), so every register index is static.
 // Values equal two expand_plan_kernel launches; the level-(q+1) array never
 // goes through HBM.
+// resident lockstep CTAs per SM the registers aim at (2: 128 registers,
+// 0.357 vs 0.332 ms on c2 -- more CTAs per SM interleave more output blocks)
+#ifndef RBC_EXPAND2_MINB
+#define RBC_EXPAND2_MINB 1
+#endif
 template <class F, class T, int W, int WHICH, bool SYNC>
-__global__ void __launch_bounds__(SYNC ? kSyncThreads : kThreads) expand2_plan_kernel(
+__global__ void __launch_bounds__(SYNC ? kSyncThreads : kThreads, SYNC ? RBC_EXPAND2_MINB : 1) expand2_plan_kernel(
     const T* __restrict__ x, int64_t x_tstride, int K, int s, T* __restrict__ out,
     const PlanLevel* __restrict__ plans, int64_t plan_tstride, int level, int64_t ntr) {
   constexpr int n = F::n;
