@@ -800,6 +800,8 @@ static cudaStream_t copy_stream(int i = 0) {
   return s[i];
 }
 
+constexpr int kMaxSlots = 7;  // pipe events: 2 per slot, plus 14 and 15
+
 static cudaEvent_t pipe_event(int i) {
   static cudaEvent_t ev[16] = {nullptr};
   if (!ev[i]) cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
@@ -858,7 +860,13 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
     return v ? atoi(v) : 0;
   }();
   const bool two = forced_streams ? forced_streams == 2 : N < 512;
-  constexpr int kSlots = 3;  // input slots: one being copied, two computing
+  // input slots: copies run ahead of the compute streams by kSlots - 2
+  // chunks (RBC_E2E_SLOTS, 3..7)
+  static const int forced_slots = [] {
+    const char* v = getenv("RBC_E2E_SLOTS");
+    return v ? atoi(v) : 0;
+  }();
+  const int kSlots = forced_slots >= 3 && forced_slots <= kMaxSlots ? forced_slots : 3;
   auto need = [&](int64_t c) {
     const size_t slot = 2 * align_up(c * N2 * es) + align_up(c * Q * RBC_PLAN_BYTES);
     return kSlots * slot + align_up(db) + 2 * align_up(T * 8) + 2 * align_up(T) + 4096 +
@@ -871,9 +879,9 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   if (need(C) > budget) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
   RBC_TRY(arena().reserve(need(C) + 256));
   Arena& A = arena();
-  void* da[kSlots];
-  void* dbb[kSlots];
-  void* dpl[kSlots];
+  void* da[kMaxSlots];
+  void* dbb[kMaxSlots];
+  void* dpl[kMaxSlots];
   for (int k = 0; k < kSlots; ++k) {
     da[k] = A.take(C * N2 * es);
     dbb[k] = A.take(C * N2 * es);

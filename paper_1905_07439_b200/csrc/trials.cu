@@ -82,10 +82,17 @@ AuxStreams* aux_streams(cudaStream_t caller) {
   AuxStreams* a = new AuxStreams;
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  // RBC_LANE_PRIO (tuning aid): 0 = truth lane high (default), 1 = all
+  // equal, 2 = product lanes high
+  static const int prio_mode = [] {
+    const char* v = getenv("RBC_LANE_PRIO");
+    return v ? atoi(v) : 0;
+  }();
   for (int i = 0; i < 3; ++i) {
     // the truth lane (FP64 pipe) gets the highest priority so its CTAs
     // interleave with the shared-memory-bound product kernels
-    cudaStreamCreateWithPriority(&a->s[i], cudaStreamNonBlocking, i == 0 ? hi : lo);
+    const bool high = prio_mode == 0 ? i == 0 : prio_mode == 2 ? i != 0 : false;
+    cudaStreamCreateWithPriority(&a->s[i], cudaStreamNonBlocking, high ? hi : lo);
     cudaEventCreateWithFlags(&a->join[i], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&a->fork, cudaEventDisableTiming);
