@@ -716,6 +716,10 @@ __device__ __forceinline__ GatherTab<n> load_tab(const GatherTab<n>& src) {
 
 // Stage-A item: one level-q0 position -> the R children, stored pairwise at
 // dst + r (dst 2-element aligned) with the level-(q0+1) sign m applied.
+// The ±1 network is odd (RN is symmetric under negation), so m is folded
+// into the n*n gather flips instead of flipping the R outputs: same values,
+// only the sign of an exact-zero child may differ (the plan path's
+// np.array_equal contract).
 template <class F, class T, int WHICH>
 __device__ __forceinline__ void expand_to_children(const T* __restrict__ src,
                                                    const GatherTab<F::n>& gt, T* dst, uint32_t m) {
@@ -724,7 +728,7 @@ __device__ __forceinline__ void expand_to_children(const T* __restrict__ src,
   using O = PackOps<T, 1>;
   Pack<T, 1> g[n * n];
 #pragma unroll
-  for (int k = 0; k < n * n; ++k) g[k] = O::flip(pload<T, 1>(src + gt.off[k]), gt.msk[k]);
+  for (int k = 0; k < n * n; ++k) g[k] = O::flip(pload<T, 1>(src + gt.off[k]), gt.msk[k] ^ m);
   Pack<T, 1> o[R];
   if (WHICH == 0)
     F::template expand_u<T, 1>(g, o, gt.lastrow, gt.lastcol);
@@ -733,11 +737,11 @@ __device__ __forceinline__ void expand_to_children(const T* __restrict__ src,
 #pragma unroll
   for (int r = 0; r + 1 < R; r += 2) {
     Pack<T, 2> v;
-    v.v[0] = flip_sign(o[r].v[0], m);
-    v.v[1] = flip_sign(o[r + 1].v[0], m);
+    v.v[0] = o[r].v[0];
+    v.v[1] = o[r + 1].v[0];
     pstore<T, 2>(dst + r, v);
   }
-  if (R & 1) dst[R - 1] = flip_sign(o[R - 1].v[0], m);
+  if (R & 1) dst[R - 1] = o[R - 1].v[0];
 }
 
 // Leaf row of lane li (k ascending, first term initialises).
@@ -964,22 +968,24 @@ subtree_reg_kernel(
         if (e < nsub * kids1) {
           using O = PackOps<T, 1>;
           const int u = e / kids1, pos = e - (e / kids1) * kids1;
+          // the child flip c_msk is folded into the n*n output flips (the
+          // contraction network is odd too; see expand_to_children)
           const T* zc = base + c_src[it];
           Pack<T, 1> pr[R];
 #pragma unroll
           for (int r = 0; r + 1 < R; r += 2) {
             const Pack<T, 2> v = pload<T, 2>(zc + r);
-            pr[r].v[0] = flip_sign(v.v[0], c_msk[it]);
-            pr[r + 1].v[0] = flip_sign(v.v[1], c_msk[it]);
+            pr[r].v[0] = v.v[0];
+            pr[r + 1].v[0] = v.v[1];
           }
-          if (R & 1) pr[R - 1].v[0] = flip_sign(zc[R - 1], c_msk[it]);
+          if (R & 1) pr[R - 1].v[0] = zc[R - 1];
           Pack<T, 1> o[n * n];
           F::template contract_w<T, 1>(pr, o);
           const int row = pos / s1, col = pos - (pos / s1) * s1;
           T* d = out + (t * K0 + k0 + u) * (int64_t)s0 * s0 + row * s0 + col;
 #pragma unroll
           for (int k = 0; k < n * n; ++k) {
-            const Pack<T, 1> val = O::flip(o[k], sc.msk[k]);
+            const Pack<T, 1> val = O::flip(o[k], sc.msk[k] ^ c_msk[it]);
             if (nonfinite) ok = ok && O::all_finite(val);
             pstore<T, 1>(d + sc.off[k], val);
           }
