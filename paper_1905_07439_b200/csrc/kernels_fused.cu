@@ -789,8 +789,17 @@ __device__ __forceinline__ Pack<T, M> leaf_row(const Pack<T, M>& xg, const Pack<
   return m;
 }
 
-template <class F, class T, int M, int SUB, bool ROT, int STG>
-__global__ void __launch_bounds__(SubtreeReg<F, T, M, SUB, STG>::NT, SubtreeReg<F, T, M, SUB, STG>::kMinBlocks)
+// the two-row leaf (ROT = 2) holds a third 27-register fiber: one resident
+// CTA fewer (RBC_SUBTREE_ROT2_DROP) keeps it spill-free
+#ifndef RBC_SUBTREE_ROT2_DROP
+#define RBC_SUBTREE_ROT2_DROP 1
+#endif
+template <class F, class T, int M, int SUB, int ROT, int STG>
+__global__ void __launch_bounds__(SubtreeReg<F, T, M, SUB, STG>::NT,
+                                  SubtreeReg<F, T, M, SUB, STG>::kMinBlocks -
+                                      (ROT == 2 && SubtreeReg<F, T, M, SUB, STG>::kMinBlocks > 1
+                                           ? RBC_SUBTREE_ROT2_DROP
+                                           : 0))
 subtree_reg_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0, int kchunk,
     T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
@@ -927,25 +936,66 @@ subtree_reg_kernel(
       const int nsub = kend - k0 < SUB ? kend - k0 : SUB;
       const T* X1 = base;
       const T* Y1 = base + kids1 * RP;
-      P xf[n * n], yf[n * n];
-#pragma unroll
-      for (int k = 0; k < n * n; ++k) {
-        const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
-#pragma unroll
-        for (int j = 0; j < M; ++j) {
-          xf[k].v[j] = X1[o + (ROT ? col_of[j] : j) * RP];
-          yf[k].v[j] = Y1[o + j * RP];
-        }
-      }
       const int xlr = pl1.perm[0][n - 1], xlc = pl1.perm[1][n - 1];
       const int ylr = pl1.perm[1][n - 1], ylc = pl1.perm[2][n - 1];
       P z[n * n];
+      if constexpr (ROT == 2) {
+        // Two Y rows per lane, one by shuffles: slot A = row ra (the lane's
+        // own row, row 0 for lane 2), slot B = row rb from the lane whose
+        // slot A holds it, slot C = row 2 on every lane.  The leaf fold
+        // ((A + B) + C) then keeps k = 2 last with no selects (the first two
+        // terms commute); the X fiber is loaded with its columns in slot
+        // order.  3 shuffles instead of 9 for one more Y network per r2.
+        static_assert(M == 3, "two-row leaf is for 3x3 leaves");
+        const int ra = li == 2 ? 0 : li;
+        const int rb = li == 1 ? 0 : 1;
+        const int xcol[3] = {ra, rb, 2};
+        const int fa = bu * S::slot + ra * s1 * RP + r1;
+        const int fc = bu * S::slot + 2 * s1 * RP + r1;
+        P xf[n * n], ya[n * n], yc[n * n];
 #pragma unroll
-      for (int r2 = 0; r2 < R; ++r2) {
-        const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
-        const P yg = F::template expand_v1<T, M>(yf, r2, ylr, ylc);
-        const P m = leaf_row<T, M, ROT>(xg, yg, gbase, gbase + rowA, gbase + rowB, li == 2);
-        F::template contract_w_step<T, M>(z, m, r2);
+        for (int k = 0; k < n * n; ++k) {
+          const int o = ((k / n) * M * s1 + (k % n) * M) * RP;
+#pragma unroll
+          for (int j = 0; j < M; ++j) {
+            xf[k].v[j] = X1[o + fib + xcol[j] * RP];
+            ya[k].v[j] = Y1[o + fa + j * RP];
+            yc[k].v[j] = Y1[o + fc + j * RP];
+          }
+        }
+        using A = Arith<T>;
+#pragma unroll
+        for (int r2 = 0; r2 < R; ++r2) {
+          const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
+          const P yag = F::template expand_v1<T, M>(ya, r2, ylr, ylc);
+          const P ycg = F::template expand_v1<T, M>(yc, r2, ylr, ylc);
+          P m;
+#pragma unroll
+          for (int j = 0; j < M; ++j) {
+            const T yb = shfl_val(yag.v[j], gbase + rb);
+            m.v[j] = A::add(A::add(A::mul(xg.v[0], yag.v[j]), A::mul(xg.v[1], yb)),
+                            A::mul(xg.v[2], ycg.v[j]));
+          }
+          F::template contract_w_step<T, M>(z, m, r2);
+        }
+      } else {
+        P xf[n * n], yf[n * n];
+#pragma unroll
+        for (int k = 0; k < n * n; ++k) {
+          const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
+#pragma unroll
+          for (int j = 0; j < M; ++j) {
+            xf[k].v[j] = X1[o + (ROT ? col_of[j] : j) * RP];
+            yf[k].v[j] = Y1[o + j * RP];
+          }
+        }
+#pragma unroll
+        for (int r2 = 0; r2 < R; ++r2) {
+          const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
+          const P yg = F::template expand_v1<T, M>(yf, r2, ylr, ylc);
+          const P m = leaf_row<T, M, ROT == 1>(xg, yg, gbase, gbase + rowA, gbase + rowB, li == 2);
+          F::template contract_w_step<T, M>(z, m, r2);
+        }
       }
       F::template contract_w_finish<T, M>(z);
       if (in_range && bu < nsub) {
@@ -1038,7 +1088,7 @@ subtree_reg_kernel(
   }
 }
 
-template <class F, class T, int M, int SUB, bool ROT, int STG>
+template <class F, class T, int M, int SUB, int ROT, int STG>
 cudaError_t launch_subtree_reg_v(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
                                  void* out, const PlanLevel* plans, int64_t pts, int q0,
                                  int64_t ntr, uint8_t* nonfinite, cudaStream_t st, int kchunk) {
@@ -1283,8 +1333,11 @@ cudaError_t launch_subtree_lane_v(const void* x, const void* y, int64_t xy_tstri
   return cudaGetLastError();
 }
 
-// Tuning aids (config 2, ms per launch): RBC_SUBTREE_SUB subtrees per CTA
-// step (1: 3.28, 3: 3.82), RBC_SUBTREE_ROT=1 rotated 6-shuffle leaf (3.38;
+// Tuning aids (config 2, ms per launch): RBC_SUBTREE_ROT leaf exchange:
+// 2 = two Y rows per lane, 3 shuffles (default: 2.743), 0 = 9 shuffles
+// (2.963; the kernel is bound by the shared-memory/shuffle data path, l1tex
+// 88%, and issue), 1 = rotated 6-shuffle leaf (3.38 in an earlier build;
+// RBC_SUBTREE_SUB subtrees per CTA step (1: 2.98, 2: 3.02, 3: 3.08);
 // a shuffle-free leaf where every lane expands the whole Y fiber measured
 // 8.5: 3x the Y network adds and 255 registers),
 // RBC_SUBTREE_STAGE TMA bulk prefetch of the level-q0 blocks (default 1:
@@ -1304,7 +1357,7 @@ cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride,
   }();
   static const int rot = [] {
     const char* v = getenv("RBC_SUBTREE_ROT");
-    return v ? atoi(v) : 0;
+    return v ? atoi(v) : 2;
   }();
   static const int kc = [] {
     const char* v = getenv("RBC_SUBTREE_CHUNK");
@@ -1332,16 +1385,18 @@ cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride,
     return launch_subtree_lane_v<F, T, M, 2>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr,
                                              nonfinite, st, kchunk);
 #define RBC_REG(SB, RT, SG)                                                                   \
-  if (sub == SB && (rot != 0) == RT && stg == SG)                                               \
+  if (sub == SB && rot == RT && stg == SG)                                                      \
     return launch_subtree_reg_v<F, T, M, SB, RT, SG>(x, y, xy_tstride, K0, out, plans, pts, q0, \
                                                      ntr, nonfinite, st, kchunk);
-  RBC_REG(1, false, 0)
-  RBC_REG(1, true, 0)
-  RBC_REG(1, false, 1)
-  RBC_REG(1, false, 2)
-  RBC_REG(2, false, 1)
-  RBC_REG(2, false, 2)
-  RBC_REG(3, false, 1)
+  RBC_REG(1, 0, 0)
+  RBC_REG(1, 1, 0)
+  RBC_REG(1, 1, 1)
+  RBC_REG(1, 0, 1)
+  RBC_REG(1, 2, 1)
+  RBC_REG(1, 0, 2)
+  RBC_REG(2, 0, 1)
+  RBC_REG(2, 0, 2)
+  RBC_REG(3, 0, 1)
 #undef RBC_REG
   return cudaErrorInvalidValue;
 }
