@@ -1334,7 +1334,10 @@ cudaError_t launch_subtree_lane_v(const void* x, const void* y, int64_t xy_tstri
 }
 
 // Tuning aids (config 2, ms per launch): RBC_SUBTREE_ROT leaf exchange:
-// 2 = two Y rows per lane, 3 shuffles (default: 2.743), 0 = 9 shuffles
+// 2 = two Y rows per lane, 3 shuffles (default: 2.743; with SUB 2: 3.16;
+// the 4 networks with a runtime fold order specialised by a CTA-uniform
+// switch on (lastrow, lastcol) instead of fold3 selects (F::kU1Last): 3.20,
+// 168 registers and jump tables), 0 = 9 shuffles
 // (2.963; the kernel is bound by the shared-memory/shuffle data path, l1tex
 // 88%, and issue), 1 = rotated 6-shuffle leaf (3.38 in an earlier build;
 // RBC_SUBTREE_SUB subtrees per CTA step (1: 2.98, 2: 3.02, 3: 3.08);

@@ -194,6 +194,14 @@ def emit():
             out.append("    (void)lastrow; (void)lastcol;")
             out.extend(expand_body(tensor, n, "lastrow", "lastcol"))
             out.append("  }")
+        for mname, tensor in (("kU1Last", f.u), ("kV1Last", f.v)):
+            # outputs whose single-output network has a runtime-ordered 3-term
+            # fold (reads lastrow / lastcol); callers may specialise those
+            mask = 0
+            for r in range(R):
+                if any("fold3" in ln for ln in expand_one_body(tensor, n, r, "lastrow", "lastcol")):
+                    mask |= 1 << r
+            out.append(f"  static constexpr unsigned long long {mname} = {mask:#x}ull;")
         for tname, tensor in (("expand_u1", f.u), ("expand_v1", f.v)):
             out.append("  // output r alone (r a compile-time constant after unrolling)")
             out.append("  template <class T, int W>")
