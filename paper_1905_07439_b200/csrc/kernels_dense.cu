@@ -11,6 +11,8 @@
 // Coefficients are per trial ((Tc, R, n, n), Tc in {1, T}); every thread of a
 // block row reads the same coefficient, so the loads are broadcasts.
 
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace rbc {
@@ -167,14 +169,13 @@ constexpr int contract_ppt() {
   return sizeof(T) == 8 && N >= 3 ? 2 : kPPT;
 }
 
-template <class T, int N>
+template <class T, int N, int CP = contract_ppt<T, N>(), int kRB = 4>
 __global__ void __launch_bounds__(kThreads) contract_dense_staged(
     const T* __restrict__ ch, int K, int mb, int R, const T* __restrict__ w, int64_t w_tstride,
     T* __restrict__ out, int64_t ntr, uint8_t* __restrict__ nonfinite) {
   extern __shared__ __align__(16) unsigned char sraw[];
   T* sw = reinterpret_cast<T*>(sraw);
   using A = Arith<T>;
-  constexpr int CP = contract_ppt<T, N>();
   const int s = N * mb;
   const int P = mb * mb;
   const int64_t items = (int64_t)K * P;
@@ -198,7 +199,6 @@ __global__ void __launch_bounds__(kThreads) contract_dense_staged(
     T acc[N * N][CP];
     // the children of kRB consecutive terms are loaded together (kRB * CP
     // independent loads in flight), then folded in ascending r
-    constexpr int kRB = 4;
     for (int r0 = 0; r0 < R; r0 += kRB) {
       T pr[kRB][CP];
 #pragma unroll
@@ -253,13 +253,12 @@ cudaError_t staged_expand_n(const void* x, int64_t xs, int64_t K, int64_t s, int
   return cudaGetLastError();
 }
 
-template <class T, int N>
+template <class T, int N, int CP = contract_ppt<T, N>(), int RB = 4>
 cudaError_t staged_contract_n(const void* ch, int64_t K, int64_t mb, int R, const void* w,
                               int64_t ws, void* out, int64_t ntr, uint8_t* nf, cudaStream_t st) {
   const int64_t items = K * mb * mb;
   const size_t smem = (size_t)R * N * N * sizeof(T);
-  constexpr int CP = contract_ppt<T, N>();
-  auto kern = contract_dense_staged<T, N>;
+  auto kern = contract_dense_staged<T, N, CP, RB>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -287,6 +286,29 @@ template <class T>
 cudaError_t staged_contract(int n, const void* ch, int64_t K, int64_t mb, int R, const void* w,
                             int64_t ws, void* out, int64_t ntr, uint8_t* nf, cudaStream_t st) {
   if ((size_t)R * n * n * sizeof(T) > 160 * 1024) return cudaErrorNotSupported;
+  // RBC_CONTRACT_DENSE=<positions per thread><children per batch> (tuning
+  // aid, binary64 n = 3): 24, 18, 28, 42, 14, 44, 112, 123, 212 (default)
+  static const int variant = [] {
+    const char* v = getenv("RBC_CONTRACT_DENSE");
+    return v ? atoi(v) : 0;
+  }();
+  if (sizeof(T) == 8 && n == 3 && variant) {
+    switch (variant) {
+      case 18: return staged_contract_n<T, 3, 1, 8>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+      case 28: return staged_contract_n<T, 3, 2, 8>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+      case 42: return staged_contract_n<T, 3, 4, 2>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+      case 14: return staged_contract_n<T, 3, 1, 4>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+      case 44: return staged_contract_n<T, 3, 4, 4>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+      case 112: return staged_contract_n<T, 3, 1, 12>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+      case 123: return staged_contract_n<T, 3, 1, 23>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+      case 212: return staged_contract_n<T, 3, 2, 12>(ch, K, mb, R, w, ws, out, ntr, nf, st);
+      default: break;
+    }
+  }
+  // binary64 n = 3 (config 3's noisy Laderman): 2 positions per thread and
+  // the children of 12 terms in flight (0.166 vs 0.183 ms per launch for 4)
+  if (sizeof(T) == 8 && n == 3)
+    return staged_contract_n<T, 3, 2, 12>(ch, K, mb, R, w, ws, out, ntr, nf, st);
   switch (n) {
     case 2: return staged_contract_n<T, 2>(ch, K, mb, R, w, ws, out, ntr, nf, st);
     case 3: return staged_contract_n<T, 3>(ch, K, mb, R, w, ws, out, ntr, nf, st);
