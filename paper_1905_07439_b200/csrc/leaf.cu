@@ -530,7 +530,7 @@ struct SmemBulk {
   static constexpr size_t smem = 2 * stage_bytes + 2 * sizeof(uint64_t);
 };
 
-template <class T, int M, int TM, int TN>
+template <class T, int M, int TM, int TN, int PF = 1>
 __global__ void __launch_bounds__(256) leaf_smem_bulk_kernel(int64_t batch, const T* __restrict__ x,
                                                              int64_t xs, const T* __restrict__ y,
                                                              int64_t ys, T* __restrict__ out) {
@@ -583,21 +583,27 @@ __global__ void __launch_bounds__(256) leaf_smem_bulk_kernel(int64_t batch, cons
       const T* gy = y + (b0 + l) * ys;
       const T* Xs = reinterpret_cast<const T*>(slot(stg, l, 0) + (reinterpret_cast<uintptr_t>(gx) & 15));
       const T* Ys = reinterpret_cast<const T*>(slot(stg, l, 1) + (reinterpret_cast<uintptr_t>(gy) & 15));
-      // operands of step k + 1 are loaded while step k multiplies (k fully
-      // unrolled); every output keeps its sequential k chain
-      T acc[TM][TN], a[2][TM], bb[2][TN];
+      // operands of step k + PF are loaded while step k multiplies (k fully
+      // unrolled, a ring of PF + 1 register slots); every output keeps its
+      // sequential k chain
+      constexpr int NS = PF + 1;
+      T acc[TM][TN], a[NS][TM], bb[NS][TN];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) a[0][i] = Xs[(ti + i) * M];
+      for (int p = 0; p < PF && p < M; ++p) {
 #pragma unroll
-      for (int j = 0; j < TN; ++j) bb[0][j] = Ys[tj + j];
+        for (int i = 0; i < TM; ++i) a[p][i] = Xs[(ti + i) * M + p];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) bb[p][j] = Ys[p * M + tj + j];
+      }
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        const int c = k & 1;
-        if (k + 1 < M) {
+        const int c = k % NS;
+        if (k + PF < M) {
+          const int nx = (k + PF) % NS;
 #pragma unroll
-          for (int i = 0; i < TM; ++i) a[c ^ 1][i] = Xs[(ti + i) * M + k + 1];
+          for (int i = 0; i < TM; ++i) a[nx][i] = Xs[(ti + i) * M + k + PF];
 #pragma unroll
-          for (int j = 0; j < TN; ++j) bb[c ^ 1][j] = Ys[(k + 1) * M + tj + j];
+          for (int j = 0; j < TN; ++j) bb[nx][j] = Ys[(k + PF) * M + tj + j];
         }
 #pragma unroll
         for (int i = 0; i < TM; ++i)
@@ -615,11 +621,11 @@ __global__ void __launch_bounds__(256) leaf_smem_bulk_kernel(int64_t batch, cons
   }
 }
 
-template <class T, int M, int TM, int TN>
+template <class T, int M, int TM, int TN, int PF = 1>
 cudaError_t run_smem_bulk(int64_t batch, const void* x, int64_t xs, const void* y, int64_t ys,
                           void* out, cudaStream_t st) {
   using S = SmemBulk<T, M, TM, TN>;
-  auto kern = leaf_smem_bulk_kernel<T, M, TM, TN>;
+  auto kern = leaf_smem_bulk_kernel<T, M, TM, TN, PF>;
   static const cudaError_t attr =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem);
   if (attr != cudaSuccess) return attr;
@@ -650,6 +656,11 @@ cudaError_t small_square(int64_t batch, int64_t M, const void* x, int64_t xs, co
       return run_smem_bulk<TIn, 27, 3, 9>(batch, x, xs, y, ys, out, st);
     if (M == 27 && batch >= 2048 && f == 212)
       return run_smem_bulk<TIn, 27, 9, 3>(batch, x, xs, y, ys, out, st);
+    // operands 2 / 3 k-steps ahead (tuning aid)
+    if (M == 27 && batch >= 2048 && f == 213)
+      return run_smem_bulk<TIn, 27, 3, 3, 2>(batch, x, xs, y, ys, out, st);
+    if (M == 27 && batch >= 2048 && f == 214)
+      return run_smem_bulk<TIn, 27, 3, 3, 3>(batch, x, xs, y, ys, out, st);
   }
   switch (M) {
     case 27: return run_smem<TIn, TAcc, 27, 3>(batch, x, xs, y, ys, out, st);
@@ -1226,6 +1237,17 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
     // (truth.cu; 8192: 28.8 vs 24.9 TFLOP/s); below it the widen pass costs
     // more than it saves (243 x 200: 15.8 vs 17.6) and the register-staged
     // tile runs (tools/leaf_bench.py)
+    if (forced == 310 && M >= 128 && N >= 128 && K >= 1)  // tuning: ragged truth tiles at any size
+      return run_truth<TIn, 128, 64, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
+    if (forced == 311 && M >= 128 && N >= 64)  // tuning: 128 x 64 tiles, 8 x 4 per thread
+      return run_tiled<TIn, TAcc, 128, 64, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
+    // binary64 operands of ragged sizes below 1024 (config 3: 729) skip the
+    // panel pass too: 128 x 64 register-staged tiles, 0.194 vs 0.233 ms per
+    // launch (config 4's 2048 binary16 truth stays on the bulk pipeline:
+    // 10.2 vs 11.8 ms)
+    if (forced == 0 && std::is_same<TIn, double>::value && M >= 512 && N >= 512 && K >= 1 &&
+        M < 1024 && N < 1024 && (M % 128 || N % 128))
+      return run_truth<TIn, 128, 64, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
     if (forced == 0 && M >= 512 && N >= 512 && K >= 1) {
       const cudaError_t e = launch_truth(std::is_same<TIn, double>::value ? kF64
                                          : std::is_same<TIn, float>::value ? kF32 : kF16,
