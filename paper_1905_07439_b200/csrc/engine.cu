@@ -29,6 +29,12 @@
 
 namespace rbc {
 
+namespace {
+thread_local cudaEvent_t t_expanded_event = nullptr;
+}  // namespace
+
+void set_expanded_event(cudaEvent_t ev) { t_expanded_event = ev; }
+
 static thread_local std::string g_last_error;
 
 static int set_error(int code, const char* fmt, ...) {
@@ -288,6 +294,7 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
         q += step;
       }
     }
+    if (t_expanded_event) CUDA_TRY(cudaEventRecord(t_expanded_event, st));
     // --- leaves (or the fused bottom subtree)
     const int64_t m = g.leaf_m;
     if (fuseL) {
