@@ -1335,7 +1335,8 @@ cudaError_t launch_subtree_lane_v(const void* x, const void* y, int64_t xy_tstri
 
 // Tuning aids (config 2, ms per launch): RBC_SUBTREE_ROT leaf exchange:
 // 2 = two Y rows per lane, 3 shuffles (default: 2.743; with SUB 2: 3.16,
-// SUB 3: 3.57 at one CTA per SM, 3.30 capped to two with spills;
+// SUB 3: 3.57 at one CTA per SM, 3.30 capped to two with spills; SUB 2
+// capped to three CTAs per SM: 3.19 with 144 bytes of spills;
 // the 4 networks with a runtime fold order specialised by a CTA-uniform
 // switch on (lastrow, lastcol) instead of fold3 selects (F::kU1Last): 3.20,
 // 168 registers and jump tables), 0 = 9 shuffles
