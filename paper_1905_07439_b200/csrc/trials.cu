@@ -341,20 +341,50 @@ int rbc_average_trials_async(int dtype, int Q, const int32_t* n, const int32_t* 
   const size_t eng_bytes = rbc_levels_workspace_bytes(dtype, Q, n, R, G, N);
   std::vector<const void*> pu(Q), pv(Q), pw(Q);
   std::vector<int64_t> tcG(Q, G), tc1(Q, 1);
+  // The pair's truth (one product: a fraction of the GPU's CTAs at config
+  // 3's size) runs on the truth lane beside the deterministic product and
+  // the start of the randomized one; the first error kernel joins it.  The
+  // fork is recorded after the previous pair's running mean, the last
+  // reader of `ref`.  Serial while the stage profiler runs.
+  static const bool serial_env = [] {
+    const char* v = getenv("RBC_SERIAL_LANES");
+    return v && v[0] == '1';
+  }();
+  const bool conc = !prof_on() && !serial_env;
+  AuxStreams* ax = conc ? aux_streams(st) : nullptr;
   for (int64_t p = 0; p < P; ++p) {
     const char* ap = (const char*)a + (size_t)p * N2 * es;
     const char* bp = (const char*)b + (size_t)p * N2 * es;
     cudaError_t e;
+    cudaStream_t s_truth = st;
+    if (conc) {
+      s_truth = ax->s[0];
+      CUDA_TRY(cudaEventRecord(ax->fork, st));
+      CUDA_TRY(cudaStreamWaitEvent(s_truth, ax->fork, 0));
+    }
     {
-      Stage stage(st, "truth_f64", (double)N2 * (2.0 * es + 8.0), 2.0 * (double)N2 * N);
-      e = launch_leaf(dtype, kF64, 1, N, N, N, ap, N2, bp, N2, ref, st);
+      Stage stage(s_truth, "truth_f64", (double)N2 * (2.0 * es + 8.0), 2.0 * (double)N2 * N);
+      e = launch_leaf(dtype, kF64, 1, N, N, N, ap, N2, bp, N2, ref, s_truth);
     }
     if (e != cudaSuccess) return fail_cuda(e, "truth", __FILE__, __LINE__);
+    bool joined = !conc;
+    auto join_truth = [&]() -> int {
+      if (!joined) {
+        CUDA_TRY(cudaEventRecord(ax->truth_done, s_truth));
+        CUDA_TRY(cudaStreamWaitEvent(st, ax->truth_done, 0));
+        joined = true;
+      }
+      return RBC_OK;
+    };
     if (det_u && err_det) {
       int rc = rbc_apply_levels_async(dtype, Q, n, R, tc1.data(), det_u, det_v, det_w, 1, N, ap,
                                       bp, 1, prod, nf_det ? nf_det + p : nullptr, eng, eng_bytes,
                                       stream);
       if (rc != RBC_OK) return rc;
+      {
+        const int jr = join_truth();
+        if (jr != RBC_OK) return jr;
+      }
       Stage stage(st, "rel_errors", (double)N2 * (es + 8.0), 3.0 * (double)N2);
       e = launch_rel_errors(dtype, 1, N2, prod, ref, 0, err_det + p, scratch, st);
       if (e != cudaSuccess) return fail_cuda(e, "rel_errors", __FILE__, __LINE__);
@@ -369,6 +399,10 @@ int rbc_average_trials_async(int dtype, int Q, const int32_t* n, const int32_t* 
                                     N, ap, bp, G, prod, nf_rand ? nf_rand + p * G : nullptr, eng,
                                     eng_bytes, stream);
     if (rc != RBC_OK) return rc;
+    {
+      const int jr = join_truth();
+      if (jr != RBC_OK) return jr;
+    }
     {
       Stage stage(st, "rel_errors", (double)G * N2 * (es + 8.0), 3.0 * (double)G * N2);
       e = launch_rel_errors(dtype, G, N2, prod, ref, 0, err_rand + p * G, scratch, st);
