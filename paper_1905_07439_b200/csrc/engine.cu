@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -417,6 +418,9 @@ static int check_device() {
 // Workspace for a synchronous call: everything not already accounted for,
 // bounded by the free device memory.
 static size_t host_ws_budget(size_t fixed, size_t want) {
+  // no device query when the arena already holds the request (see
+  // rbc_error_trials: cudaMemGetInfo can stall behind driver queries)
+  if (fixed + want + 256 <= arena().cap) return want;
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return want;
   const size_t usable = (size_t)((double)(free_b + arena().cap) * 0.85);
@@ -839,6 +843,15 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   if (!rand_plans && !with_det) return set_error(RBC_EVALUE, "no product requested");
   RBC_TRY(check_device());
   if (T == 0 || N == 0) return RBC_OK;
+  // RBC_E2E_HOST_TRACE=1: host-side phase times of the call (setup, plan
+  // upload, enqueue, wait for the results) on stderr
+  static const bool htrace = [] {
+    const char* v = getenv("RBC_E2E_HOST_TRACE");
+    return v && v[0] == '1';
+  }();
+  using hclock = std::chrono::steady_clock;
+  const hclock::time_point h0 = hclock::now();
+  hclock::time_point h1 = h0, h2 = h0, h3 = h0;
   const size_t es = dtype_size(dtype);
   const size_t N2 = (size_t)N * N;
   const size_t db = (size_t)Q * RBC_PLAN_BYTES;
@@ -879,11 +892,18 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
     return kSlots * slot + align_up(db) + 2 * align_up(T * 8) + 2 * align_up(T) + 4096 +
            (two ? 2 : 1) * align_up(rbc_error_trials_workspace_bytes(dtype, formula, Q, c, N));
   };
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
-  const size_t budget = (size_t)((double)(free_b + arena().cap) * 0.85);
-  while (C > 1 && need(C) > budget) C = (C + 1) / 2;
-  if (need(C) > budget) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
+  // The device memory query runs only when the arena must grow: in steady
+  // state an earlier call's arena already holds this chunking, and
+  // cudaMemGetInfo can stall the host for tens of ms behind concurrent
+  // driver queries (NVML polling; RBC_E2E_HOST_TRACE showed 31 and 97 ms
+  // "setup" phases in 30 calls).
+  if (need(C) > arena().cap) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t budget = (size_t)((double)(free_b + arena().cap) * 0.85);
+    while (C > 1 && need(C) > budget) C = (C + 1) / 2;
+    if (need(C) > budget) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
+  }
   RBC_TRY(arena().reserve(need(C) + 256));
   Arena& A = arena();
   void* da[kMaxSlots];
@@ -916,7 +936,9 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < n; ++j) ident[q].perm[i][j] = ident[q].inv[i][j] = (int8_t)j;
   }
+  h1 = hclock::now();
   CUDA_TRY(cudaMemcpyAsync(ddet, ident.data(), db, cudaMemcpyHostToDevice, sc));
+  h2 = hclock::now();
   CUDA_TRY(cudaEventRecord(pipe_event(15), sc));
   CUDA_TRY(cudaStreamWaitEvent(scs[1], pipe_event(15), 0));
   static const bool trace = [] {
@@ -987,6 +1009,7 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   }
   CUDA_TRY(cudaEventRecord(pipe_event(15), scs[1]));
   CUDA_TRY(cudaStreamWaitEvent(sc, pipe_event(15), 0));
+  h3 = hclock::now();
   if (trace) {  // RBC_E2E_TRACE=1: per-chunk copy / compute completion times
     CUDA_TRY(cudaStreamSynchronize(sc));
     for (size_t i = 0; i < tr_copy.size(); ++i) {
@@ -1008,6 +1031,13 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
     if (nf_det) CUDA_TRY(cudaMemcpyAsync(nf_det, dnf_d, T, cudaMemcpyDeviceToHost, sc));
   }
   CUDA_TRY(cudaStreamSynchronize(sc));
+  if (htrace) {
+    auto ms = [](hclock::time_point a, hclock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    fprintf(stderr, "e2e host: setup %.3f ms, plan upload %.3f, enqueue %.3f, wait %.3f (total %.3f)\n",
+            ms(h0, h1), ms(h1, h2), ms(h2, h3), ms(h3, hclock::now()), ms(h0, hclock::now()));
+  }
   return RBC_OK;
 }
 

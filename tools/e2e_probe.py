@@ -28,7 +28,7 @@ for _ in range(3):
 An, Bn, Pn = Ap.numpy(), Bp.numpy(), Pp.numpy()
 times = []
 f = cfg.formula_obj()
-for i in range(12):
+for i in range(int(sys.argv[3]) if len(sys.argv) > 3 else 12):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     error_trials(f, cfg.Q, An, Bn, cfg.mode, packed=Pn)
     torch.cuda.synchronize()
