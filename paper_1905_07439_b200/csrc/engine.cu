@@ -871,6 +871,13 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
                                                     1, (int64_t)(2 * T * N2 * es >> 23)));
   int64_t C = std::max<int64_t>(1, (T + nchunks - 1) / nchunks);
   if (C > 8) C = (C + 7) / 8 * 8;  // whole multiples of 8 trials keep grids regular
+  // RBC_E2E_RAMP (tuning aid): 1 = a 16, 32, ... ramp, then chunks of 2C;
+  // 2 = the ramp, then chunks of C
+  static const int ramp = [] {
+    const char* v = getenv("RBC_E2E_RAMP");
+    return v ? atoi(v) : 0;
+  }();
+  if (ramp == 1) C *= 2;
   // Two compute streams pay off for many small chunks (config 2: 1000 pairs
   // of 243); products of 512 and up are whole-GPU jobs per chunk, and their
   // truth scratch comes from the stream-ordered pool, which two streams
@@ -958,6 +965,12 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   std::vector<int64_t> sizes;
   {
     int64_t rem = T;
+    if (ramp && C >= 32) {  // 16, 32, ... up to C
+      for (int64_t r = 16; r < C && rem > 2 * r; r *= 2) {
+        sizes.push_back(r);
+        rem -= r;
+      }
+    }
     while (rem > C) {
       sizes.push_back(C);
       rem -= C;
