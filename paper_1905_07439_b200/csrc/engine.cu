@@ -16,7 +16,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
+#include <map>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -381,6 +383,7 @@ struct Arena {
   char* ptr = nullptr;
   size_t cap = 0;
   size_t off = 0;
+  unsigned gen = 0;  // bumped whenever the allocation moves
   int reserve(size_t bytes) {
     if (bytes <= cap) {
       off = 0;
@@ -389,6 +392,7 @@ struct Arena {
     if (ptr) cudaFree(ptr);
     ptr = nullptr;
     cap = 0;
+    ++gen;
     cudaError_t e = cudaMalloc((void**)&ptr, bytes);
     if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(arena)", __FILE__, __LINE__);
     cap = bytes;
@@ -819,6 +823,19 @@ static cudaEvent_t pipe_event(int i) {
   return ev[i];
 }
 
+// Per-chunk compute graphs of the host-buffer pipeline, keyed by every
+// argument (pointers into the arena included: a grown arena gets new keys;
+// the old execs are dropped with it).
+using GraphKey = std::array<uintptr_t, 16>;
+static std::map<GraphKey, cudaGraphExec_t>& chunk_graphs() {
+  static std::map<GraphKey, cudaGraphExec_t> m;
+  return m;
+}
+static void drop_chunk_graphs() {
+  for (auto& kv : chunk_graphs()) cudaGraphExecDestroy(kv.second);
+  chunk_graphs().clear();
+}
+
 // Host-buffer error trials, pipelined: trials are cut into chunks; chunk k+1
 // is copied host->device on a copy stream (into a ring of three input slots)
 // while chunks k and k-1 compute on two alternating compute streams with
@@ -913,6 +930,20 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   }
   RBC_TRY(arena().reserve(need(C) + 256));
   Arena& A = arena();
+  {
+    static unsigned graphs_gen = 0;
+    if (graphs_gen != A.gen) {  // graphs of an earlier allocation: stale
+      drop_chunk_graphs();
+      graphs_gen = A.gen;
+    }
+  }
+  // RBC_E2E_GRAPHS=1 (tuning aid): replay each chunk's compute as a CUDA
+  // graph.  Measured equal (c2 10.54 vs 10.50 ms per call, c1 1.25 both):
+  // launch gaps are not what makes chunked compute slower than one step
+  static const bool graphs = [] {
+    const char* v = getenv("RBC_E2E_GRAPHS");
+    return v && v[0] == '1';
+  }();
   void* da[kMaxSlots];
   void* dbb[kMaxSlots];
   void* dpl[kMaxSlots];
@@ -1009,10 +1040,42 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
       cudaEventRecord(tr_copy.back(), sx);
     }
     CUDA_TRY(cudaStreamWaitEvent(sk, copied, 0));
-    RBC_TRY(rbc_error_trials_async(dtype, formula, Q, nt, N, da[slot], dbb[slot],
-                                   rand_plans ? dpl[slot] : nullptr, with_det ? ddet : nullptr,
-                                   derr_r + t0, derr_d + t0, dnf_r + t0, dnf_d + t0,
-                                   dws[two ? (k & 1) : 0], ws, sk));
+    {
+      const void* pr = rand_plans ? dpl[slot] : nullptr;
+      const void* pd = with_det ? ddet : nullptr;
+      void* wsp = dws[two ? (k & 1) : 0];
+      if (graphs) {
+        // the chunk's compute as a CUDA graph, captured on first use and
+        // replayed by later calls (the arena keeps every pointer stable)
+        const GraphKey key = {(uintptr_t)sk, (uintptr_t)dtype, (uintptr_t)formula, (uintptr_t)Q,
+                              (uintptr_t)nt, (uintptr_t)N, (uintptr_t)da[slot],
+                              (uintptr_t)dbb[slot], (uintptr_t)pr, (uintptr_t)pd,
+                              (uintptr_t)(derr_r + t0), (uintptr_t)(derr_d + t0),
+                              (uintptr_t)(dnf_r + t0), (uintptr_t)(dnf_d + t0), (uintptr_t)wsp,
+                              (uintptr_t)ws};
+        auto it = chunk_graphs().find(key);
+        if (it == chunk_graphs().end()) {
+          cudaGraph_t gr = nullptr;
+          CUDA_TRY(cudaStreamBeginCapture(sk, cudaStreamCaptureModeThreadLocal));
+          const int rc = rbc_error_trials_async(dtype, formula, Q, nt, N, da[slot], dbb[slot], pr,
+                                                pd, derr_r + t0, derr_d + t0, dnf_r + t0,
+                                                dnf_d + t0, wsp, ws, sk);
+          const cudaError_t ce = cudaStreamEndCapture(sk, &gr);
+          if (rc != RBC_OK) return rc;
+          if (ce != cudaSuccess) return fail_cuda(ce, "capture (host-buffer chunk)", __FILE__, __LINE__);
+          cudaGraphExec_t ex = nullptr;
+          const cudaError_t ie = cudaGraphInstantiate(&ex, gr, 0);
+          cudaGraphDestroy(gr);
+          if (ie != cudaSuccess) return fail_cuda(ie, "graph instantiate", __FILE__, __LINE__);
+          it = chunk_graphs().emplace(key, ex).first;
+        }
+        CUDA_TRY(cudaGraphLaunch(it->second, sk));
+      } else {
+        RBC_TRY(rbc_error_trials_async(dtype, formula, Q, nt, N, da[slot], dbb[slot], pr, pd,
+                                       derr_r + t0, derr_d + t0, dnf_r + t0, dnf_d + t0, wsp, ws,
+                                       sk));
+      }
+    }
     CUDA_TRY(cudaEventRecord(computed, sk));
     if (trace) {
       tr_comp.emplace_back();
