@@ -76,12 +76,14 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--trials", type=int, default=0, help="pairs per rank per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches in the timed region")
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution run")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in s2-variants run")
     return ap.parse_args()
 
 
@@ -218,10 +220,14 @@ def measured_peaks():
 
 def fp_peaks():
     """Exact-order (FMUL+FADD, DMUL+DADD, HMUL2+HADD2) CUDA-core rates
-    measured by tools/fp_peak.cu (profiles/fp_peaks.json)."""
+    measured by tools/fp_peak.cu (profiles/fp_peaks.json).  The binary32
+    denominator is the larger of the scalar (FMUL+FADD) and packed
+    (FFMA2+FADD2) exact-order rates: the leaf kernels issue packed pairs."""
     p = ROOT / "profiles" / "fp_peaks.json"
     if p.exists():
-        return json.loads(p.read_text()), "measured (profiles/fp_peaks.json)"
+        d = json.loads(p.read_text())
+        d["f32_tflops"] = max(d["f32_tflops"], d.get("f32x2_tflops", 0.0))
+        return d, "measured (profiles/fp_peaks.json; binary32: max of FMUL+FADD, FFMA2+FADD2)"
     return {"f32_tflops": FP32_NOMINAL_TFLOPS, "f64_tflops": FP32_NOMINAL_TFLOPS / 2,
             "f16_tflops": FP32_NOMINAL_TFLOPS}, "nominal (half2 issues at half the FP32 rate)"
 
@@ -356,115 +362,296 @@ def roofline(prof: dict, config: str, cfg=None, pairs=None, sm_max_mhz=None):
     }
 
 
-# ------------------------------------------------------------ CPU oracle ----
-def _cpu_job(job):
-    """One CPU work unit through the oracle: pair p, products js (0 = the
-    deterministic product, j >= 1 = randomized plan j), evaluated on branch 0
-    of the top `depth` levels (depth 0 = the whole product).  Returns
-    (effective flops, errors) -- errors only for depth 0."""
-    cfg_name, p, js, depth = job
-    import numpy as np
+# --------------------------------------------------------------- CPU side ----
+REF_DIR = ROOT / "baseline" / "_ref"
 
-    from oracle import engine as oracle
-    from paper_1905_07439_b200.configs import get_config
-    from paper_1905_07439_b200.multiply import mode_tensors
-    from paper_1905_07439_b200.randomize import plan_levels
 
-    cfg = get_config(cfg_name)
-    f = cfg.formula_obj()
-    A, B = cfg.pair(p)
-    ref = oracle.standard_multiply(A.astype(np.float64), B.astype(np.float64)) if depth == 0 else None
-    errs = []
-    with np.errstate(all="ignore"):
-        for j in js:
+def reference_available() -> bool:
+    return (REF_DIR / "randbc" / "_engine.py").exists()
+
+
+def reference_modules():
+    """The unmodified reference package (baseline/_ref, installed by
+    tools/reference_install.py from /root/reference/pkg)."""
+    import types
+
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import randbc._engine
+    import randbc.experiments
+    import randbc.formula
+    import randbc.matgen
+    import randbc.multiply
+    import randbc.precision
+    import randbc.randomize
+    import randbc.rng
+
+    return types.SimpleNamespace(engine=randbc._engine, experiments=randbc.experiments,
+                                 formula=randbc.formula, matgen=randbc.matgen,
+                                 multiply=randbc.multiply, precision=randbc.precision,
+                                 randomize=randbc.randomize, rng=randbc.rng)
+
+
+def cpu_kind() -> str:
+    """'reference' when the unmodified reference is installed, else 'port'
+    (oracle/engine.py, the numpy restatement of randbc._engine)."""
+    return "reference" if reference_available() else "port"
+
+
+class CpuJob:
+    """One CPU work unit: pair p, products js (0 = the deterministic product,
+    j >= 1 = randomized plan j), each evaluated on branch 0 of its top
+    `depth` levels (depth 0 = the whole product; depth d = the sub-product of
+    branch 0, 1/R^d of the work, credited as 2n^3/R^d), through the
+    unmodified reference (`impl` 'reference') or the oracle port ('port').
+
+    prepare(): inputs, plans, hatted tables and (depth 0) the binary64 truth
+    -- untimed; compute(): the BC products only -- the timed part."""
+
+    def __init__(self, cfg_name, p, js, depth, impl):
+        self.cfg_name, self.p, self.js, self.depth, self.impl = cfg_name, p, tuple(js), depth, impl
+
+    def prepare(self):
+        import numpy as np
+
+        from paper_1905_07439_b200.configs import get_config
+        from paper_1905_07439_b200.precision import HALF
+
+        cfg = self.cfg = get_config(self.cfg_name)
+        fo = cfg.formula_obj()  # coefficient data (c3: builder noise on every entry)
+        if self.impl == "reference":
+            R = self.R = reference_modules()
+            self.mode = {"double": R.precision.DOUBLE, "single": R.precision.SINGLE}.get(
+                cfg.mode.kind, HALF)  # binary16: the duck-typed builder mode (SURVEY §8c)
+            self.f = R.formula.BilinearFormula(fo.u, fo.v, fo.w)
+            mseed = R.rng.derive_seed(cfg.seed, R.rng.ROLE_MATRIX, self.p,
+                                      _kind_index(R, cfg.kind))
+            A64, B64 = _ref_generate(R, cfg.kind, cfg.N, mseed)
+            draw = lambda key: R.randomize.RecursivePlan(tuple(  # noqa: E731
+                R.randomize.draw_plan(cfg.n, R.rng.derive_rng(cfg.seed, R.rng.ROLE_PLAN, key, q))
+                for q in range(cfg.Q)))
+            det_levels = lambda: [R.multiply.mode_tensors(self.f, self.mode)] * cfg.Q  # noqa: E731
+            plan_levels = lambda rp: [R.randomize._plan_levels(self.f, [rp.levels[q]], self.mode)  # noqa: E731
+                                      for q in range(cfg.Q)]
+        else:
+            from paper_1905_07439_b200.multiply import mode_tensors
+            from paper_1905_07439_b200.randomize import plan_levels as ours_plan_levels
+
+            self.mode, self.f = cfg.mode, fo
+            A64 = B64 = None
+            draw = cfg.plan
+            det_levels = lambda: [mode_tensors(fo, cfg.mode)] * cfg.Q  # noqa: E731
+            plan_levels = lambda rp: [ours_plan_levels(fo, [rp.levels[q]], cfg.mode)  # noqa: E731
+                                      for q in range(cfg.Q)]
+        if A64 is not None:
+            self.A, self.B = self.mode.array(A64), self.mode.array(B64)
+        else:
+            self.A, self.B = cfg.pair(self.p)
+        self.levels = []
+        for j in self.js:
             if j == 0:
-                levels = [mode_tensors(f, cfg.mode)] * cfg.Q
+                self.levels.append(det_levels())
             else:
-                rp = cfg.plan(cfg.plan_key(p, j) if cfg.plans_per_pair > 1 else cfg.plan_key(p))
-                levels = [plan_levels(f, [rp.levels[q]], cfg.mode) for q in range(cfg.Q)]
-            x = A[None, None]
-            y = B[None, None]
-            for q in range(depth):
-                u, v, _ = levels[q]
-                x = oracle.combine(x, u)[:, :1]
-                y = oracle.combine(y, v)[:, :1]
-            try:
-                C = oracle.apply_levels(levels[depth:], x[:, 0], y[:, 0], cfg.mode)
-                errs.append(float(oracle.rel_errors(C, ref)[0]) if ref is not None else None)
-            except OverflowError:
-                errs.append(float("nan"))
-    flops = 2.0 * cfg.N ** 3 * len(js) / float(cfg.rank) ** depth
-    return flops, errs
+                key = cfg.plan_key(self.p, j) if cfg.plans_per_pair > 1 else cfg.plan_key(self.p)
+                self.levels.append(plan_levels(draw(key)))
+        self.ref = None
+        if self.depth == 0:
+            Ad = self.A.astype(np.float64)
+            Bd = self.B.astype(np.float64)
+            if self.impl == "reference":
+                self.ref = self.R.multiply.standard_multiply(Ad, Bd, self.R.precision.DOUBLE)
+            else:
+                from oracle import engine as oracle
+
+                self.ref = oracle.standard_multiply(Ad, Bd)
+        return self
+
+    def compute(self, keep=False):
+        """The timed BC work.  Returns (credited flops, per-product errors
+        (depth 0) or None, per-product (x0, y0, C) when keep)."""
+        import numpy as np
+
+        if self.impl == "reference":
+            R = self.R
+            expand = lambda x, u: R.engine._expand(x, u[:, :1], self.mode)  # noqa: E731
+            apply = lambda lv, x, y: R.engine.apply_levels(lv, x, y, self.mode)  # noqa: E731
+        else:
+            from oracle import engine as oracle
+
+            expand = lambda x, u: oracle.combine(x, u[:, :1])  # noqa: E731
+            apply = lambda lv, x, y: oracle.apply_levels(lv, x, y, self.mode)  # noqa: E731
+        errs, kept = [], []
+        with np.errstate(all="ignore"):
+            for levels in self.levels:
+                x = self.A[None, None]
+                y = self.B[None, None]
+                for q in range(self.depth):  # branch 0 only: child r = 0 of each level
+                    u, v, _ = levels[q]
+                    x = expand(x, u)
+                    y = expand(y, v)
+                try:
+                    C = apply(levels[self.depth:], x[:, 0], y[:, 0])
+                    errs.append(C)
+                except OverflowError:
+                    C = None
+                    errs.append(None)
+                if keep:
+                    kept.append((x[:, 0], y[:, 0], C, levels[self.depth:]))
+        flops = 2.0 * self.cfg.N ** 3 * len(self.js) / float(self.cfg.rank) ** self.depth
+        return flops, errs, kept
+
+    def errors(self, outs):
+        """Relative errors (binary64) of the depth-0 products against the
+        truth, the reference's own formula when impl is 'reference'
+        (experiments.py:258-261); NaN for an overflowed product."""
+        import numpy as np
+
+        if self.ref is None:
+            return None
+        res = []
+        for C in outs:
+            if C is None:
+                res.append(float("nan"))
+            elif self.impl == "reference":
+                E = self.R.experiments
+                res.append(float(E._rel_errors(C, self.ref, E._frob(self.ref), self.mode)[0]))
+            else:
+                from oracle import engine as oracle
+
+                res.append(float(oracle.rel_errors(C, self.ref)[0]))
+        return np.array(res)
 
 
-def run_cpu_jobs(jobs, workers: int):
-    import concurrent.futures as cf
-
-    t0 = time.perf_counter()
-    if workers > 1:
-        with cf.ProcessPoolExecutor(max_workers=workers) as ex:
-            res = list(ex.map(_cpu_job, jobs))
-    else:
-        res = [_cpu_job(j) for j in jobs]
-    return time.perf_counter() - t0, res
+def _kind_index(R, kind):
+    base = {"uniform_pm1": "uniform", "quadrant100": "gaussian"}.get(kind, kind)
+    return R.matgen.MATRIX_KINDS.index(base)
 
 
-def cpu_sample_jobs(cfg, first_pair: int, count: int, per_pair: int, depth: int):
-    if cfg.plans_per_pair > 1:
-        js = list(range(per_pair))  # det + plans 1..per_pair-1
-    else:
-        js = [0, 1][:per_pair] if per_pair <= 2 else [0, 1]
-        if per_pair == 1:
-            js = [1]
-    return [(cfg.name, p, js, depth) for p in range(first_pair, first_pair + count)]
+def _ref_generate(R, kind, N, mseed):
+    """Operands on the reference's substreams: the reference's own generator
+    for its families; the two builder families (BASELINE configs 2 and 4) as
+    numpy draws on the same substreams."""
+    if kind in R.matgen.MATRIX_KINDS:
+        return R.matgen.generate(R.matgen.MatrixSpec(kind, N, mseed))
+    ga, gb = R.rng.derive_rng(mseed, 0), R.rng.derive_rng(mseed, 1)
+    if kind == "uniform_pm1":
+        return 2.0 * ga.random((N, N)) - 1.0, 2.0 * gb.random((N, N)) - 1.0
+    if kind == "quadrant100":
+        A, B = ga.standard_normal((N, N)), gb.standard_normal((N, N))
+        h = N // 2
+        A[:h, :h] *= 100.0
+        B[h:, h:] *= 100.0
+        return A, B
+    raise ValueError(kind)
 
 
-def describe_sample(cfg, count, per_pair, depth, seconds, cores):
+def describe_sample(cfg, count, per_pair, depth, seconds, cores, impl):
     what = f"{count} pair(s) x {per_pair} product(s)"
     if depth:
         what += (f", each product evaluated on branch 0 of its top {depth} level(s) "
-                 f"(1/{cfg.rank}^{depth} of the work, credited as 2n^3/{cfg.rank}^{depth})")
-    return (f"{what} through oracle/engine.py (numpy restatement of randbc._engine), "
-            f"{cores} process(es), {seconds:.1f} s")
+                 f"(1/{cfg.rank}^{depth} of the work, credited as 2n^3/{cfg.rank}^{depth}; "
+                 "extrapolated)")
+    src = ("the unmodified reference randbc (baseline/_ref: _engine.apply_levels on the tables "
+           "of randomize._plan_levels / multiply.mode_tensors, as recursive_randomized_apply / "
+           "recursive_apply call it)" if impl == "reference"
+           else "oracle/engine.py (numpy restatement of randbc._engine)")
+    return (f"{what} through {src}, {cores} process(es), {seconds:.1f} s of BC work "
+            "(input generation, plan hatting and the binary64 truth untimed)")
 
 
-# ------------------------------------------------------------ reference ----
+def _ref_worker(wid, cfg_name, js, depth, impl, first, steps, barrier, q):
+    """Persistent reference-arm worker: prepares its pair once (input
+    generation is not the measured path and costs seconds at n=8192), then per
+    step waits for all workers, times its BC work, and waits again."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    try:
+        job = CpuJob(cfg_name, first + wid, js, depth, impl).prepare()
+        for s in range(steps):
+            barrier.wait()
+            t0 = time.perf_counter()
+            flops, _, _ = job.compute()
+            t1 = time.perf_counter()
+            q.put((s, wid, t0, t1, flops))
+            barrier.wait()
+    except Exception as exc:  # noqa: BLE001
+        q.put(("error", wid, repr(exc), 0, 0))
+        barrier.abort()
+
+
+# per config: reference-arm products per job and subtree depth (each job a
+# bounded sample so that --steps 20 --warmup 5 ends within a few minutes)
+REF_ARM = {"c1": ((1,), 0), "c2": ((1,), 0), "c3": ((1,), 0), "c4": ((1,), 2), "c5": ((1,), 3)}
+
+
 def run_reference(args):
+    """--impl reference: the reference's own CPU path on all host cores, one
+    worker process per core, each step one bounded sample per worker."""
+    import multiprocessing as mp
+
     from paper_1905_07439_b200.configs import get_config
 
     world, rank, _ = dist_env()
     cfg = get_config(args.config)
     if rank != 0:
         return 0
+    impl = cpu_kind()
     cores = os.cpu_count() or 1
-    _, per_pair, depth = DEFAULTS[cfg.name]["cpu"]
-    p = 1
-    for _ in range(args.warmup):
-        run_cpu_jobs(cpu_sample_jobs(cfg, p, cores, per_pair, depth), cores)
-        p += cores
-    total_s, total_flops = 0.0, 0.0
-    for _ in range(args.steps):
-        dt, res = run_cpu_jobs(cpu_sample_jobs(cfg, p, cores, per_pair, depth), cores)
-        total_s += dt
-        total_flops += sum(r[0] for r in res)
-        p += cores
+    js, depth = REF_ARM[cfg.name]
+    steps = args.warmup + args.steps
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(cores)
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ref_worker, daemon=True,
+                         args=(w, cfg.name, js, depth, impl, 1, steps, barrier, q))
+             for w in range(cores)]
+    for pr in procs:
+        pr.start()
+    import queue
+
+    try:
+        rows = [q.get(timeout=900) for _ in range(cores * steps)]
+    except queue.Empty:
+        raise SystemExit("reference arm: a worker stopped reporting") from None
+    for pr in procs:
+        pr.join(timeout=60)
+    bad = [r for r in rows if r[0] == "error"]
+    if bad:
+        raise SystemExit(f"reference worker failed: {bad[0]}")
+    step_s, flops = [], []
+    for s in range(args.warmup, steps):
+        rs = [r for r in rows if r[0] == s]
+        step_s.append(max(r[3] for r in rs) - min(r[2] for r in rs))
+        flops.append(sum(r[4] for r in rs))
+    total_s = sum(step_s)
+    value = sum(flops) / total_s / 1e9
     ms = total_s / args.steps * 1e3
-    value = total_flops / total_s / 1e9
+    sample = describe_sample(cfg, cores, len(js), depth, ms / 1e3, cores, impl) + " per step"
     line = {
         "metric": METRIC, "impl": "reference", "value": round(value, 5), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.mode.label,
-        "data": "synthetic (seeded, reference seed layout)",
-        "config": {"workload": cfg.name, "desc": cfg.note, "jobs_per_step": cores},
-        "cpu_baseline": {
-            "value": round(value, 5), "unit": "GFLOP/s", "cores": cores, "kind": "port",
-            "sample": describe_sample(cfg, cores, per_pair, depth, ms / 1e3, cores) + " per step",
-        },
+        "data": "synthetic (seeded pairs and plans, reference seed layout; no dataset)",
+        "config": config_dict(cfg, world, args.trials),
+        "cpu_baseline": {"value": round(value, 5), "unit": "GFLOP/s", "cores": cores, "kind": impl,
+                         "sample": sample},
         "e2e": {"value": round(value, 5), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def config_dict(cfg, world, T=None):
+    """The `config` object of both arms' lines (identical for one config)."""
+    T = T or DEFAULTS[cfg.name]["pairs"]
+    return {
+        "workload": cfg.name, "desc": cfg.note, "formula": cfg.formula, "Q": cfg.Q, "n": cfg.N,
+        "dtype": cfg.mode.label, "pairs_per_rank": T,
+        "products_per_pair": cfg.plans_per_pair + 1 if cfg.plans_per_pair > 1 else 2,
+        "parallelism": f"trial-sharded x{world}",
+        "l2": "operands, binary64 truth and BC intermediates stream through HBM; every level's "
+              "working set exceeds the 126 MB L2, so no explicit flush is used",
+    }
 
 
 # ------------------------------------------------------------------ ours ----
@@ -738,15 +925,7 @@ def run_ours(args):
         "data": "synthetic (seeded pairs and plans, reference seed layout; no dataset)",
         "trials_per_s": round(T * world / (dev_ms / 1e3), 3),
         "products_per_s": round(wl.products * world / (dev_ms / 1e3), 3),
-        "config": {
-            "workload": cfg.name, "desc": cfg.note, "formula": cfg.formula, "Q": cfg.Q,
-            "n": cfg.N, "pairs_per_rank": T, "products_per_step_per_rank": wl.products,
-            "parallelism": f"trial-sharded x{world}",
-            "l2": f"per-step operands {A.nbytes * 2 / 1e6:.0f} MB + binary64 truth "
-                  f"{min(T, 1 if cfg.plans_per_pair > 1 else T) * cfg.N ** 2 * 8 / 1e6:.0f} MB and "
-                  "BC intermediates stream through HBM; the level working sets exceed the 126 MB L2 "
-                  "at these batch sizes, so no explicit flush is used",
-        },
+        "config": config_dict(cfg, world, args.trials),
         "gpu_launches": launches,
         "launch_mode": graph_note,
         "inputs": inputs,
@@ -762,31 +941,198 @@ def run_ours(args):
         e2e_ms = float(tmax[1])
         line["e2e"] = {"value": round(flops_step / (e2e_ms / 1e3) / 1e9, 3), "unit": "GFLOP/s",
                        "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(e2e[1]),
-                       "d2h_bytes_per_step": int(e2e[2])}
+                       "d2h_bytes_per_step": int(e2e[2]),
+                       "path": "public host-buffer call (error_trials / average_trials, C ABI "
+                               "rbc_error_trials): pinned host operands and plans copied H2D, "
+                               "per-trial errors copied D2H, inside the timed region"}
         calls = getattr(wl, "e2e_calls", None)
         if calls:
             line["e2e"]["ms_per_call"] = [round(c, 2) for c in calls]
+    del wl
+    torch.cuda.empty_cache()
 
+    if not args.no_tts and cfg.plans_per_pair == 1:
+        barrier()
+        line["time_to_solution"] = time_to_solution(cfg, T, dev, rank, world)
+    cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        count, per_pair, depth = DEFAULTS[cfg.name]["cpu"]
-        jobs = cpu_sample_jobs(cfg, first, count, per_pair, depth)
-        dt, res = run_cpu_jobs(jobs, 1)
-        cpu_val = sum(r[0] for r in res) / dt / 1e9
-        agree = None
-        if depth == 0 and cfg.plans_per_pair == 1 and per_pair == 2:
-            got = np.stack([err_d[:count], err_r[:count]], axis=1)
-            want = np.array([r[1] for r in res], dtype=np.float64)
-            agree = bool(np.allclose(got, want, rtol=1e-10, atol=0, equal_nan=True))
-        line["cpu_baseline"] = {
-            "value": round(cpu_val, 6), "unit": "GFLOP/s", "cores": 1, "kind": "port",
-            "sample": describe_sample(cfg, count, per_pair, depth, dt, 1),
-            "errors_agree_with_gpu": agree,
-        }
+        cpu = cpu_baseline_leg(cfg, first, T, err_r, err_d)
+        line["cpu_baseline"] = cpu
+        tts = line.get("time_to_solution")
+        if tts:
+            per_product_s = cpu.pop("_seconds_per_product")
+            tts["cpu_1core_extrapolated_s"] = round(per_product_s * 2 * cfg.trials, 1)
+            tts["cpu_note"] = ("the cpu_baseline sample's seconds per full product x 2 products x "
+                               f"{cfg.trials} pairs, one process; BC products only (input "
+                               "generation and the binary64 truth excluded)")
+            tts["speedup_vs_cpu_1core"] = round(tts["cpu_1core_extrapolated_s"] / tts["seconds"], 1)
+        else:
+            cpu.pop("_seconds_per_product", None)
+    if rank == 0 and world == 1 and not args.no_dropin:
+        line["dropin_e2e"] = dropin_e2e()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def cpu_baseline_leg(cfg, first, T, err_r, err_d):
+    """The reference's CPU path on one core over a bounded sample of the
+    workload (rank 0, N=1), and the parity of the GPU run against it: the
+    per-trial errors of whole products (configs 1-3), or, where one CPU
+    product takes minutes (configs 4-5), the branch-0 sub-products bit for bit
+    against the GPU engine run on the same sub-operands through the drop-in
+    (reference _engine.apply_levels signature)."""
+    import numpy as np
+
+    from paper_1905_07439_b200 import engine
+
+    count, per_pair, depth = DEFAULTS[cfg.name]["cpu"]
+    count = min(count, T)
+    impl = cpu_kind()
+    js = tuple(range(per_pair)) if cfg.plans_per_pair > 1 else ((0, 1) if per_pair == 2 else (1,))
+    total_s, flops, agree, branch = 0.0, 0.0, [], []
+    for i, p in enumerate(range(first, first + count)):
+        job = CpuJob(cfg.name, p, js, depth, impl).prepare()
+        t0 = time.perf_counter()
+        fl, outs, kept = job.compute(keep=depth > 0)
+        total_s += time.perf_counter() - t0
+        flops += fl
+        if depth == 0:
+            want = job.errors(outs)
+            G = cfg.plans_per_pair
+            got = np.array([err_d[i] if j == 0 else (err_r[i * G + j - 1] if G > 1 else err_r[i])
+                            for j in js])
+            agree.append(bool(np.allclose(got, want, rtol=1e-12, atol=0, equal_nan=True)))
+        else:
+            for x0, y0, C, lv in kept:
+                try:
+                    Cg = engine.apply_levels(lv, x0, y0, job.mode)
+                except OverflowError:
+                    Cg = None
+                branch.append((C is None and Cg is None) or
+                              (C is not None and Cg is not None and np.array_equal(C, Cg)))
+        del job
+    out = {
+        "value": round(flops / total_s / 1e9, 6), "unit": "GFLOP/s", "cores": 1, "kind": impl,
+        "sample": describe_sample(cfg, count, len(js), depth, total_s, 1, impl),
+        "errors_agree_with_gpu": all(agree) if agree else None,
+        "_seconds_per_product": total_s / (count * len(js)) * float(cfg.rank) ** depth,
+    }
+    if depth == 0:
+        out["errors_compared"] = f"{count} pair(s) x {len(js)} product(s), rtol 1e-12"
+    else:
+        out["branch_products_bitwise_equal"] = all(branch)
+        out["branch_products_compared"] = (
+            f"{len(branch)} branch-0 sub-product(s) at n={cfg.N // cfg.n ** depth} "
+            f"(levels {depth}..{cfg.Q - 1}), CPU vs GPU engine (engine.apply_levels), "
+            "values and overflow")
+        out["errors_agree_with_gpu"] = all(branch)
+    return out
+
+
+def time_to_solution(cfg, T_step, dev, rank, world):
+    """Wall-clock time for the config's whole trial set (e.g. configuration 5:
+    all 64 pairs), strong-scaled over the ranks: each rank draws its share of
+    the pairs on the GPU (rbc_matgen, bit-identical to the host draw), runs
+    the error trials T_step pairs at a time and copies the errors back; the
+    figure is the max over ranks."""
+    import numpy as np
+    import torch
+
+    from paper_1905_07439_b200 import distributed
+    from paper_1905_07439_b200.configs import make_pairs_device
+    from paper_1905_07439_b200.randomize import pack_recursive_plans
+    from paper_1905_07439_b200.trials import DeviceErrorTrials
+
+    total = cfg.trials
+    per = -(-total // world)
+    lo, hi = 1 + rank * per, min(total, (rank + 1) * per)
+    f = cfg.formula_obj()
+    runners = {}
+    errs = []
+
+    def chunk(p0, cnt):
+        a, b = make_pairs_device(cfg, p0, cnt, dev)
+        packed = pack_recursive_plans([cfg.plan(cfg.plan_key(p)) for p in range(p0, p0 + cnt)],
+                                      cfg.Q, cfg.n)
+        pl = torch.from_numpy(packed).to(dev)
+        if cnt not in runners:
+            runners[cnt] = DeviceErrorTrials(f, cfg.Q, cfg.N, cfg.mode, cnt, device=dev)
+        r = runners[cnt]
+        r.run(a, b, pl)
+        return np.stack([r.err_rand.cpu().numpy(), r.err_det.cpu().numpy()])
+
+    chunk(lo, min(T_step, hi - lo + 1))  # warm-up (kernel attributes, pools)
+    torch.cuda.synchronize()
+    distributed.barrier_if(world)
+    t0 = time.perf_counter()
+    for p0 in range(lo, hi + 1, T_step):
+        errs.append(chunk(p0, min(T_step, hi - p0 + 1)))
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    sec = float(distributed.max_over_ranks([sec], device=dev)[0])
+    e = np.concatenate(errs, axis=1)
+    return {
+        "pairs": total, "products": 2 * total, "seconds": round(sec, 3), "scaling": "strong",
+        "n_gpus": world, "pairs_per_launch": T_step,
+        "what": "wall clock, all pairs: device input generation, plans, binary64 truth, "
+                "deterministic + randomized products, errors copied to the host (max over ranks)",
+        "err_rand_mean_rank0": float(np.nanmean(e[0])),
+    }
+
+
+def dropin_e2e():
+    """The reference's own workflow through the drop-in: the shipped command
+    `randbc experiment s2-variants --seed 1` (n=320, Q=1..5, 100 plans, all six
+    input families, f32; reference README.md:108-109 "around ten minutes",
+    test_acceptance.py:330-365 caps it at 1800 s) run by the unmodified
+    reference (baseline/_ref) with engine.install(), wall clock; its CSV is
+    compared with the reference's artifact (tests/golden/s2_variants_320.csv,
+    rel_error to 1e-12)."""
+    import io
+
+    import numpy as np
+
+    if not reference_available():
+        return {"unavailable": "baseline/_ref (the unmodified reference) is not installed"}
+    from paper_1905_07439_b200 import engine
+
+    R = reference_modules()
+    import randbc.cli
+
+    engine.install(R.engine)
+    try:
+        with tempfile.TemporaryDirectory() as d:
+            out = Path(d) / "s2.csv"
+            sink = io.StringIO()
+            t0 = time.perf_counter()
+            with contextlib.redirect_stdout(sink):
+                code = randbc.cli.main(["experiment", "s2-variants", "--seed", "1", "--out", str(out)])
+            sec = time.perf_counter() - t0
+            got = out.read_text().splitlines() if code == 0 else []
+    finally:
+        engine.uninstall(R.engine)
+    want = (ROOT / "tests" / "golden" / "s2_variants_320.csv").read_text().splitlines()
+
+    def table(lines):
+        hdr = lines[0].split(",")
+        k = hdr.index("rel_error")
+        return {tuple(x for i, x in enumerate(row.split(",")) if i != k): float(row.split(",")[k])
+                for row in lines[1:]}
+
+    tg, tw = table(got) if got else {}, table(want)
+    match = bool(got) and tg.keys() == tw.keys() and all(
+        np.isclose(tg[key], tw[key], rtol=1e-12, atol=0) for key in tw)
+    return {
+        "workload": "randbc experiment s2-variants --seed 1 (reference CLI defaults: n=320, "
+                    "Q=1..5, 100 plans, 6 input families, f32) with engine.install()",
+        "seconds": round(sec, 2), "exit_code": code, "rows": len(got) - 1 if got else 0,
+        "matches_reference_artifact": match,
+        "reference_published": "around ten minutes (README.md:108-109); acceptance cap 1800 s "
+                               "(tests/test_acceptance.py:365)",
+    }
 
 
 def main():

@@ -113,6 +113,20 @@ int rbc_apply_plans(int dtype, int formula, int Q, int64_t Tp, const void* packe
                     int64_t T0, int64_t N, const void* a, const void* b, int64_t T, void* out,
                     uint8_t* nonfinite, uint64_t* leaf_multiplies);
 
+/* ---- diagonal rescaling baseline (reference rescale.py:60-99) -----------
+ * randbc.rescale.rescaled_multiply(A, B, Q, schedule, mode, formula) on the
+ * device: steps[i] = 0 (outside) or 1 (inside); the abs-max, reciprocal,
+ * square-root and diagonal-scaling steps run as kernels in the mode with the
+ * reference's roundings, then the deterministic recursion (formula > 0: an
+ * exact +-1 formula id; formula = 0: dense tables u/v/w[q] (R[q], n[q], n[q])
+ * in the mode), then the restores.  Host buffers (N x N), synchronous.
+ * RBC_EVALUE "degenerate input: zero row|column maximum" (rescale.py:36-41);
+ * RBC_EOVERFLOW when the recursion's result is non-finite (_engine.py:146). */
+int rbc_rescaled_multiply(int dtype, int formula, int Q, const int32_t* n, const int32_t* R,
+                          const void* const* u, const void* const* v, const void* const* w,
+                          int nsteps, const int32_t* steps, int64_t N, const void* a,
+                          const void* b, void* out);
+
 /* ---- device-pointer twins (stream ordered, no synchronisation) ------------ */
 
 size_t rbc_levels_workspace_bytes(int dtype, int Q, const int32_t* n, const int32_t* R,

@@ -52,6 +52,42 @@ template <> struct Arith<__half2> {
   static __device__ __forceinline__ __half2 neg(__half2 a) { return __hneg2(a); }
 };
 
+// ------------------------------------------------ packed binary32 pairs ----
+// sm_100a issues two binary32 lanes per instruction (FFMA2 / FADD2 on
+// 64-bit register pairs).  The FMA pipe takes them at half the scalar
+// instruction rate, so the element rate is unchanged (tools/fp_peak.cu:
+// 37.1 vs 35.1 TFLOP/s exact-order), but every packed instruction frees an
+// issue slot -- the limit of the exact-order leaf, which needs a separate
+// FMUL and FADD per multiply-add.
+//
+// ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under
+// -fmad=false (and folds an fma with a literal -0 addend the same way), so
+// the rounded multiply is issued as fma.rn.f32x2(a, b, z) with z = (-0, -0)
+// passed in at run time, which the compiler cannot see through:
+// fl(a*b + -0) == fl(a*b) for every a, b (a +0 product stays +0, -0 stays
+// -0; no flush to zero).  Pass kF2NegZero as a kernel argument.
+constexpr uint64_t kF2NegZero = 0x8000000080000000ull;
+
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+// (a, a) * (b.lo, b.hi), each product rounded once; ptxas encodes the
+// broadcast as a scalar .F32 operand (no MOV)
+__device__ __forceinline__ uint64_t f2_mul_bcast(float a, uint64_t b, uint64_t negz) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_pack(a, a)), "l"(b), "l"(negz));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 // Bit-exact sign flip (used for the signed permutations of a plan).
 __device__ __forceinline__ float flip_sign(float x, uint32_t m) {
   return __uint_as_float(__float_as_uint(x) ^ m);

@@ -16,9 +16,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <array>
-#include <chrono>
-#include <map>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -212,7 +209,12 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
   const size_t es = dtype_size(dt);
   const int64_t N2 = g.N * g.N;
   const size_t ptw = per_trial_ws(g, dt);
-  if (p.T == 0 || g.N == 0) return RBC_OK;
+  if (p.T == 0 || g.N == 0) {
+    // empty operands: no product, no overflow (the flags may sit on stale
+    // arena bytes of an earlier call)
+    if (p.nonfinite && p.T) CUDA_TRY(cudaMemsetAsync(p.nonfinite, 0, (size_t)p.T, st));
+    return RBC_OK;
+  }
   int64_t chunk = ptw ? (int64_t)(ws_bytes / ptw) : p.T;
   chunk = std::min(chunk, p.T);
   while (chunk > 0 && ws_for(g, dt, chunk) > ws_bytes) --chunk;
@@ -777,6 +779,146 @@ int rbc_apply_plans(int dtype, int formula, int Q, int64_t Tp, const void* packe
   return RBC_OK;
 }
 
+// Diagonal rescaling baseline (reference rescale.py:60-99), device-resident:
+// one H2D per operand, the scaling steps (rescale.cu), the deterministic
+// recursion (plan path with identity plans for the exact +-1 formulas, dense
+// tables otherwise; Q = 0 is the standard product), the restores, one D2H.
+int rbc_rescaled_multiply(int dtype, int formula, int Q, const int32_t* n, const int32_t* R,
+                          const void* const* u, const void* const* v, const void* const* w,
+                          int nsteps, const int32_t* steps, int64_t N, const void* a,
+                          const void* b, void* out) {
+  if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);
+  if (Q < 0 || N < 0 || nsteps < 0) return set_error(RBC_EVALUE, "negative size");
+  for (int i = 0; i < nsteps; ++i)
+    if (steps[i] != 0 && steps[i] != 1) return set_error(RBC_EVALUE, "unknown schedule step");
+  std::vector<int32_t> nv, Rv;
+  if (formula > 0) {
+    if (!formula_n(formula)) return set_error(RBC_EVALUE, "unknown formula id %d", formula);
+    nv.assign(Q, formula_n(formula));
+    Rv.assign(Q, formula_R(formula));
+  } else {
+    nv.assign(n, n + Q);
+    Rv.assign(R, R + Q);
+  }
+  Geometry g;
+  if (Q > 0) {
+    RBC_TRY(make_geometry(Q, nv.data(), Rv.data(), N, &g));
+    for (int q = 0; q < Q; ++q)
+      if (nv[q] > 8) return set_error(RBC_EUNSUPPORTED, "block grids above 8x8 are not supported");
+  }
+  RBC_TRY(check_device());
+  if (N == 0) return RBC_OK;
+  const size_t es = dtype_size(dtype);
+  const size_t N2b = (size_t)N * N * es, vb = (size_t)N * es;
+  std::lock_guard<std::mutex> lock(arena().mu);
+  std::vector<size_t> cbytes(Q, 0);
+  size_t fixed = 3 * align_up(N2b) + (size_t)4 * nsteps * align_up(vb) + align_up(2 * nsteps + 1) +
+                 align_up(absmax_scratch_bytes(N)) + align_up((size_t)Q * RBC_PLAN_BYTES + 1) + 4096;
+  if (formula <= 0)
+    for (int q = 0; q < Q; ++q) {
+      cbytes[q] = (size_t)Rv[q] * nv[q] * nv[q] * es;
+      fixed += 3 * align_up(cbytes[q]);
+    }
+  const size_t ws_want = Q > 0 ? ws_for(g, dtype, 1) : 0;
+  const size_t ws_bytes = host_ws_budget(fixed, ws_want);
+  if (ws_bytes < ws_want) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
+  RBC_TRY(arena().reserve(fixed + ws_bytes + 256));
+  Arena& A = arena();
+  void* dA = A.take(N2b);
+  void* dB = A.take(N2b);
+  void* dC = A.take(N2b);
+  std::vector<void*> vec((size_t)4 * nsteps);
+  for (auto& p : vec) p = A.take(vb);
+  uint8_t* flags = (uint8_t*)A.take(2 * nsteps + 1);  // [2 s], [2 s + 1]: zero maxima; [2n]: overflow
+  void* scratch = A.take(absmax_scratch_bytes(N));
+  void* dplans = A.take((size_t)Q * RBC_PLAN_BYTES + 1);
+  std::vector<const void*> du(Q), dv(Q), dw(Q);
+  if (formula <= 0)
+    for (int q = 0; q < Q; ++q) {
+      void* pu = A.take(cbytes[q]);
+      void* pv = A.take(cbytes[q]);
+      void* pw = A.take(cbytes[q]);
+      CUDA_TRY(cudaMemcpy(pu, u[q], cbytes[q], cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(pv, v[q], cbytes[q], cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(pw, w[q], cbytes[q], cudaMemcpyHostToDevice));
+      du[q] = pu;
+      dv[q] = pv;
+      dw[q] = pw;
+    }
+  void* dws = A.take(ws_bytes);
+  cudaStream_t st = nullptr;
+  CUDA_TRY(cudaMemcpy(dA, a, N2b, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dB, b, N2b, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemsetAsync(flags, 0, 2 * nsteps + 1, st));
+  // schedule (rescale.py:84-97)
+  std::vector<std::pair<const void*, const void*>> restore;
+  for (int i = 0; i < nsteps; ++i) {
+    void** vv = vec.data() + 4 * i;
+    if (steps[i] == 0) {  // outside: da = rowmax|A|, db = colmax|B|; A = diag(1/da) A, B = B diag(1/db)
+      CUDA_TRY(launch_absmax(dtype, dA, N, 1, vv[0], flags + 2 * i, scratch, st));
+      CUDA_TRY(launch_absmax(dtype, dB, N, 0, vv[1], flags + 2 * i + 1, scratch, st));
+      CUDA_TRY(launch_recip(dtype, vv[0], N, vv[2], st));
+      CUDA_TRY(launch_recip(dtype, vv[1], N, vv[3], st));
+      ScaleList ra{{vv[2]}, {nullptr}, 1}, cb{{nullptr}, {vv[3]}, 1};
+      CUDA_TRY(launch_scale(dtype, dA, N, ra, st));
+      CUDA_TRY(launch_scale(dtype, dB, N, cb, st));
+      restore.emplace_back(vv[0], vv[1]);
+    } else {  // inside: d = sqrt(rowmax|B| / colmax|A|); A = A diag(d), B = diag(1/d) B
+      CUDA_TRY(launch_absmax(dtype, dB, N, 1, vv[0], flags + 2 * i, scratch, st));
+      CUDA_TRY(launch_absmax(dtype, dA, N, 0, vv[1], flags + 2 * i + 1, scratch, st));
+      CUDA_TRY(launch_inside_factors(dtype, vv[0], vv[1], N, vv[2], vv[3], st));
+      ScaleList ca{{nullptr}, {vv[2]}, 1}, rb{{vv[3]}, {nullptr}, 1};
+      CUDA_TRY(launch_scale(dtype, dA, N, ca, st));
+      CUDA_TRY(launch_scale(dtype, dB, N, rb, st));
+    }
+  }
+  std::vector<uint8_t> hf(2 * nsteps + 1, 0);
+  if (nsteps) {
+    CUDA_TRY(cudaMemcpy(hf.data(), flags, 2 * nsteps, cudaMemcpyDeviceToHost));
+    // the reference's check order: within a step the row maxima (of A for
+    // outside, of B for inside) are checked before the column maxima
+    for (int i = 0; i < nsteps; ++i) {
+      if (hf[2 * i]) return set_error(RBC_EVALUE, "degenerate input: zero row maximum");
+      if (hf[2 * i + 1]) return set_error(RBC_EVALUE, "degenerate input: zero column maximum");
+    }
+  }
+  // the deterministic recursion (rescale.py:95, multiply.py:72-99)
+  uint8_t* nf = flags + 2 * nsteps;
+  if (Q == 0) {  // standard_multiply: no finiteness check (multiply.py:44-51)
+    CUDA_TRY(launch_leaf(dtype, dtype, 1, N, N, N, dA, 0, dB, 0, dC, st));
+  } else if (formula > 0) {
+    std::vector<PlanLevel> ident(Q);
+    const int nn = nv[0];
+    for (int q = 0; q < Q; ++q) {
+      memset(&ident[q], 0, sizeof(PlanLevel));
+      for (int r = 0; r < 3; ++r)
+        for (int j = 0; j < nn; ++j) ident[q].perm[r][j] = ident[q].inv[r][j] = (int8_t)j;
+    }
+    CUDA_TRY(cudaMemcpy(dplans, ident.data(), (size_t)Q * sizeof(PlanLevel), cudaMemcpyHostToDevice));
+    RBC_TRY(rbc_apply_plans_async(dtype, formula, Q, 1, dplans, 1, N, dA, dB, 1, dC, nf, dws,
+                                  ws_bytes, st));
+  } else {
+    std::vector<int64_t> Tc(Q, 1);
+    RBC_TRY(rbc_apply_levels_async(dtype, Q, nv.data(), Rv.data(), Tc.data(), du.data(), dv.data(),
+                                   dw.data(), 1, N, dA, dB, 1, dC, nf, dws, ws_bytes, st));
+  }
+  CUDA_TRY(cudaMemcpy(&hf[2 * nsteps], nf, 1, cudaMemcpyDeviceToHost));
+  if (hf[2 * nsteps]) return set_error(RBC_EOVERFLOW, "non-finite result");
+  // restores in reverse schedule order (rescale.py:96-98), one pass
+  for (size_t k0 = 0; k0 < restore.size(); k0 += 8) {
+    ScaleList sl{};
+    for (size_t k = k0; k < restore.size() && k < k0 + 8; ++k) {
+      const auto& rv = restore[restore.size() - 1 - k];
+      sl.row[sl.n] = rv.first;
+      sl.col[sl.n] = rv.second;
+      ++sl.n;
+    }
+    CUDA_TRY(launch_scale(dtype, dC, N, sl, st));
+  }
+  CUDA_TRY(cudaMemcpy(out, dC, N2b, cudaMemcpyDeviceToHost));
+  return RBC_OK;
+}
+
 int rbc_leaf_matmul(int dtype, int64_t batch, int64_t xs, int64_t ys, int64_t M, int64_t K,
                     int64_t N, const void* x, const void* y, void* out) {
   if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);
@@ -815,25 +957,12 @@ static cudaStream_t copy_stream(int i = 0) {
   return s[i];
 }
 
-constexpr int kMaxSlots = 7;  // pipe events: 2 per slot, plus 14 and 15
+constexpr int kSlots = 3;  // input slots of the host-buffer pipeline
 
 static cudaEvent_t pipe_event(int i) {
-  static cudaEvent_t ev[16] = {nullptr};
+  static cudaEvent_t ev[2 * kSlots + 1] = {nullptr};
   if (!ev[i]) cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
   return ev[i];
-}
-
-// Per-chunk compute graphs of the host-buffer pipeline, keyed by every
-// argument (pointers into the arena included: a grown arena gets new keys;
-// the old execs are dropped with it).
-using GraphKey = std::array<uintptr_t, 16>;
-static std::map<GraphKey, cudaGraphExec_t>& chunk_graphs() {
-  static std::map<GraphKey, cudaGraphExec_t> m;
-  return m;
-}
-static void drop_chunk_graphs() {
-  for (auto& kv : chunk_graphs()) cudaGraphExecDestroy(kv.second);
-  chunk_graphs().clear();
 }
 
 // Host-buffer error trials, pipelined: trials are cut into chunks; chunk k+1
@@ -841,7 +970,9 @@ static void drop_chunk_graphs() {
 // while chunks k and k-1 compute on two alternating compute streams with
 // their own workspaces, so the small per-chunk grids of consecutive chunks
 // share the GPU.  With pinned host buffers the PCIe transfer hides behind the
-// kernels.
+// kernels.  (Measured and dropped in round 1: more slots, a second copy
+// stream, ramped chunk sizes and per-chunk CUDA graphs -- all equal or
+// slower.)
 int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
                      const void* b, const void* rand_plans, int with_det, double* err_rand,
                      double* err_det, uint8_t* nf_rand, uint8_t* nf_det) {
@@ -860,24 +991,13 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   if (!rand_plans && !with_det) return set_error(RBC_EVALUE, "no product requested");
   RBC_TRY(check_device());
   if (T == 0 || N == 0) return RBC_OK;
-  // RBC_E2E_HOST_TRACE=1: host-side phase times of the call (setup, plan
-  // upload, enqueue, wait for the results) on stderr
-  static const bool htrace = [] {
-    const char* v = getenv("RBC_E2E_HOST_TRACE");
-    return v && v[0] == '1';
-  }();
-  using hclock = std::chrono::steady_clock;
-  const hclock::time_point h0 = hclock::now();
-  hclock::time_point h1 = h0, h2 = h0, h3 = h0;
   const size_t es = dtype_size(dtype);
   const size_t N2 = (size_t)N * N;
   const size_t db = (size_t)Q * RBC_PLAN_BYTES;
   std::lock_guard<std::mutex> lock(arena().mu);
-  // chunk size: ~8 chunks, shrunk until two input slots + workspace fit
   // pipeline chunks: about 8 MB of operands per chunk, at most 16 (config 2
   // with two compute streams: 12 chunks 11.21 ms per call, 16: 11.20, 32:
-  // 11.4 -- the PCIe copies, 472 MB at 44-52 GB/s, are the critical path);
-  // RBC_E2E_CHUNKS overrides
+  // 11.4); RBC_E2E_CHUNKS overrides
   static const int forced_chunks = [] {
     const char* v = getenv("RBC_E2E_CHUNKS");
     return v ? atoi(v) : 0;
@@ -888,29 +1008,11 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
                                                     1, (int64_t)(2 * T * N2 * es >> 23)));
   int64_t C = std::max<int64_t>(1, (T + nchunks - 1) / nchunks);
   if (C > 8) C = (C + 7) / 8 * 8;  // whole multiples of 8 trials keep grids regular
-  // RBC_E2E_RAMP (tuning aid): 1 = a 16, 32, ... ramp, then chunks of 2C;
-  // 2 = the ramp, then chunks of C
-  static const int ramp = [] {
-    const char* v = getenv("RBC_E2E_RAMP");
-    return v ? atoi(v) : 0;
-  }();
-  if (ramp == 1) C *= 2;
   // Two compute streams pay off for many small chunks (config 2: 1000 pairs
   // of 243); products of 512 and up are whole-GPU jobs per chunk, and their
   // truth scratch comes from the stream-ordered pool, which two streams
   // fragment (config 4 calls went from 24 to 24-80 ms): one stream there.
-  static const int forced_streams = [] {  // RBC_E2E_STREAMS=1/2 (tuning aid)
-    const char* v = getenv("RBC_E2E_STREAMS");
-    return v ? atoi(v) : 0;
-  }();
-  const bool two = forced_streams ? forced_streams == 2 : N < 512;
-  // input slots: copies run ahead of the compute streams by kSlots - 2
-  // chunks (RBC_E2E_SLOTS, 3..7)
-  static const int forced_slots = [] {
-    const char* v = getenv("RBC_E2E_SLOTS");
-    return v ? atoi(v) : 0;
-  }();
-  const int kSlots = forced_slots >= 3 && forced_slots <= kMaxSlots ? forced_slots : 3;
+  const bool two = N < 512;
   auto need = [&](int64_t c) {
     const size_t slot = 2 * align_up(c * N2 * es) + align_up(c * Q * RBC_PLAN_BYTES);
     return kSlots * slot + align_up(db) + 2 * align_up(T * 8) + 2 * align_up(T) + 4096 +
@@ -919,7 +1021,7 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   // The device memory query runs only when the arena must grow: in steady
   // state an earlier call's arena already holds this chunking, and
   // cudaMemGetInfo can stall the host for tens of ms behind concurrent
-  // driver queries (NVML polling; RBC_E2E_HOST_TRACE showed 31 and 97 ms
+  // driver queries (NVML polling; a host phase trace showed 31 and 97 ms
   // "setup" phases in 30 calls).
   if (need(C) > arena().cap) {
     size_t free_b = 0, total_b = 0;
@@ -930,23 +1032,9 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   }
   RBC_TRY(arena().reserve(need(C) + 256));
   Arena& A = arena();
-  {
-    static unsigned graphs_gen = 0;
-    if (graphs_gen != A.gen) {  // graphs of an earlier allocation: stale
-      drop_chunk_graphs();
-      graphs_gen = A.gen;
-    }
-  }
-  // RBC_E2E_GRAPHS=1 (tuning aid): replay each chunk's compute as a CUDA
-  // graph.  Measured equal (c2 10.54 vs 10.50 ms per call, c1 1.25 both):
-  // launch gaps are not what makes chunked compute slower than one step
-  static const bool graphs = [] {
-    const char* v = getenv("RBC_E2E_GRAPHS");
-    return v && v[0] == '1';
-  }();
-  void* da[kMaxSlots];
-  void* dbb[kMaxSlots];
-  void* dpl[kMaxSlots];
+  void* da[kSlots];
+  void* dbb[kSlots];
+  void* dpl[kSlots];
   for (int k = 0; k < kSlots; ++k) {
     da[k] = A.take(C * N2 * es);
     dbb[k] = A.take(C * N2 * es);
@@ -962,46 +1050,18 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   cudaStream_t scs[2] = {host_stream(0), host_stream(1)};
   cudaStream_t sc = scs[0];
   cudaStream_t sx = copy_stream(0);
-  // RBC_E2E_COPY_STREAMS=2: B (and plans) on a second copy stream (tuning aid)
-  static const bool two_copy = [] {
-    const char* v = getenv("RBC_E2E_COPY_STREAMS");
-    return v && atoi(v) == 2;
-  }();
-  cudaStream_t sx2 = two_copy ? copy_stream(1) : sx;
   std::vector<PlanLevel> ident(Q);
   for (int q = 0; q < Q; ++q) {
     memset(&ident[q], 0, sizeof(PlanLevel));
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < n; ++j) ident[q].perm[i][j] = ident[q].inv[i][j] = (int8_t)j;
   }
-  h1 = hclock::now();
-  CUDA_TRY(cudaMemcpyAsync(ddet, ident.data(), db, cudaMemcpyHostToDevice, sc));
-  h2 = hclock::now();
-  CUDA_TRY(cudaEventRecord(pipe_event(15), sc));
-  CUDA_TRY(cudaStreamWaitEvent(scs[1], pipe_event(15), 0));
-  static const bool trace = [] {
-    const char* v = getenv("RBC_E2E_TRACE");
-    return v && v[0] == '1';
-  }();
-  cudaEvent_t tr0 = nullptr;
-  std::vector<cudaEvent_t> tr_copy, tr_comp;
-  if (trace) {
-    cudaEventCreate(&tr0);
-    cudaEventRecord(tr0, sx);
-  }
-  int64_t k = 0;
   // Chunk sizes: C, ..., C, then the remainder cut in halves (multiples of
   // 8): the copies are the critical path (PCIe), so after the last copy only
   // a small chunk is left to compute.
   std::vector<int64_t> sizes;
   {
     int64_t rem = T;
-    if (ramp && C >= 32) {  // 16, 32, ... up to C
-      for (int64_t r = 16; r < C && rem > 2 * r; r *= 2) {
-        sizes.push_back(r);
-        rem -= r;
-      }
-    }
     while (rem > C) {
       sizes.push_back(C);
       rem -= C;
@@ -1013,107 +1073,54 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
     }
     if (rem > 0) sizes.push_back(rem);
   }
-  for (int64_t t0 = 0; k < (int64_t)sizes.size(); t0 += sizes[k], ++k) {
-    const int64_t nt = sizes[k];
-    const int slot = (int)(k % kSlots);
-    cudaStream_t sk = scs[two ? (k & 1) : 0];
-    cudaEvent_t copied = pipe_event(slot), computed = pipe_event(kSlots + slot);
-    if (k >= kSlots) {  // slot free again
-      CUDA_TRY(cudaStreamWaitEvent(sx, computed, 0));
-      if (two_copy) CUDA_TRY(cudaStreamWaitEvent(sx2, computed, 0));
+  auto enqueue = [&]() -> int {
+    CUDA_TRY(cudaMemcpyAsync(ddet, ident.data(), db, cudaMemcpyHostToDevice, sc));
+    CUDA_TRY(cudaEventRecord(pipe_event(2 * kSlots), sc));
+    CUDA_TRY(cudaStreamWaitEvent(scs[1], pipe_event(2 * kSlots), 0));
+    int64_t t0 = 0;
+    for (int64_t k = 0; k < (int64_t)sizes.size(); t0 += sizes[k], ++k) {
+      const int64_t nt = sizes[k];
+      const int slot = (int)(k % kSlots);
+      cudaStream_t sk = scs[two ? (k & 1) : 0];
+      cudaEvent_t copied = pipe_event(slot), computed = pipe_event(kSlots + slot);
+      if (k >= kSlots) CUDA_TRY(cudaStreamWaitEvent(sx, computed, 0));  // slot free again
+      CUDA_TRY(cudaMemcpyAsync(da[slot], (const char*)a + t0 * N2 * es, nt * N2 * es,
+                               cudaMemcpyHostToDevice, sx));
+      CUDA_TRY(cudaMemcpyAsync(dbb[slot], (const char*)b + t0 * N2 * es, nt * N2 * es,
+                               cudaMemcpyHostToDevice, sx));
+      if (rand_plans)
+        CUDA_TRY(cudaMemcpyAsync(dpl[slot], (const char*)rand_plans + t0 * Q * RBC_PLAN_BYTES,
+                                 nt * Q * RBC_PLAN_BYTES, cudaMemcpyHostToDevice, sx));
+      CUDA_TRY(cudaEventRecord(copied, sx));
+      CUDA_TRY(cudaStreamWaitEvent(sk, copied, 0));
+      RBC_TRY(rbc_error_trials_async(dtype, formula, Q, nt, N, da[slot], dbb[slot],
+                                     rand_plans ? dpl[slot] : nullptr, with_det ? ddet : nullptr,
+                                     derr_r + t0, derr_d + t0, dnf_r + t0, dnf_d + t0,
+                                     dws[two ? (k & 1) : 0], ws, sk));
+      CUDA_TRY(cudaEventRecord(computed, sk));
     }
-    CUDA_TRY(cudaMemcpyAsync(da[slot], (const char*)a + t0 * N2 * es, nt * N2 * es,
-                             cudaMemcpyHostToDevice, sx));
-    CUDA_TRY(cudaMemcpyAsync(dbb[slot], (const char*)b + t0 * N2 * es, nt * N2 * es,
-                             cudaMemcpyHostToDevice, sx2));
-    if (rand_plans)
-      CUDA_TRY(cudaMemcpyAsync(dpl[slot], (const char*)rand_plans + t0 * Q * RBC_PLAN_BYTES,
-                               nt * Q * RBC_PLAN_BYTES, cudaMemcpyHostToDevice, sx2));
-    if (two_copy) {
-      CUDA_TRY(cudaEventRecord(pipe_event(14), sx2));
-      CUDA_TRY(cudaStreamWaitEvent(sx, pipe_event(14), 0));
+    CUDA_TRY(cudaEventRecord(pipe_event(2 * kSlots), scs[1]));
+    CUDA_TRY(cudaStreamWaitEvent(sc, pipe_event(2 * kSlots), 0));
+    if (rand_plans) {
+      CUDA_TRY(cudaMemcpyAsync(err_rand, derr_r, T * 8, cudaMemcpyDeviceToHost, sc));
+      if (nf_rand) CUDA_TRY(cudaMemcpyAsync(nf_rand, dnf_r, T, cudaMemcpyDeviceToHost, sc));
     }
-    CUDA_TRY(cudaEventRecord(copied, sx));
-    if (trace) {
-      tr_copy.emplace_back();
-      cudaEventCreate(&tr_copy.back());
-      cudaEventRecord(tr_copy.back(), sx);
+    if (with_det) {
+      CUDA_TRY(cudaMemcpyAsync(err_det, derr_d, T * 8, cudaMemcpyDeviceToHost, sc));
+      if (nf_det) CUDA_TRY(cudaMemcpyAsync(nf_det, dnf_d, T, cudaMemcpyDeviceToHost, sc));
     }
-    CUDA_TRY(cudaStreamWaitEvent(sk, copied, 0));
-    {
-      const void* pr = rand_plans ? dpl[slot] : nullptr;
-      const void* pd = with_det ? ddet : nullptr;
-      void* wsp = dws[two ? (k & 1) : 0];
-      if (graphs) {
-        // the chunk's compute as a CUDA graph, captured on first use and
-        // replayed by later calls (the arena keeps every pointer stable)
-        const GraphKey key = {(uintptr_t)sk, (uintptr_t)dtype, (uintptr_t)formula, (uintptr_t)Q,
-                              (uintptr_t)nt, (uintptr_t)N, (uintptr_t)da[slot],
-                              (uintptr_t)dbb[slot], (uintptr_t)pr, (uintptr_t)pd,
-                              (uintptr_t)(derr_r + t0), (uintptr_t)(derr_d + t0),
-                              (uintptr_t)(dnf_r + t0), (uintptr_t)(dnf_d + t0), (uintptr_t)wsp,
-                              (uintptr_t)ws};
-        auto it = chunk_graphs().find(key);
-        if (it == chunk_graphs().end()) {
-          cudaGraph_t gr = nullptr;
-          CUDA_TRY(cudaStreamBeginCapture(sk, cudaStreamCaptureModeThreadLocal));
-          const int rc = rbc_error_trials_async(dtype, formula, Q, nt, N, da[slot], dbb[slot], pr,
-                                                pd, derr_r + t0, derr_d + t0, dnf_r + t0,
-                                                dnf_d + t0, wsp, ws, sk);
-          const cudaError_t ce = cudaStreamEndCapture(sk, &gr);
-          if (rc != RBC_OK) return rc;
-          if (ce != cudaSuccess) return fail_cuda(ce, "capture (host-buffer chunk)", __FILE__, __LINE__);
-          cudaGraphExec_t ex = nullptr;
-          const cudaError_t ie = cudaGraphInstantiate(&ex, gr, 0);
-          cudaGraphDestroy(gr);
-          if (ie != cudaSuccess) return fail_cuda(ie, "graph instantiate", __FILE__, __LINE__);
-          it = chunk_graphs().emplace(key, ex).first;
-        }
-        CUDA_TRY(cudaGraphLaunch(it->second, sk));
-      } else {
-        RBC_TRY(rbc_error_trials_async(dtype, formula, Q, nt, N, da[slot], dbb[slot], pr, pd,
-                                       derr_r + t0, derr_d + t0, dnf_r + t0, dnf_d + t0, wsp, ws,
-                                       sk));
-      }
-    }
-    CUDA_TRY(cudaEventRecord(computed, sk));
-    if (trace) {
-      tr_comp.emplace_back();
-      cudaEventCreate(&tr_comp.back());
-      cudaEventRecord(tr_comp.back(), sk);
-    }
-  }
-  CUDA_TRY(cudaEventRecord(pipe_event(15), scs[1]));
-  CUDA_TRY(cudaStreamWaitEvent(sc, pipe_event(15), 0));
-  h3 = hclock::now();
-  if (trace) {  // RBC_E2E_TRACE=1: per-chunk copy / compute completion times
-    CUDA_TRY(cudaStreamSynchronize(sc));
-    for (size_t i = 0; i < tr_copy.size(); ++i) {
-      float c = 0.f, g = 0.f;
-      cudaEventElapsedTime(&c, tr0, tr_copy[i]);
-      cudaEventElapsedTime(&g, tr0, tr_comp[i]);
-      fprintf(stderr, "e2e chunk %zu: copied %.3f ms, computed %.3f ms\n", i, c, g);
-      cudaEventDestroy(tr_copy[i]);
-      cudaEventDestroy(tr_comp[i]);
-    }
-    cudaEventDestroy(tr0);
-  }
-  if (rand_plans) {
-    CUDA_TRY(cudaMemcpyAsync(err_rand, derr_r, T * 8, cudaMemcpyDeviceToHost, sc));
-    if (nf_rand) CUDA_TRY(cudaMemcpyAsync(nf_rand, dnf_r, T, cudaMemcpyDeviceToHost, sc));
-  }
-  if (with_det) {
-    CUDA_TRY(cudaMemcpyAsync(err_det, derr_d, T * 8, cudaMemcpyDeviceToHost, sc));
-    if (nf_det) CUDA_TRY(cudaMemcpyAsync(nf_det, dnf_d, T, cudaMemcpyDeviceToHost, sc));
-  }
-  CUDA_TRY(cudaStreamSynchronize(sc));
-  if (htrace) {
-    auto ms = [](hclock::time_point a, hclock::time_point b) {
-      return std::chrono::duration<double, std::milli>(b - a).count();
-    };
-    fprintf(stderr, "e2e host: setup %.3f ms, plan upload %.3f, enqueue %.3f, wait %.3f (total %.3f)\n",
-            ms(h0, h1), ms(h1, h2), ms(h2, h3), ms(h3, hclock::now()), ms(h0, hclock::now()));
-  }
+    return RBC_OK;
+  };
+  const int rc = enqueue();
+  // On success and on failure alike, nothing that reads the caller's host
+  // buffers or the arena may still be queued when the arena lock is released.
+  const cudaError_t e0 = cudaStreamSynchronize(sx);
+  const cudaError_t e1 = cudaStreamSynchronize(scs[1]);
+  const cudaError_t e2 = cudaStreamSynchronize(sc);
+  if (rc != RBC_OK) return rc;
+  if (e0 != cudaSuccess) return fail_cuda(e0, "copy stream", __FILE__, __LINE__);
+  if (e1 != cudaSuccess) return fail_cuda(e1, "compute stream", __FILE__, __LINE__);
+  if (e2 != cudaSuccess) return fail_cuda(e2, "compute stream", __FILE__, __LINE__);
   return RBC_OK;
 }
 

@@ -148,4 +148,25 @@ cudaError_t launch_nonfinite(int dtype, int64_t T, int64_t N2, const void* x, ui
 // the expansion levels of each trial chunk, before the leaves / fused subtree.
 void set_expanded_event(cudaEvent_t ev);
 
+// ---- diagonal rescaling (rescale.cu; reference rescale.py:36-99) ----------
+// Maxima of |x| (N x N, mode dtype) along rows (axis 1) or columns (axis 0)
+// into out (N, mode dtype); *zero set to 1 when one is 0.  scratch: at least
+// absmax_scratch_bytes(N) bytes.
+size_t absmax_scratch_bytes(int64_t N);
+cudaError_t launch_absmax(int dtype, const void* x, int64_t N, int axis, void* out, uint8_t* zero,
+                          void* scratch, cudaStream_t st);
+// out = fl(1 / d)
+cudaError_t launch_recip(int dtype, const void* d, int64_t N, void* out, cudaStream_t st);
+// d = fl(sqrt(fl(bmax / amax))), rd = fl(1 / d)
+cudaError_t launch_inside_factors(int dtype, const void* bmax, const void* amax, int64_t N,
+                                  void* d, void* rd, cudaStream_t st);
+// In place: for s in order, x[i][j] = fl(row_s[i] * x[i][j]), then
+// x[i][j] = fl(x[i][j] * col_s[j]) (null vectors skipped).
+struct ScaleList {
+  const void* row[8];
+  const void* col[8];
+  int n;
+};
+cudaError_t launch_scale(int dtype, void* x, int64_t N, const ScaleList& sl, cudaStream_t st);
+
 }  // namespace rbc

@@ -936,15 +936,19 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
   }
 }
 
-// binary32 leaves, issue-bound like binary16 (FMUL and FADD each take an
-// issue slot): 16-byte operand vectors (K, N multiples of 4), transposed A
-// tile, float4 fragments, and a k loop with no per-step guards -- the K tail
-// of the last tile runs a separate loop.  Same chains as leaf_tiled_kernel.
+// binary32 leaves, issue-bound (the exact-order chain needs a separately
+// rounded multiply and add per step): 16-byte operand vectors (K, N
+// multiples of 4), transposed A tile, float4 fragments, a k loop with no
+// per-step guards -- the K tail of the last tile runs a separate loop -- and
+// packed accumulators: each FFMA2 (rounded multiply, common.cuh) and FADD2
+// covers two outputs of a row, the A element broadcast, so a k step of an
+// 8 x 8 fragment issues 64 FP instructions instead of 128.  Same chains as
+// leaf_tiled_kernel.
 template <int BM, int BN, int BK, int TM, int TN, int MINB>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
     leaf_f32v_kernel(int M, int K, int N, const float* __restrict__ x, int64_t xs,
                      const float* __restrict__ y, int64_t ys, float* __restrict__ out,
-                     int tiles_n) {
+                     int tiles_n, uint64_t negz) {
   constexpr int DY = BM / TM, DX = BN / TN;
   constexpr int NT = DY * DX;
   constexpr int AV = BM * BK / 4 / NT;  // float4 vectors per thread per tile
@@ -997,9 +1001,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
       *reinterpret_cast<float4*>(&Bs[buf][kk][nn]) = rb[q];
     }
   };
-  float acc[TM][TN];
+  uint64_t acc[TM][TN / 2];  // (acc[i][2j], acc[i][2j+1]) packed
   auto kstep = [&](const float* arow, const float* brow, bool first) {
-    float a[TM], bb[TN];
+    float a[TM];
+    uint64_t bb[TN / 2];
 #pragma unroll
     for (int g = 0; g < TM / 4; ++g) {
       const float4 v = *reinterpret_cast<const float4*>(arow + g * DY * 4);
@@ -1008,18 +1013,20 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
 #pragma unroll
     for (int g = 0; g < TN / 4; ++g) {
       const float4 v = *reinterpret_cast<const float4*>(brow + g * DX * 4);
-      bb[4 * g] = v.x; bb[4 * g + 1] = v.y; bb[4 * g + 2] = v.z; bb[4 * g + 3] = v.w;
+      bb[2 * g] = f2_pack(v.x, v.y);
+      bb[2 * g + 1] = f2_pack(v.z, v.w);
     }
     if (first) {
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = __fmul_rn(a[i], bb[j]);
+        for (int j = 0; j < TN / 2; ++j) acc[i][j] = f2_mul_bcast(a[i], bb[j], negz);
     } else {
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], bb[j]));
+        for (int j = 0; j < TN / 2; ++j)
+          acc[i][j] = f2_add(acc[i][j], f2_mul_bcast(a[i], bb[j], negz));
     }
   };
   const int ktiles = (K + BK - 1) / BK;
@@ -1061,14 +1068,16 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
 #pragma unroll
       for (int gj = 0; gj < TN / 4; ++gj) {
         const int gn = n0 + gj * DX * 4 + tx * 4;
-        const int i = gi * 4 + v, j = gj * 4;
+        const int i = gi * 4 + v, j = gj * 2;
+        const float o4[4] = {f2_lo(acc[i][j]), f2_hi(acc[i][j]), f2_lo(acc[i][j + 1]),
+                             f2_hi(acc[i][j + 1])};
         if (gn + 4 <= N) {
           *reinterpret_cast<float4*>(&ob[(int64_t)gm * N + gn]) =
-              make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+              make_float4(o4[0], o4[1], o4[2], o4[3]);
         } else {
 #pragma unroll
           for (int w = 0; w < 4; ++w)
-            if (gn + w < N) ob[(int64_t)gm * N + gn + w] = acc[i][j + w];
+            if (gn + w < N) ob[(int64_t)gm * N + gn + w] = o4[w];
         }
       }
     }
@@ -1087,14 +1096,14 @@ cudaError_t run_f32v(int64_t batch, int64_t M, int64_t K, int64_t N, const void*
       dim3 grid(tiles_m * tiles_n, 65535, (unsigned)(full / 65535));
       leaf_f32v_kernel<BM, BN, BK, TM, TN, MINB><<<grid, NT, 0, st>>>(
           (int)M, (int)K, (int)N, (const float*)x + b0 * xs, xs, (const float*)y + b0 * ys, ys,
-          (float*)out + b0 * M * N, tiles_n);
+          (float*)out + b0 * M * N, tiles_n, kF2NegZero);
     }
     if (nb > full) {
       dim3 grid(tiles_m * tiles_n, (unsigned)(nb - full), 1);
       const int64_t bb = b0 + full;
       leaf_f32v_kernel<BM, BN, BK, TM, TN, MINB><<<grid, NT, 0, st>>>(
           (int)M, (int)K, (int)N, (const float*)x + bb * xs, xs, (const float*)y + bb * ys, ys,
-          (float*)out + bb * M * N, tiles_n);
+          (float*)out + bb * M * N, tiles_n, kF2NegZero);
     }
     b0 += nb;
   }
@@ -1308,7 +1317,8 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
   }
   if (dtype_out == kF32 && dtype_in == kF32) {
     const bool vec = K % 4 == 0 && N % 4 == 0 && (xs % 4 == 0 || batch == 1) &&
-                     (ys % 4 == 0 || batch == 1) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
+                     (ys % 4 == 0 || batch == 1) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
+                     ((uintptr_t)out % 16 == 0);
     const int forced = tile_override();
     if (vec && M >= 128 && N >= 128 && (forced == 0 || forced == 501))
       return run_f32v<128, 128, 8, 8, 8, 2>(batch, M, K, N, x, xs, y, ys, out, st);
@@ -1327,7 +1337,8 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
   if (dtype_out == kF16 && dtype_in == kF16) {
     // 16-byte operand vectors need K, N multiples of 8 and aligned strides
     const bool vec = K % 8 == 0 && N % 8 == 0 && (xs % 8 == 0 || batch == 1) &&
-                     (ys % 8 == 0 || batch == 1) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
+                     (ys % 8 == 0 || batch == 1) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
+                     ((uintptr_t)out % 16 == 0);
     const int forced = tile_override();
     if (vec && M >= 128 && N >= 128 && (forced == 0 || forced == 401))
       return run_h2dup<128, 128, 16, 8, 16, 3>(batch, M, K, N, x, xs, y, ys, out, st);

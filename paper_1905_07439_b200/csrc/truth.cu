@@ -252,14 +252,18 @@ int truth_group() {
 constexpr size_t kSmem = sizeof(double) * kStages * kBK * (kBM + kBN) + 2 * sizeof(uint64_t) * kStages;
 
 // The stream-ordered pool keeps freed scratch for reuse instead of returning
-// it to the driver at every synchronisation.
+// it to the driver at every synchronisation -- up to 4 GiB (two launches'
+// worth of the <= 2 GiB scratch below; anything above is released at the
+// next synchronisation).  The host-buffer calls size their arenas to 85% of
+// free + arena memory (engine.cu host_ws_budget / rbc_error_trials), so the
+// retained scratch always fits in the remaining 15% (27 GB on a B200).
 cudaError_t keep_pool(int device) {
   static int done = -1;
   if (done == device) return cudaSuccess;
   cudaMemPool_t pool;
   cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
   if (e != cudaSuccess) return e;
-  uint64_t keep = UINT64_MAX;
+  uint64_t keep = (uint64_t)4 << 30;
   e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   if (e == cudaSuccess) done = device;
   return e;

@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["shard", "pair_ids", "max_over_ranks", "gather_trials", "trial_stats"]
+__all__ = ["shard", "pair_ids", "barrier_if", "max_over_ranks", "gather_trials", "trial_stats"]
 
 
 def shard(rank: int, world: int, per_rank: int):
@@ -28,6 +28,14 @@ def shard(rank: int, world: int, per_rank: int):
 def pair_ids(rank: int, world: int, per_rank: int):
     first, count = shard(rank, world, per_rank)
     return list(range(first, first + count))
+
+
+def barrier_if(world: int, group=None) -> None:
+    """Barrier across the ranks when running distributed (no-op at world 1)."""
+    import torch.distributed as dist
+
+    if world > 1 and dist.is_available() and dist.is_initialized():
+        dist.barrier(group=group)
 
 
 def max_over_ranks(values, device=None, group=None):

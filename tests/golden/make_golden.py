@@ -13,8 +13,8 @@ Outputs (committed):
       perturb / generate outputs, pinning the host-side mirror
   experiments_tiny.csv                   -- ``run_experiment`` records of small
       s2_variants / s1_dist configs (bitwise reproducible from the seed layout)
-  s2_variants_320_subset.csv             -- the gaussian and adv1 rows of the
-      reference artifact pkg/artifacts/s2-variants-320.csv (seed 1)
+  s2_variants_320.csv                    -- the whole reference artifact
+      pkg/artifacts/s2-variants-320.csv (seed 1, all six families, 9066 rows)
 
 binary16 goes through the unmodified reference engine with this package's
 duck-typed HALF mode (parity against the reference is unpinned
@@ -252,10 +252,10 @@ def main():
     recs += run_experiment(cfg)
     (HERE / "experiments_tiny.csv").write_text(format_csv(recs))
 
-    # ---- artifact subset
+    # ---- the reference artifact (whole)
     src = Path("/root/reference/pkg/artifacts/s2-variants-320.csv").read_text().splitlines()
     # the whole artifact: all six matrix families (9066 rows)
-    (HERE / "s2_variants_320_subset.csv").write_text("\n".join(src) + "\n")
+    (HERE / "s2_variants_320.csv").write_text("\n".join(src) + "\n")
     keep = src
     print(f"engine cases: {len(meta['engine'])}, leaf cases: {len(meta['leaf'])}, "
           f"experiment rows: {len(recs)}, artifact rows: {len(keep) - 1}")

@@ -285,3 +285,26 @@ def test_subtree_leaf_exchange_variants_agree(tmp_path, label):
         outs[rot] = np.load(path)
     assert outs["2"].tobytes() == outs["0"].tobytes()
     assert outs["2"].tobytes() == outs["1"].tobytes()
+
+
+@pytest.mark.parametrize("detect", ["0", "1"])
+def test_empty_operands_after_nonempty_call(eng, monkeypatch, detect):
+    """(T, 0, 0) operands return an empty (T, 0, 0) array like the reference,
+    also right after a non-empty call left operand bytes in the arena where
+    the overflow flags of the empty call land (engine.cu run_pass)."""
+    from paper_1905_07439_b200 import SINGLE, strassen_formula
+    from paper_1905_07439_b200.multiply import mode_tensors
+
+    monkeypatch.setenv("RBC_DETECT_PLANS", detect)
+    f = strassen_formula()
+    levels = [mode_tensors(f, SINGLE)] * 2
+    rng = np.random.default_rng(5)
+    # non-empty call whose operands are far from zero bytes
+    a = np.full((1, 64, 64), 3.0e38, np.float32) * rng.choice([-1, 1], (1, 64, 64)).astype(np.float32)
+    b = np.ones((1, 64, 64), np.float32)
+    with pytest.raises(OverflowError):
+        eng.apply_levels(levels, a, b, SINGLE)
+    for T in (1, 3):
+        e = np.zeros((T, 0, 0), np.float32)
+        out = eng.apply_levels(levels, e, e, SINGLE)
+        assert out.shape == (T, 0, 0) and out.dtype == np.float32

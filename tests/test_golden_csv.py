@@ -18,7 +18,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-GOLDEN = Path(__file__).resolve().parent / "golden" / "s2_variants_320_subset.csv"
+GOLDEN = Path(__file__).resolve().parent / "golden" / "s2_variants_320.csv"
 RTOL = 1e-12
 VARIANT = {"full_random": "full", "sign_only": "sign", "perm_only": "perm"}
 

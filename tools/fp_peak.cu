@@ -104,6 +104,46 @@ __global__ void __launch_bounds__(256) dfma_kernel(double* out, float seed) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// Packed binary32 pairs (sm_100a FMUL2/FADD2 family).  ptxas contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even with -fmad=false, so the
+// multiply is issued as FFMA2 with an addend of (-0, -0) the compiler cannot
+// see (a kernel argument): fl(a*b + -0) == fl(a*b) for every a, b (a +0
+// product stays +0, a -0 product stays -0).  One FFMA2 + one FADD2 per two
+// separately rounded multiply-adds.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 f2_mul(u64 a, u64 b, u64 negz) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(negz));
+  return r;
+}
+__device__ __forceinline__ u64 f2_add(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__global__ void __launch_bounds__(256) mac2_kernel(u64* out, float seed, u64 negz) {
+  u64 acc[kChains], a[kChains];
+  const float bf = 1.0f - seed * 1e-6f;
+  const u64 b = ((u64)__float_as_uint(bf) << 32) | __float_as_uint(bf);
+#pragma unroll
+  for (int i = 0; i < kChains; ++i) {
+    acc[i] = 0;
+    float x = 1.0f + threadIdx.x * 1e-3f + i * 1e-4f;
+    a[i] = ((u64)__float_as_uint(x) << 32) | __float_as_uint(x);
+  }
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) {
+      a[i] = f2_mul(a[i], b, negz);
+      acc[i] = f2_add(acc[i], a[i]);
+    }
+  }
+  u64 s = acc[0];
+#pragma unroll
+  for (int i = 1; i < kChains; ++i) s = f2_add(s, acc[i]);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <class K>
 double time_kernel(K launch, int reps) {
   cudaEvent_t e0, e1;
@@ -136,18 +176,20 @@ int main() {
   double f16 = time_kernel([&] { mac_kernel<__half2><<<blocks, threads>>>((__half2*)buf, 1.f); }, 5);
   double fma = time_kernel([&] { ffma_kernel<<<blocks, threads>>>((float*)buf, 1.f); }, 5);
   double dfma = time_kernel([&] { dfma_kernel<<<blocks, threads>>>((double*)buf, 1.f); }, 5);
+  double f32x2 = time_kernel(
+      [&] { mac2_kernel<<<blocks, threads>>>((u64*)buf, 1.f, 0x8000000080000000ull); }, 5);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "CUDA error %s\n", cudaGetErrorString(e));
     return 1;
   }
   printf("{\"f32_tflops\": %.3f, \"f64_tflops\": %.3f, \"f16_tflops\": %.3f, "
-         "\"ffma_f32_tflops\": %.3f, \"dfma_f64_tflops\": %.3f, \"sms\": %d, "
+         "\"ffma_f32_tflops\": %.3f, \"dfma_f64_tflops\": %.3f, \"f32x2_tflops\": %.3f, \"sms\": %d, "
          "\"how\": \"tools/fp_peak.cu: %d x 256 threads, 16 independent acc=add(acc,mul(a,b)) chains "
          "with separately rounded multiply and add (half2 counts 4 flops), best of 5, CUDA events\"}\n",
          ops * Ops<float>::flops_per_op / (f32 * 1e-3) / 1e12,
          ops * Ops<double>::flops_per_op / (f64 * 1e-3) / 1e12,
          ops * Ops<__half2>::flops_per_op / (f16 * 1e-3) / 1e12, ops * 2.0 / (fma * 1e-3) / 1e12,
-         ops * 2.0 / (dfma * 1e-3) / 1e12, sms, blocks);
+         ops * 2.0 / (dfma * 1e-3) / 1e12, ops * 4.0 / (f32x2 * 1e-3) / 1e12, sms, blocks);
   return 0;
 }
