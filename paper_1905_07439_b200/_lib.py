@@ -51,6 +51,7 @@ EXPORTS = (
     "rbc_average_trials_async",
     "rbc_sum_trials_async",
     "rbc_matgen",
+    "rbc_rescaled_multiply",
 )
 
 _lock = threading.Lock()
@@ -115,6 +116,11 @@ def _declare(lib):
             [c_int, c_int, P(c_i32), P(c_i32), c_i64, c_i64, c_i64, c_vp, c_vp,
              P(c_vp), P(c_vp), P(c_vp), P(c_vp), P(c_vp), P(c_vp), c_int, P(c_i32),
              c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp],
+        ),
+        "rbc_rescaled_multiply": (
+            c_int,
+            [c_int, c_int, c_int, P(c_i32), P(c_i32), P(c_vp), P(c_vp), P(c_vp), c_int, P(c_i32),
+             c_i64, c_vp, c_vp, c_vp],
         ),
         "rbc_error_trials_async": (
             c_int,

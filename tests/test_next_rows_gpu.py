@@ -1,6 +1,6 @@
-"""GPU: SURVEY §8f "next" rows -- plan-enumeration expectation
-(randomize.py:293-334) and the rescaled 2x O-I baseline (rescale.py:60-99) --
-against the CPU oracle restatement, plus the reference's own invariants."""
+"""GPU: SURVEY §8f "next" row 3 -- plan-enumeration expectation
+(randomize.py:293-334) -- against the CPU oracle restatement, plus the
+reference's own invariants.  Row 2 (rescaling) is tests/test_rescale_gpu.py."""
 
 import itertools
 
@@ -51,31 +51,3 @@ def test_enumerate_expectation_matches_oracle(label, which, size):
         assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-13
 
 
-@pytest.mark.parametrize("label", ["f32", "f64", "f16"])
-def test_rescaled_multiply_matches_oracle(label):
-    import paper_1905_07439_b200 as rbc
-    from paper_1905_07439_b200.multiply import mode_tensors
-    from paper_1905_07439_b200.precision import parse_precision
-    from paper_1905_07439_b200.rescale import DEFAULT_SCHEDULE, INSIDE, OUTSIDE, rescaled_multiply
-
-    mode = parse_precision(label)
-    g = rbc.derive_rng(40)
-    A = mode.array(g.random((32, 32)) + 0.1)
-    B = mode.array(g.random((32, 32)) + 0.1)
-    f = rbc.strassen_formula()
-    for schedule in (DEFAULT_SCHEDULE, (OUTSIDE,), (INSIDE,), ()):
-        got = rescaled_multiply(A, B, 3, schedule, mode)
-        # oracle: identical host scaling, oracle recursion
-        import paper_1905_07439_b200.rescale as rs
-
-        orig = rs.recursive_apply
-        try:
-            rs.recursive_apply = lambda f_, A_, B_, Q_, m_: oracle.apply_levels(
-                [mode_tensors(f_, m_)] * Q_, A_[None], B_[None], m_)[0]
-            want = rescaled_multiply(A, B, 3, schedule, mode)
-        finally:
-            rs.recursive_apply = orig
-        assert np.array_equal(got, want), schedule
-    assert np.array_equal(rescaled_multiply(A, B, 2, (), mode), rbc.recursive_apply(f, A, B, 2, mode))
-    with pytest.raises(ValueError):
-        rescaled_multiply(np.zeros((4, 4)), B[:4, :4], 1, DEFAULT_SCHEDULE, mode)
