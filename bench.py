@@ -84,6 +84,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="eager launches in the timed region")
     ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution run")
     ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in s2-variants run")
+    ap.add_argument("--dump-errors", default="", help="rank 0 writes the gathered per-trial errors (npz)")
     return ap.parse_args()
 
 
@@ -677,13 +678,14 @@ class ErrorTrialWorkload:
     """c1, c2, c4, c5: 2 products per pair (plan path, packed plans)."""
 
     def __init__(self, cfg, pair_ids, A, B, dev, torch):
-        from paper_1905_07439_b200.randomize import pack_recursive_plans
+        from paper_1905_07439_b200.configs import packed_plans
         from paper_1905_07439_b200.trials import DeviceErrorTrials
 
         self.cfg, self.torch = cfg, torch
         self.f = cfg.formula_obj()
         self.A, self.B = A, B
-        self.packed = pack_recursive_plans([cfg.plan(cfg.plan_key(p)) for p in pair_ids], cfg.Q, cfg.n)
+        self.pair_ids = list(pair_ids)
+        self.packed = packed_plans(cfg, [cfg.plan_key(p) for p in pair_ids])
         self.a = torch.from_numpy(A).to(dev)
         self.b = torch.from_numpy(B).to(dev)
         self.pl = torch.from_numpy(self.packed).to(dev)
@@ -734,6 +736,40 @@ class ErrorTrialWorkload:
         h2d = self.A.nbytes + self.B.nbytes + self.packed.nbytes
         d2h = 2 * len(err_r) * 9
         return ms, h2d, d2h
+
+
+    def fresh(self, steps, warmup=2):
+        """Fresh inputs every step: the step's operand pairs drawn on the GPU
+        (rbc_matgen from keys of the native SeedSequence), its plans drawn on
+        the host (native draw_plan) and copied H2D, the error trials run, the
+        per-trial errors copied D2H; wall clock per step.  Pairs continue
+        after the resident set (no pair is reused)."""
+        import torch
+
+        from paper_1905_07439_b200.configs import make_pairs_device, packed_plans
+
+        cfg, T = self.cfg, len(self.pair_ids)
+        nxt = [self.pair_ids[-1] + 1]
+        dev = self.a.device
+
+        def step():
+            p0 = nxt[0]
+            nxt[0] += T
+            a, b = make_pairs_device(cfg, p0, T, dev)
+            pl = torch.from_numpy(packed_plans(cfg, [cfg.plan_key(p) for p in range(p0, p0 + T)]))
+            self.runner.run(a, b, pl.to(dev, non_blocking=True))
+            return self.runner.err_rand.cpu(), self.runner.err_det.cpu()
+
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        with no_gc():
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                step()
+            torch.cuda.synchronize()
+            ms = (time.perf_counter() - t0) / steps * 1e3
+        return ms
 
 
 class AverageWorkload:
@@ -801,20 +837,29 @@ class AverageWorkload:
 def device_inputs(cfg, first, T, A, B, host_s, workers):
     """Informational: the same operand pairs drawn on the GPU (rbc_matgen,
     SURVEY §8f rank 4) -- time and bitwise agreement with the host draw that
-    feeds the timed region."""
+    feeds the timed region.  The first full-size call also pays the one-time
+    allocations (torch's caching allocator growing to the outputs, the
+    generator's word and map buffers), which is what made round 1's single
+    timing vary (671 vs 35-73 ms); the steady figure is the median of three
+    later calls."""
     import torch
 
     from paper_1905_07439_b200.configs import make_pairs_device
 
-    make_pairs_device(cfg, first, min(T, 2))  # warm-up
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    dA, dB = make_pairs_device(cfg, first, T)
-    torch.cuda.synchronize()
-    dev_s = time.perf_counter() - t0
+    make_pairs_device(cfg, first, min(T, 2))  # warm-up (module load, small buffers)
+    times = []
+    for _ in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dA, dB = make_pairs_device(cfg, first, T)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        if len(times) < 4:
+            del dA, dB
     same = (dA.cpu().numpy().tobytes() == A.tobytes() and dB.cpu().numpy().tobytes() == B.tobytes())
     del dA, dB
-    return {"kind": cfg.kind, "device_matgen_ms": round(dev_s * 1e3, 2),
+    return {"kind": cfg.kind, "device_matgen_first_call_ms": round(times[0] * 1e3, 2),
+            "device_matgen_ms": round(statistics.median(times[1:]) * 1e3, 2),
             "host_numpy_ms": round(host_s * 1e3, 1), "host_workers": workers,
             "bitwise_equal": same}
 
@@ -830,12 +875,17 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # RBC_BENCH_BACKEND=gloo: test hook (tests/test_multiprocess_gpu.py) --
+        # ranks share the visible GPUs and the statistics collectives go over
+        # gloo on host tensors; the driver's runs use NCCL, one GPU per rank
+        backend = os.environ.get("RBC_BENCH_BACKEND", "nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group(backend)
     else:
         dist = None
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
+    coll = None if (dist is not None and dist.get_backend() == "gloo") else dev  # collective tensors
     _lib.require_device()
 
     cfg = get_config(args.config)
@@ -910,11 +960,14 @@ def run_ours(args):
         barrier()
         e2e = wl.e2e(args.steps, args.warmup)
 
-    tmax = distributed.max_over_ranks([dev_ms, e2e[0] if e2e else 0.0], device=dev)
+    tmax = distributed.max_over_ranks([dev_ms, e2e[0] if e2e else 0.0], device=coll)
     dev_ms = float(tmax[0])
     allerr = distributed.gather_trials(
-        np.stack([err_r, nf_r.astype(np.float64)]), device=dev)
-    alldet = distributed.gather_trials(np.stack([err_d, nf_d.astype(np.float64)]), device=dev)
+        np.stack([err_r, nf_r.astype(np.float64)]), device=coll)
+    alldet = distributed.gather_trials(np.stack([err_d, nf_d.astype(np.float64)]), device=coll)
+    if args.dump_errors and rank == 0:  # per-trial errors of all ranks, trial order
+        np.savez(args.dump_errors, err_rand=allerr[0], nf_rand=allerr[1], err_det=alldet[0],
+                 nf_det=alldet[1])
 
     flops_step = 2.0 * cfg.N ** 3 * wl.products * world
     value = flops_step / (dev_ms / 1e3) / 1e9
@@ -937,6 +990,17 @@ def run_ours(args):
         me = wl.mean_errors()
         line["errors"]["running_mean_at_G"] = {
             "mean": float(np.nanmean(me[:, -1])), "checkpoints": wl.runner.cps}
+    if hasattr(wl, "fresh") and not args.no_e2e:
+        barrier()
+        fresh_ms = float(distributed.max_over_ranks([wl.fresh(args.steps)], device=coll)[0])
+        line["e2e_fresh_inputs"] = {
+            "value": round(flops_step / (fresh_ms / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+            "ms_per_step": round(fresh_ms, 3),
+            "what": "every step draws new operand pairs on the GPU (rbc_matgen; keys from the "
+                    "native SeedSequence), new plans on the host (native draw_plan, copied H2D), "
+                    "runs the error trials and copies the errors D2H; wall clock",
+            "ratio_to_resident_step": round(fresh_ms / dev_ms, 3),
+        }
     if e2e is not None:
         e2e_ms = float(tmax[1])
         line["e2e"] = {"value": round(flops_step / (e2e_ms / 1e3) / 1e9, 3), "unit": "GFLOP/s",
@@ -953,7 +1017,10 @@ def run_ours(args):
 
     if not args.no_tts and cfg.plans_per_pair == 1:
         barrier()
-        line["time_to_solution"] = time_to_solution(cfg, T, dev, rank, world)
+        line["time_to_solution"] = time_to_solution(cfg, T, dev, rank, world, coll)
+        tts_err = line["time_to_solution"].pop("_errors")
+        if args.dump_errors and rank == 0:
+            np.savez(args.dump_errors + ".tts.npz", err_rand=tts_err[0], err_det=tts_err[1])
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_leg(cfg, first, T, err_r, err_d)
@@ -1032,7 +1099,7 @@ def cpu_baseline_leg(cfg, first, T, err_r, err_d):
     return out
 
 
-def time_to_solution(cfg, T_step, dev, rank, world):
+def time_to_solution(cfg, T_step, dev, rank, world, coll=None):
     """Wall-clock time for the config's whole trial set (e.g. configuration 5:
     all 64 pairs), strong-scaled over the ranks: each rank draws its share of
     the pairs on the GPU (rbc_matgen, bit-identical to the host draw), runs
@@ -1043,7 +1110,7 @@ def time_to_solution(cfg, T_step, dev, rank, world):
 
     from paper_1905_07439_b200 import distributed
     from paper_1905_07439_b200.configs import make_pairs_device
-    from paper_1905_07439_b200.randomize import pack_recursive_plans
+    from paper_1905_07439_b200.configs import packed_plans
     from paper_1905_07439_b200.trials import DeviceErrorTrials
 
     total = cfg.trials
@@ -1055,8 +1122,7 @@ def time_to_solution(cfg, T_step, dev, rank, world):
 
     def chunk(p0, cnt):
         a, b = make_pairs_device(cfg, p0, cnt, dev)
-        packed = pack_recursive_plans([cfg.plan(cfg.plan_key(p)) for p in range(p0, p0 + cnt)],
-                                      cfg.Q, cfg.n)
+        packed = packed_plans(cfg, [cfg.plan_key(p) for p in range(p0, p0 + cnt)])
         pl = torch.from_numpy(packed).to(dev)
         if cnt not in runners:
             runners[cnt] = DeviceErrorTrials(f, cfg.Q, cfg.N, cfg.mode, cnt, device=dev)
@@ -1072,14 +1138,17 @@ def time_to_solution(cfg, T_step, dev, rank, world):
         errs.append(chunk(p0, min(T_step, hi - p0 + 1)))
     torch.cuda.synchronize()
     sec = time.perf_counter() - t0
-    sec = float(distributed.max_over_ranks([sec], device=dev)[0])
+    sec = float(distributed.max_over_ranks([sec], device=coll)[0])
     e = np.concatenate(errs, axis=1)
+    if total % world == 0:  # equal shards: gather in rank (= pair) order
+        e = distributed.gather_trials(e, device=coll)
     return {
         "pairs": total, "products": 2 * total, "seconds": round(sec, 3), "scaling": "strong",
         "n_gpus": world, "pairs_per_launch": T_step,
         "what": "wall clock, all pairs: device input generation, plans, binary64 truth, "
                 "deterministic + randomized products, errors copied to the host (max over ranks)",
-        "err_rand_mean_rank0": float(np.nanmean(e[0])),
+        "err_rand_mean": float(np.nanmean(e[0])), "err_det_mean": float(np.nanmean(e[1])),
+        "_errors": e,
     }
 
 

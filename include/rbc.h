@@ -191,6 +191,24 @@ int rbc_nonfinite_async(int dtype, int64_t T, int64_t N, const void* x, uint8_t*
 int rbc_matgen(int kind, int dtype, int64_t count, int64_t n, const uint64_t* keys,
                const int32_t* which, void* out, uint8_t* nonfinite, void* stream);
 
+/* ---- host seed derivation and plan draws (reference rng.py:20-29,
+ * randomize.py:118-127), numpy's SeedSequence / Philox4x64-10 / bounded-
+ * integer / shuffle algorithms restated in C++ (csrc/hostrng.cu), bit for bit.
+ * Stream i = derive_rng(seeds[i * seed_stride], *paths[i]) (seed_stride 0:
+ * one seed for all), paths: (count, depth) u64 spawn keys.
+ *   rbc_derive_seeds : out[i] = derive_seed(seed_i, *paths[i])
+ *   rbc_philox_keys  : keys[2i], keys[2i+1] = that stream's Philox key
+ *                      (the rbc_matgen input)
+ *   rbc_draw_plans   : perms (count, 3, n) int64 and signs (count, 3, n) f64 of
+ *                      draw_plan(n, derive_rng(seed_i, *paths[i]))
+ * Host only (no device needed); multithreaded for large counts. */
+int rbc_derive_seeds(const uint64_t* seeds, int64_t seed_stride, int depth,
+                     const uint64_t* paths, int64_t count, uint64_t* out);
+int rbc_philox_keys(const uint64_t* seeds, int64_t seed_stride, int depth, const uint64_t* paths,
+                    int64_t count, uint64_t* keys);
+int rbc_draw_plans(int n, const uint64_t* seeds, int64_t seed_stride, int depth,
+                   const uint64_t* paths, int64_t count, int64_t* perms, double* signs);
+
 /* ---- error trials: the per-pair work of the distribution experiments ----
  * (experiments.py:248-261, 327-379): for each trial t with operands
  * (a[t], b[t]) in the mode, ref_t = binary64 inner-product truth, then the

@@ -52,6 +52,9 @@ EXPORTS = (
     "rbc_sum_trials_async",
     "rbc_matgen",
     "rbc_rescaled_multiply",
+    "rbc_derive_seeds",
+    "rbc_philox_keys",
+    "rbc_draw_plans",
 )
 
 _lock = threading.Lock()
@@ -117,6 +120,9 @@ def _declare(lib):
              P(c_vp), P(c_vp), P(c_vp), P(c_vp), P(c_vp), P(c_vp), c_int, P(c_i32),
              c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp],
         ),
+        "rbc_derive_seeds": (c_int, [c_vp, c_i64, c_int, c_vp, c_i64, c_vp]),
+        "rbc_philox_keys": (c_int, [c_vp, c_i64, c_int, c_vp, c_i64, c_vp]),
+        "rbc_draw_plans": (c_int, [c_int, c_vp, c_i64, c_int, c_vp, c_i64, c_vp, c_vp]),
         "rbc_rescaled_multiply": (
             c_int,
             [c_int, c_int, c_int, P(c_i32), P(c_i32), P(c_vp), P(c_vp), P(c_vp), c_int, P(c_i32),

@@ -102,9 +102,26 @@ def get_config(name: str) -> TrialConfig:
 
 
 def pair_seeds(cfg: TrialConfig, first: int, count: int):
-    """Matrix seeds mseed of pairs first..first+count-1 (experiments.py:237-239)."""
-    return [derive_seed(cfg.seed, ROLE_MATRIX, p, kind_index(cfg.kind))
-            for p in range(first, first + count)]
+    """Matrix seeds mseed of pairs first..first+count-1 (experiments.py:237-239),
+    through the native SeedSequence (hostrng; bit-identical to derive_seed)."""
+    from . import hostrng
+
+    k = kind_index(cfg.kind)
+    return [int(x) for x in hostrng.derive_seeds(
+        cfg.seed, [(ROLE_MATRIX, p, k) for p in range(first, first + count)])]
+
+
+def packed_plans(cfg: TrialConfig, keys) -> np.ndarray:
+    """(len(keys), Q, 40) packed plan records of trials ``keys`` (plan of
+    trial t, level q: draw_plan(n, derive_rng(S, ROLE_PLAN, t, q))), drawn by
+    the native host RNG (hostrng: bit-identical to cfg.plan) and packed for
+    the plan kernels."""
+    from . import engine, hostrng
+
+    keys = list(keys)
+    perms, signs = hostrng.draw_plans(
+        cfg.n, cfg.seed, [(ROLE_PLAN, t, q) for t in keys for q in range(cfg.Q)])
+    return engine.pack_plans(cfg.n, perms, signs).reshape(len(keys), cfg.Q, -1)
 
 
 def make_pairs_device(cfg: TrialConfig, first: int, count: int, device="cuda:0"):

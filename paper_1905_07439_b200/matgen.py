@@ -109,7 +109,7 @@ def generate_device(kind: str, size: int, seeds, mode, device="cuda:0", which=(0
 
     import torch
 
-    from . import _lib
+    from . import _lib, hostrng
     from .precision import dtype_code, mode_of
 
     if kind not in MATRIX_KINDS + BUILDER_KINDS:
@@ -128,7 +128,7 @@ def generate_device(kind: str, size: int, seeds, mode, device="cuda:0", which=(0
         flags = torch.zeros(max(1, len(seeds)), dtype=torch.uint8, device=dev)
         for c0 in range(0, len(seeds), 65535):
             part = seeds[c0:c0 + 65535]
-            keys = np.array([philox_key(sd, w) for sd in part], dtype=np.uint64).reshape(-1)
+            keys = hostrng.philox_keys(part, [(w,)] * len(part)).reshape(-1)
             wh = np.full(len(part), w, dtype=np.int32)
             with torch.cuda.device(dev):
                 st = torch.cuda.current_stream(dev).cuda_stream

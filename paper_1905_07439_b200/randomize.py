@@ -255,13 +255,43 @@ def _all_plans(n: int):
         yield RandomizationPlan(np.array([s1, s2, s3]), np.array([p1, p2, p3]))
 
 
+def all_plan_arrays(n: int):
+    """perms (count, 3, n) int64 and signs (count, 3, n) float64 of every plan
+    in the enumeration order of _all_plans (randomize.py:282-290:
+    itertools.product(signs x3, perms x3), the last factor fastest), built
+    with array indexing instead of one RandomizationPlan per plan (110,592
+    objects at n = 3)."""
+    import itertools
+
+    S = np.array(list(itertools.product((1.0, -1.0), repeat=n)))     # (2^n, n)
+    P = np.array(list(itertools.permutations(range(n))), dtype=np.int64)  # (n!, n)
+    ns, npm = len(S), len(P)
+    idx = np.unravel_index(np.arange(plan_count(n)), (ns, ns, ns, npm, npm, npm))
+    signs = np.stack([S[idx[0]], S[idx[1]], S[idx[2]]], axis=1)
+    perms = np.stack([P[idx[3]], P[idx[4]], P[idx[5]]], axis=1)
+    return perms, signs
+
+
+def _hatted_batch(f, perms, signs, m):
+    """plan_levels over plan arrays (the same gathers and exact sign flips)."""
+    c = _rescale_factor(f)
+
+    def hat(t, a, b):
+        g = t[:, perms[:, a][:, :, None], perms[:, b][:, None, :]]
+        g = np.moveaxis(g, 0, 1)
+        return g * (signs[:, a][:, :, None] * signs[:, b][:, None, :])[:, None]
+
+    return m.array(hat(f.u, 0, 1)), m.array(hat(f.v, 1, 2)), m.array(hat(f.w, 0, 2) * c)
+
+
 def enumerate_expectation(f, A, B, mode=DOUBLE, chunk_elements: int = DEFAULT_CHUNK_ELEMENTS,
                           device="cuda:0") -> np.ndarray:
     """Exact expectation of the single-level randomized product over every
     plan (randomize.py:293-334), on the device: plans are evaluated in
     batches and accumulated sequentially in binary64 in enumeration order;
-    the average is total / count.  ``chunk_elements`` bounds the batch the
-    same way as the reference (values never depend on it)."""
+    the average is total / count.  The plan set is built as arrays
+    (all_plan_arrays) and packed per batch; ``chunk_elements`` bounds the
+    batch the same way as the reference (values never depend on it)."""
     import torch
 
     from .multiply import _as_operands, _check_blocked
@@ -283,35 +313,24 @@ def enumerate_expectation(f, A, B, mode=DOUBLE, chunk_elements: int = DEFAULT_CH
     total = torch.zeros(N * N, dtype=torch.float64, device=dev)
     fid = plan_formula_id(f)
     tdt = {np.float64: torch.float64, np.float32: torch.float32, np.float16: torch.float16}[m.dtype]
-    done = 0
-    batch = []
-
-    def flush():
-        nonlocal done
-        if not batch:
-            return
-        T = len(batch)
+    perms, signs = all_plan_arrays(f.n)
+    nf_any = torch.zeros(1, dtype=torch.uint8, device=dev)
+    for c0 in range(0, count, chunk):
+        P, S = perms[c0:c0 + chunk], signs[c0:c0 + chunk]
+        T = len(P)
         out = torch.empty((T, N, N), dtype=tdt, device=dev)
         nf = torch.zeros(T, dtype=torch.uint8, device=dev)
         if fid is not None:
-            packed = pack_recursive_plans([RecursivePlan((p,)) for p in batch], 1, f.n)
+            packed = engine.pack_plans(f.n, P, S).reshape(T, 1, -1)
             eng.apply_plans(fid, 1, torch.from_numpy(packed).to(dev), a, b, out, nf)
         else:
-            lv = [tuple(torch.from_numpy(t).to(dev) for t in plan_levels(f, batch, m))]
+            lv = [tuple(torch.from_numpy(t).to(dev) for t in _hatted_batch(f, P, S, m))]
             eng.apply_levels(lv, a, b, out, nf)
-        if bool(nf.any()):
-            raise OverflowError(f"result left the {m.kind} range")
+        nf_any |= nf.max().reshape(1)
         eng.sum_trials(out, total)
-        done += T
-        batch.clear()
-
-    for plan in _all_plans(f.n):
-        batch.append(plan)
-        if len(batch) >= chunk:
-            flush()
-    flush()
-    assert done == count
     torch.cuda.synchronize(dev)
+    if bool(nf_any.item()):
+        raise OverflowError(f"result left the {m.kind} range")
     return total.cpu().numpy().reshape(N, N) / float(count)
 
 

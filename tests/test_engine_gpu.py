@@ -308,3 +308,4 @@ def test_empty_operands_after_nonempty_call(eng, monkeypatch, detect):
         e = np.zeros((T, 0, 0), np.float32)
         out = eng.apply_levels(levels, e, e, SINGLE)
         assert out.shape == (T, 0, 0) and out.dtype == np.float32
+

@@ -120,3 +120,18 @@ def test_plan_recognition_reproduces_tables(name):
     u, v, w = (t.copy() for t in mode_tensors(f, rbc.DOUBLE))
     u[0, 0, 0, 0] = -u[0, 0, 0, 0] if u[0, 0, 0, 0] else 1.0
     assert match_plans([[u, v, w]]) is None
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_all_plan_arrays_follow_enumeration_order(n):
+    """The array form of the plan enumeration (randomize.all_plan_arrays)
+    equals the reference order of _all_plans (randomize.py:282-290)."""
+    from paper_1905_07439_b200.randomize import _all_plans, all_plan_arrays, plan_count
+
+    perms, signs = all_plan_arrays(n)
+    plans = list(_all_plans(n))
+    assert len(perms) == len(plans) == plan_count(n)
+    step = 1 if n < 3 else 97
+    for i in range(0, len(plans), step):
+        assert np.array_equal(perms[i], plans[i].perms) and np.array_equal(signs[i], plans[i].signs)
+    assert np.array_equal(perms[-1], plans[-1].perms) and np.array_equal(signs[-1], plans[-1].signs)

@@ -51,3 +51,40 @@ def test_enumerate_expectation_matches_oracle(label, which, size):
         assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-13
 
 
+
+
+@pytest.mark.parametrize("label,N", [("f64", 3), ("f32", 6)])
+def test_enumerate_expectation_laderman_110592_plans(label, N):
+    """n = 3 (Laderman, (2^3)^3 (3!)^3 = 110,592 plans, under the reference's
+    10^6 budget, randomize.py:293-334): the device enumeration equals the
+    oracle's sequential binary64 average in enumeration order, bit for bit,
+    and (binary64) the exact formula's expectation is A @ B to rounding."""
+    import time
+
+    import paper_1905_07439_b200 as rbc
+    from paper_1905_07439_b200.precision import parse_precision
+    from paper_1905_07439_b200.randomize import _hatted_batch, all_plan_arrays, enumerate_expectation
+
+    mode = parse_precision(label)
+    f = rbc.laderman_formula()
+    g = rbc.derive_rng(36, N)
+    A = mode.array(g.standard_normal((N, N)))
+    B = mode.array(g.standard_normal((N, N)))
+    t0 = time.perf_counter()
+    got = enumerate_expectation(f, A, B, mode)
+    dt = time.perf_counter() - t0
+    perms, signs = all_plan_arrays(3)
+    total = np.zeros((N, N))
+    for c0 in range(0, len(perms), 8192):
+        lv = _hatted_batch(f, perms[c0:c0 + 8192], signs[c0:c0 + 8192], mode)
+        C = oracle.apply_levels([lv], A[None], B[None], mode)
+        for t in range(C.shape[0]):
+            np.add(total, C[t].astype(np.float64), out=total)
+    want = total / float(len(perms))
+    assert np.array_equal(got, want)
+    print(f"110,592-plan enumeration on the GPU: {dt:.2f} s")
+    if label == "f64":
+        # unbiasedness of an exact formula, up to the rounding of a
+        # sequential sum of 110,592 products (~count * u relative)
+        ref = A @ B
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-10
