@@ -751,11 +751,12 @@ class ErrorTrialWorkload:
         cfg, T = self.cfg, len(self.pair_ids)
         nxt = [self.pair_ids[-1] + 1]
         dev = self.a.device
+        bufs = (torch.empty_like(self.a), torch.empty_like(self.b))  # drawn into every step
 
         def step():
             p0 = nxt[0]
             nxt[0] += T
-            a, b = make_pairs_device(cfg, p0, T, dev)
+            a, b = make_pairs_device(cfg, p0, T, dev, out=bufs)
             pl = torch.from_numpy(packed_plans(cfg, [cfg.plan_key(p) for p in range(p0, p0 + T)]))
             self.runner.run(a, b, pl.to(dev, non_blocking=True))
             return self.runner.err_rand.cpu(), self.runner.err_det.cpu()

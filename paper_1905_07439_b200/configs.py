@@ -124,13 +124,14 @@ def packed_plans(cfg: TrialConfig, keys) -> np.ndarray:
     return engine.pack_plans(cfg.n, perms, signs).reshape(len(keys), cfg.Q, -1)
 
 
-def make_pairs_device(cfg: TrialConfig, first: int, count: int, device="cuda:0"):
+def make_pairs_device(cfg: TrialConfig, first: int, count: int, device="cuda:0", out=None):
     """Device twin of :func:`make_pairs`: (A, B) torch tensors (count, N, N)
     in the mode dtype on ``device``, bit-identical to make_pairs (the matrices
     are drawn on the GPU from the same Philox streams)."""
     from .matgen import generate_device
 
-    return generate_device(cfg.kind, cfg.N, pair_seeds(cfg, first, count), cfg.mode, device)
+    return generate_device(cfg.kind, cfg.N, pair_seeds(cfg, first, count), cfg.mode, device,
+                           out=out)
 
 
 def make_pairs(cfg: TrialConfig, first: int, count: int, workers: int = 1):

@@ -114,6 +114,11 @@ cudaError_t launch_truth(int dtype_in, int64_t batch, int64_t M, int64_t K, int6
                          const void* x, int64_t x_bstride, const void* y, int64_t y_bstride,
                          void* out, cudaStream_t st);
 
+// The stream-ordered default pool of `device` retains up to 4 GiB of freed
+// scratch (truth panels, generator words) instead of returning it at every
+// synchronisation (truth.cu).
+cudaError_t keep_pool(int device);
+
 // ---- seeded test matrices (matgen.cu) -----------------------------------
 // Matrix families, in the order of reference MATRIX_KINDS (matgen.py:21)
 // followed by the builder kinds.

@@ -482,6 +482,11 @@ int run_normals(int64_t count, int64_t n, const uint64_t* dkeys, const int* dwhi
     const size_t oLi = take(sizeof(int64_t) * cap);
     const size_t oCr = take(sizeof(unsigned long long));
     char* scratch = nullptr;
+    {
+      int dev = 0;
+      CUDA_TRY(cudaGetDevice(&dev));
+      CUDA_TRY(keep_pool(dev));  // repeated draws reuse the scratch
+    }
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), off, st));
     auto at = [&](size_t o) { return scratch + o; };
     uint64_t* W = reinterpret_cast<uint64_t*>(at(oW));

@@ -257,6 +257,8 @@ constexpr size_t kSmem = sizeof(double) * kStages * kBK * (kBM + kBN) + 2 * size
 // next synchronisation).  The host-buffer calls size their arenas to 85% of
 // free + arena memory (engine.cu host_ws_budget / rbc_error_trials), so the
 // retained scratch always fits in the remaining 15% (27 GB on a B200).
+}  // namespace
+
 cudaError_t keep_pool(int device) {
   static int done = -1;
   if (done == device) return cudaSuccess;
@@ -268,6 +270,8 @@ cudaError_t keep_pool(int device) {
   if (e == cudaSuccess) done = device;
   return e;
 }
+
+namespace {
 
 template <class TIn>
 cudaError_t run_truth_bulk(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x,

@@ -97,14 +97,15 @@ def philox_key(seed: int, *path: int) -> tuple[int, int]:
     return int(key[0]), int(key[1])
 
 
-def generate_device(kind: str, size: int, seeds, mode, device="cuda:0", which=(0, 1)):
+def generate_device(kind: str, size: int, seeds, mode, device="cuda:0", which=(0, 1), out=None):
     """Device twin of :func:`generate` over many seeds: returns a tuple of
     torch tensors, one per entry of ``which`` (0 = A, 1 = B), each
     (len(seeds), size, size) in the mode dtype on ``device``, bit-identical to
     ``mode.array(generate(MatrixSpec(kind, size, seed))[w])`` (librbc
     rbc_matgen: Philox4x64-10 and numpy's ziggurat on the device, SURVEY §8f
     rank 4).  Raises OverflowError where the rounding into the mode overflows,
-    like ``mode.array``."""
+    like ``mode.array``.  ``out``: optional tensors (one per ``which``) to
+    draw into instead of allocating."""
     import ctypes
 
     import torch
@@ -123,8 +124,12 @@ def generate_device(kind: str, size: int, seeds, mode, device="cuda:0", which=(0
     lib = _lib.load()
     code = (MATRIX_KINDS + BUILDER_KINDS).index(kind)
     outs = []
-    for w in which:
-        out = torch.empty((len(seeds), size, size), dtype=tdt, device=dev)
+    dst = list(out) if out is not None else [None] * len(which)
+    for w, buf in zip(which, dst):
+        shape = (len(seeds), size, size)
+        if buf is not None and (tuple(buf.shape) != shape or buf.dtype != tdt or not buf.is_contiguous()):
+            raise ValueError("out tensor does not match the draw")
+        out = buf if buf is not None else torch.empty(shape, dtype=tdt, device=dev)
         flags = torch.zeros(max(1, len(seeds)), dtype=torch.uint8, device=dev)
         for c0 in range(0, len(seeds), 65535):
             part = seeds[c0:c0 + 65535]
