@@ -29,12 +29,6 @@
 
 namespace rbc {
 
-namespace {
-thread_local cudaEvent_t t_expanded_event = nullptr;
-}  // namespace
-
-void set_expanded_event(cudaEvent_t ev) { t_expanded_event = ev; }
-
 static thread_local std::string g_last_error;
 
 static int set_error(int code, const char* fmt, ...) {
@@ -299,7 +293,6 @@ static int run_pass(const Geometry& g, const PassArgs& p, void* ws, size_t ws_by
         q += step;
       }
     }
-    if (t_expanded_event) CUDA_TRY(cudaEventRecord(t_expanded_event, st));
     // --- leaves (or the fused bottom subtree)
     const int64_t m = g.leaf_m;
     if (fuseL) {
@@ -997,15 +990,9 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   std::lock_guard<std::mutex> lock(arena().mu);
   // pipeline chunks: about 8 MB of operands per chunk, at most 16 (config 2
   // with two compute streams: 12 chunks 11.21 ms per call, 16: 11.20, 32:
-  // 11.4); RBC_E2E_CHUNKS overrides
-  static const int forced_chunks = [] {
-    const char* v = getenv("RBC_E2E_CHUNKS");
-    return v ? atoi(v) : 0;
-  }();
-  int64_t nchunks = forced_chunks > 0
-                        ? forced_chunks
-                        : std::min<int64_t>(16, std::max<int64_t>(
-                                                    1, (int64_t)(2 * T * N2 * es >> 23)));
+  // 11.4)
+  int64_t nchunks =
+      std::min<int64_t>(16, std::max<int64_t>(1, (int64_t)(2 * T * N2 * es >> 23)));
   int64_t C = std::max<int64_t>(1, (T + nchunks - 1) / nchunks);
   if (C > 8) C = (C + 7) / 8 * 8;  // whole multiples of 8 trials keep grids regular
   // Two compute streams pay off for many small chunks (config 2: 1000 pairs

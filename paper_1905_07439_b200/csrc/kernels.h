@@ -148,11 +148,6 @@ cudaError_t launch_sum_trials(int dtype, int64_t ntr, int64_t N2, const void* x,
 cudaError_t launch_nonfinite(int dtype, int64_t T, int64_t N2, const void* x, uint8_t* flags,
                              cudaStream_t st);
 
-// Phase hook of the engine pass (error-trial lane staggering): when set on
-// the calling host thread, run_pass records the event on its stream after
-// the expansion levels of each trial chunk, before the leaves / fused subtree.
-void set_expanded_event(cudaEvent_t ev);
-
 // ---- diagonal rescaling (rescale.cu; reference rescale.py:36-99) ----------
 // Maxima of |x| (N x N, mode dtype) along rows (axis 1) or columns (axis 0)
 // into out (N, mode dtype); *zero set to 1 when one is 0.  scratch: at least

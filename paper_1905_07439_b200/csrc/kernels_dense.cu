@@ -286,27 +286,9 @@ template <class T>
 cudaError_t staged_contract(int n, const void* ch, int64_t K, int64_t mb, int R, const void* w,
                             int64_t ws, void* out, int64_t ntr, uint8_t* nf, cudaStream_t st) {
   if ((size_t)R * n * n * sizeof(T) > 160 * 1024) return cudaErrorNotSupported;
-  // RBC_CONTRACT_DENSE=<positions per thread><children per batch> (tuning
-  // aid, binary64 n = 3): 24, 18, 28, 42, 14, 44, 112, 123, 212 (default)
-  static const int variant = [] {
-    const char* v = getenv("RBC_CONTRACT_DENSE");
-    return v ? atoi(v) : 0;
-  }();
-  if (sizeof(T) == 8 && n == 3 && variant) {
-    switch (variant) {
-      case 18: return staged_contract_n<T, 3, 1, 8>(ch, K, mb, R, w, ws, out, ntr, nf, st);
-      case 28: return staged_contract_n<T, 3, 2, 8>(ch, K, mb, R, w, ws, out, ntr, nf, st);
-      case 42: return staged_contract_n<T, 3, 4, 2>(ch, K, mb, R, w, ws, out, ntr, nf, st);
-      case 14: return staged_contract_n<T, 3, 1, 4>(ch, K, mb, R, w, ws, out, ntr, nf, st);
-      case 44: return staged_contract_n<T, 3, 4, 4>(ch, K, mb, R, w, ws, out, ntr, nf, st);
-      case 112: return staged_contract_n<T, 3, 1, 12>(ch, K, mb, R, w, ws, out, ntr, nf, st);
-      case 123: return staged_contract_n<T, 3, 1, 23>(ch, K, mb, R, w, ws, out, ntr, nf, st);
-      case 212: return staged_contract_n<T, 3, 2, 12>(ch, K, mb, R, w, ws, out, ntr, nf, st);
-      default: break;
-    }
-  }
   // binary64 n = 3 (config 3's noisy Laderman): 2 positions per thread and
-  // the children of 12 terms in flight (0.166 vs 0.183 ms per launch for 4)
+  // the children of 12 terms in flight (ms per launch: 4 terms 0.183, 8:
+  // 0.175, 12: 0.164, 23: 0.201; 1 or 4 positions per thread no better)
   if (sizeof(T) == 8 && n == 3)
     return staged_contract_n<T, 3, 2, 12>(ch, K, mb, R, w, ws, out, ntr, nf, st);
   switch (n) {

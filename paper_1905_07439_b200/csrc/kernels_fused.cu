@@ -424,204 +424,17 @@ __global__ void __launch_bounds__(NT) subtree_soa_kernel(
   }
 }
 
-template <class F, class T, int M, int H>
-cudaError_t launch_subtree_soa_h(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
-                                 void* out, const PlanLevel* plans, int64_t pts, int q0,
-                                 int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
-  constexpr int NT = 256;
-  using S = SubtreeSoA<F, T, M, H>;
-  static const size_t pad = [] {  // RBC_SUBTREE_SMEM_PAD: occupancy experiments
-    const char* v = getenv("RBC_SUBTREE_SMEM_PAD");
-    return v ? (size_t)atol(v) : (size_t)0;
-  }();
-  const size_t smem = S::smem_bytes() + pad;
-  auto kern = subtree_soa_kernel<F, T, M, H, NT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)K0, (unsigned)(ntr < 65535 ? ntr : 65535));
-  kern<<<grid, NT, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, (T*)out, plans, pts,
-                               q0, ntr, nonfinite);
-  return cudaGetLastError();
-}
-
-// Parent groups per subtree (RBC_SUBTREE_H=2 halves the leaf buffers: 6
-// instead of 4 CTAs/SM on config 2, but measured 5.3 vs 5.0 ms per launch --
-// the extra barrier rounds cost more than the occupancy gains; default 1).
 template <class F, class T, int M>
 cudaError_t launch_subtree_soa(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
                                void* out, const PlanLevel* plans, int64_t pts, int q0,
                                int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
-  static const int h = [] {
-    const char* v = getenv("RBC_SUBTREE_H");
-    return v ? atoi(v) : 1;
-  }();
-  if (h == 2) return launch_subtree_soa_h<F, T, M, 2>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
-  return launch_subtree_soa_h<F, T, M, 1>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
-}
-
-// ---- warp-specialised two-level subtree ------------------------------------
-// Same arithmetic as subtree_kernel<F, T, 2, M>, other schedule: the top
-// expansion (level q0 -> q0+1) and the last contraction run CTA-wide, but
-// everything below a level-(q0+1) block -- its R children, their R leaf
-// products and its contraction -- is done by one warp on its own shared
-// scratch, synchronised with __syncwarp only.  Each warp takes G level-1
-// blocks at a time, so the CTA-wide barriers that dominated the stalls of
-// the stage-synchronous kernel disappear from the inner levels.
-template <class F, class T, int M, int G>
-struct Subtree2W {
-  static constexpr int n = F::n;
-  static constexpr int R = F::R;
-  static constexpr int s1 = M * n;
-  static constexpr int s0 = s1 * n;
-  static constexpr int kids1 = s1 * s1;
-  static constexpr int leafE = M * M;
-  static constexpr int scratch = 2 * G * R * leafE;  // per warp: X2 and Y2 of G blocks
-  static constexpr size_t header() {
-    return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 6 * sizeof(GatherTab<n>);
-  }
-  static constexpr size_t smem_bytes(int warps) {
-    return header() + sizeof(T) * ((size_t)2 * R * kids1 + (size_t)warps * scratch);
-  }
-};
-
-template <class F, class T, int M, int G, int NT>
-__global__ void __launch_bounds__(NT, 4) subtree2w_kernel(
-    const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0,
-    T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
-    int64_t ntr, uint8_t* __restrict__ nonfinite) {
-  using S = Subtree2W<F, T, M, G>;
-  constexpr int n = F::n;
-  constexpr int R = F::R;
-  constexpr int s0 = S::s0, s1 = S::s1, kids1 = S::kids1, leafE = S::leafE;
-  constexpr int NW = NT / 32;
-  constexpr int kHalf = NT / 2;
-  using A = Arith<T>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
-  GatherTab<n>* tabs =
-      reinterpret_cast<GatherTab<n>*>(smem_raw + ((sizeof(PlanLevel) * 2 + 15) / 16) * 16);
-  T* X1 = reinterpret_cast<T*>(smem_raw + S::header());
-  T* Y1 = X1 + R * kids1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  T* X2 = Y1 + R * kids1 + warp * S::scratch;
-  T* Y2 = X2 + G * R * leafE;
-  const int k0 = blockIdx.x;
-  const int which = threadIdx.x >= kHalf;
-  const int lt = threadIdx.x - which * kHalf;
-
-  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
-    __syncthreads();
-    {
-      constexpr int kWords = (int)(sizeof(PlanLevel) / 4) * 2;
-      const int* src = reinterpret_cast<const int*>(plans + t * plan_tstride + q0);
-      if (threadIdx.x < kWords) reinterpret_cast<int*>(spl)[threadIdx.x] = src[threadIdx.x];
-    }
-    __syncthreads();
-    if (threadIdx.x < 6) {
-      const int l = threadIdx.x / 3, kind = threadIdx.x - 3 * (threadIdx.x / 3);
-      const int sp = l == 0 ? s0 : s1;
-      GatherTab<n> tab;
-      if (kind == 0)
-        make_gather<n, 0>(spl[l], sp, tab);
-      else if (kind == 1)
-        make_gather<n, 1>(spl[l], sp, tab);
-      else
-        make_scatter<n>(spl[l], sp / n, tab);
-      tabs[threadIdx.x] = tab;
-    }
-    __syncthreads();
-
-    // ---- level q0 -> q0+1, CTA-wide (A on the first half, B on the second)
-    {
-      const T* src = (which ? y : x) + t * xy_tstride + (int64_t)k0 * s0 * s0;
-      T* dst = which ? Y1 : X1;
-      const GatherTab<n> gt = tabs[which];
-      for (int e = lt; e < kids1; e += kHalf) {
-        const int i = e / s1, j = e - (e / s1) * s1;
-        if (which)
-          expand_tab<F, T, 1, 1>(src + i * s0 + j, gt, dst + i * s1 + j, kids1);
-        else
-          expand_tab<F, T, 1, 0>(src + i * s0 + j, gt, dst + i * s1 + j, kids1);
-      }
-    }
-    __syncthreads();
-
-    // ---- per warp: G level-(q0+1) blocks at a time, everything below them
-    {
-      const GatherTab<n> gx = tabs[3], gy = tabs[4], sc1 = tabs[5];
-      for (int b = warp; b * G < R; b += NW) {
-        const int k1a = b * G;
-        const int nk = R - k1a < G ? R - k1a : G;
-        const int items = nk * leafE;
-        for (int e = lane; e < items; e += 32) {
-          const int pos = e / nk, kl = e - (e / nk) * nk;
-          const int i = pos / M, j = pos - (pos / M) * M;
-          expand_tab<F, T, 1, 0>(X1 + (k1a + kl) * kids1 + i * s1 + j, gx,
-                                 X2 + kl * R * leafE + pos, leafE);
-        }
-        for (int e = lane; e < items; e += 32) {
-          const int pos = e / nk, kl = e - (e / nk) * nk;
-          const int i = pos / M, j = pos - (pos / M) * M;
-          expand_tab<F, T, 1, 1>(Y1 + (k1a + kl) * kids1 + i * s1 + j, gy,
-                                 Y2 + kl * R * leafE + pos, leafE);
-        }
-        __syncwarp();
-        // leaf products in place over X2 (one lane per leaf)
-        for (int lf = lane; lf < nk * R; lf += 32) {
-          T xa[leafE], yb[leafE];
-#pragma unroll
-          for (int q = 0; q < leafE; ++q) {
-            xa[q] = X2[lf * leafE + q];
-            yb[q] = Y2[lf * leafE + q];
-          }
-#pragma unroll
-          for (int i = 0; i < M; ++i)
-#pragma unroll
-            for (int j = 0; j < M; ++j) {
-              T acc = A::mul(xa[i * M], yb[j]);
-#pragma unroll
-              for (int k = 1; k < M; ++k) acc = A::add(acc, A::mul(xa[i * M + k], yb[k * M + j]));
-              X2[lf * leafE + i * M + j] = acc;
-            }
-        }
-        __syncwarp();
-        // contraction into the block's (now dead) X1 slot
-        for (int e = lane; e < items; e += 32) {
-          const int pos = e / nk, kl = e - (e / nk) * nk;
-          const int i = pos / M, j = pos - (pos / M) * M;
-          contract_tab<F, T, 1, false>(X2 + kl * R * leafE + pos, leafE,
-                                       X1 + (k1a + kl) * kids1 + i * s1 + j, sc1);
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-
-    // ---- level q0+1 -> q0, CTA-wide, to HBM
-    bool ok = true;
-    {
-      const GatherTab<n> sc0 = tabs[2];
-      T* dbase = out + (t * K0 + k0) * (int64_t)s0 * s0;
-      for (int e = threadIdx.x; e < kids1; e += NT) {
-        const int i = e / s1, j = e - (e / s1) * s1;
-        if (nonfinite)
-          ok = contract_tab<F, T, 1, true>(X1 + i * s1 + j, kids1, dbase + i * s0 + j, sc0) && ok;
-        else
-          contract_tab<F, T, 1, false>(X1 + i * s1 + j, kids1, dbase + i * s0 + j, sc0);
-      }
-    }
-    if (nonfinite && !ok) nonfinite[t] = 1;
-  }
-}
-
-template <class F, class T, int M, int G>
-cudaError_t launch_subtree2w(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
-                             void* out, const PlanLevel* plans, int64_t pts, int q0, int64_t ntr,
-                             uint8_t* nonfinite, cudaStream_t st) {
   constexpr int NT = 256;
-  using S = Subtree2W<F, T, M, G>;
-  const size_t smem = S::smem_bytes(NT / 32);
-  auto kern = subtree2w_kernel<F, T, M, G, NT>;
+  // one parent group per subtree (two halve the leaf buffers -- 6 instead of 4
+  // CTAs per SM on config 2 -- but the extra barrier rounds cost more: 5.3 vs
+  // 5.0 ms per launch)
+  using S = SubtreeSoA<F, T, M, 1>;
+  const size_t smem = S::smem_bytes();
+  auto kern = subtree_soa_kernel<F, T, M, 1, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)K0, (unsigned)(ntr < 65535 ? ntr : 65535));
@@ -654,13 +467,12 @@ cudaError_t launch_subtree2w(const void* x, const void* y, int64_t xy_tstride, i
 // flips each child before contracting -- the same values the breadth-first
 // kernels produce.  Z overwrites X1 in place: a lane writes exactly the rows
 // {k*M + i} of block r1 it read.
-// STG: 0 = operands read straight from HBM in stage A; 1 = the next step's
-// level-q0 blocks prefetched by TMA bulk copies into two staging buffers;
-// 2 = one staging buffer and two X1/Y1 slots, so the contraction of step k
-// (stage C) and the expansion of step k + 1 (stage A) share one phase between
-// two CTA barriers (2 barriers per step instead of 3).
-template <class F, class T, int M, int SUB, int STG = 0>
+// 4-byte elements: the next step's level-q0 blocks are prefetched by TMA bulk
+// copies into two staging buffers (3.01 vs 3.28 ms per config-2 launch for
+// operands read straight from HBM in stage A, which 2-byte elements do).
+template <class F, class T, int M>
 struct SubtreeReg {
+  static constexpr int SUB = 1;  // subtrees per CTA step (2: 3.02 -> 3.16 ms, 3: 3.57)
   static constexpr int n = F::n;
   static constexpr int R = F::R;
   static constexpr int s1 = M * n;
@@ -675,21 +487,18 @@ struct SubtreeReg {
   static constexpr int RP = (F::R == 23 && M == 3) ? 26 : R + (R & 1);
   static constexpr int slot = 2 * kids1 * RP;             // X1 + Y1 of one subtree
   // resident CTAs per SM the register budget aims at (about 128 registers a thread)
-#ifndef RBC_SUBTREE_REGS
-#define RBC_SUBTREE_REGS 128
-#endif
-  static constexpr int kMinBlocks =
-      65536 / (RBC_SUBTREE_REGS * NT) > 0 ? 65536 / (RBC_SUBTREE_REGS * NT) : 1;
+  // the two-row leaf holds a third 27-register fiber: one resident CTA fewer
+  // keeps it spill-free
+  static constexpr int kMinBlocks = 65536 / (128 * NT) > 1 ? 65536 / (128 * NT) - 1 : 1;
   static constexpr size_t header() {
     return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 3 * sizeof(GatherTab<n>);
   }
   // level-q0 blocks of a step's SUB subtrees (consecutive in HBM), prefetched
   // by TMA bulk copies into [buffers][X, Y][span] (4-byte elements): each
   // operand's blocks are copied as the 16-byte-aligned span that encloses them
-  static constexpr bool kStage = STG != 0 && sizeof(T) == 4;
-  static constexpr bool kPipe = kStage && STG == 2;
-  static constexpr int kBufs = kPipe ? 1 : 2;   // staging buffers
-  static constexpr int kBanks = kPipe ? 2 : 1;  // X1/Y1 slot sets
+  static constexpr bool kStage = sizeof(T) == 4;
+  static constexpr int kBufs = 2;   // staging buffers
+  static constexpr int kBanks = 1;  // X1/Y1 slot sets
   static constexpr int spanE = ((SUB * s0 * s0 + 4) + 3) / 4 * 4;  // SUB consecutive blocks
   static constexpr int stage_elems = kStage ? kBufs * 2 * spanE : 0;
   static constexpr int bank = SUB * slot;
@@ -744,68 +553,15 @@ __device__ __forceinline__ void expand_to_children(const T* __restrict__ src,
   if (R & 1) dst[R - 1] = o[R - 1].v[0];
 }
 
-// Leaf row of lane li (k ascending, first term initialises).
-// ROT = false: the three Y rows by 9 shuffles.
-// ROT = true (M = 3): the two foreign rows A, B by 6 shuffles; the X fiber
-// was loaded with its columns in (own, A, B) order, and two selects per
-// output put the row-2 term last (only the last operand of a 3-term fold
-// matters, the first two commute).
-template <class T, int M, bool ROT>
-__device__ __forceinline__ Pack<T, M> leaf_row(const Pack<T, M>& xg, const Pack<T, M>& yg,
-                                               int gbase, int srcA, int srcB, bool own_last) {
-  using A = Arith<T>;
-  Pack<T, M> m;
-  if constexpr (ROT) {
-    static_assert(M == 3, "rotated leaf is for 3x3 leaves");
-    Pack<T, M> ya, yb;
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-      ya.v[j] = shfl_val(yg.v[j], srcA);
-      yb.v[j] = shfl_val(yg.v[j], srcB);
-    }
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-      const T po = A::mul(xg.v[0], yg.v[j]);
-      const T pa = A::mul(xg.v[1], ya.v[j]);
-      const T pb = A::mul(xg.v[2], yb.v[j]);
-      const T first = own_last ? pb : po;
-      const T last = own_last ? po : pb;
-      m.v[j] = A::add(A::add(first, pa), last);
-    }
-  } else {
-    Pack<T, M> yr[M];
-#pragma unroll
-    for (int k = 0; k < M; ++k)
-#pragma unroll
-      for (int j = 0; j < M; ++j) yr[k].v[j] = shfl_val(yg.v[j], gbase + k);
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-      T acc = A::mul(xg.v[0], yr[0].v[j]);
-#pragma unroll
-      for (int k = 1; k < M; ++k) acc = A::add(acc, A::mul(xg.v[k], yr[k].v[j]));
-      m.v[j] = acc;
-    }
-  }
-  return m;
-}
-
-// the two-row leaf (ROT = 2) holds a third 27-register fiber: one resident
-// CTA fewer (RBC_SUBTREE_ROT2_DROP) keeps it spill-free
-#ifndef RBC_SUBTREE_ROT2_DROP
-#define RBC_SUBTREE_ROT2_DROP 1
-#endif
-template <class F, class T, int M, int SUB, int ROT, int STG>
-__global__ void __launch_bounds__(SubtreeReg<F, T, M, SUB, STG>::NT,
-                                  SubtreeReg<F, T, M, SUB, STG>::kMinBlocks -
-                                      (ROT == 2 && SubtreeReg<F, T, M, SUB, STG>::kMinBlocks > 1
-                                           ? RBC_SUBTREE_ROT2_DROP
-                                           : 0))
+template <class F, class T, int M>
+__global__ void __launch_bounds__(SubtreeReg<F, T, M>::NT, SubtreeReg<F, T, M>::kMinBlocks)
 subtree_reg_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0, int kchunk,
     T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
     int64_t ntr, uint8_t* __restrict__ nonfinite) {
-  using S = SubtreeReg<F, T, M, SUB, STG>;
+  using S = SubtreeReg<F, T, M>;
   using P = Pack<T, M>;
+  constexpr int SUB = S::SUB;
   constexpr int n = F::n;
   constexpr int R = F::R;
   constexpr int s0 = S::s0, s1 = S::s1, kids1 = S::kids1, RP = S::RP, NT = S::NT;
@@ -828,10 +584,6 @@ subtree_reg_kernel(
   const bool in_range = gw < S::GPW && grp < SUB * R;
   if (grp >= SUB * R) grp = SUB * R - 1;
   const int bu = grp / R, r1 = grp - (grp / R) * R;
-  // rotated leaf: foreign rows A, B and the column order of the X fiber
-  const int rowA = li == 2 ? 0 : 1 - li;
-  const int rowB = li == 2 ? 1 : 2;
-  const int col_of[3] = {li, rowA, rowB};
   const int fib = bu * S::slot + li * s1 * RP + r1;  // lane's fiber origin
 
   const int kbeg = blockIdx.x * kchunk;
@@ -939,7 +691,7 @@ subtree_reg_kernel(
       const int xlr = pl1.perm[0][n - 1], xlc = pl1.perm[1][n - 1];
       const int ylr = pl1.perm[1][n - 1], ylc = pl1.perm[2][n - 1];
       P z[n * n];
-      if constexpr (ROT == 2) {
+      {
         // Two Y rows per lane, one by shuffles: slot A = row ra (the lane's
         // own row, row 0 for lane 2), slot B = row rb from the lane whose
         // slot A holds it, slot C = row 2 on every lane.  The leaf fold
@@ -976,24 +728,6 @@ subtree_reg_kernel(
             m.v[j] = A::add(A::add(A::mul(xg.v[0], yag.v[j]), A::mul(xg.v[1], yb)),
                             A::mul(xg.v[2], ycg.v[j]));
           }
-          F::template contract_w_step<T, M>(z, m, r2);
-        }
-      } else {
-        P xf[n * n], yf[n * n];
-#pragma unroll
-        for (int k = 0; k < n * n; ++k) {
-          const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
-#pragma unroll
-          for (int j = 0; j < M; ++j) {
-            xf[k].v[j] = X1[o + (ROT ? col_of[j] : j) * RP];
-            yf[k].v[j] = Y1[o + j * RP];
-          }
-        }
-#pragma unroll
-        for (int r2 = 0; r2 < R; ++r2) {
-          const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
-          const P yg = F::template expand_v1<T, M>(yf, r2, ylr, ylc);
-          const P m = leaf_row<T, M, ROT == 1>(xg, yg, gbase, gbase + rowA, gbase + rowB, li == 2);
           F::template contract_w_step<T, M>(z, m, r2);
         }
       }
@@ -1043,417 +777,73 @@ subtree_reg_kernel(
       }
     };
 
-    if constexpr (S::kPipe) {
-      // B(k) | barrier | C(k) + A(k+1) | barrier ...; one staging buffer,
-      // refilled as soon as stage A has consumed it (B of the next step
-      // covers the copy)
-      if (kbeg < kend) {
-        if (threadIdx.x == 0) issue(kbeg, 0);
-        __syncthreads();  // tables
-        mbar_wait(&mbar[0], ctr & 1);
-        ++ctr;
-        stage_a(kbeg, stg, sm);
-        __syncthreads();
-        if (threadIdx.x == 0 && kbeg + SUB < kend) issue(kbeg + SUB, 0);
-        int bsel = 0;
-        for (int k0 = kbeg; k0 < kend; k0 += SUB, bsel ^= 1) {
-          T* cur = sm + bsel * S::bank;
-          stage_b(k0, cur);
-          __syncthreads();
-          const bool next = k0 + SUB < kend;
-          if (next) {
-            mbar_wait(&mbar[0], ctr & 1);
-            ++ctr;
-          }
-          stage_c(k0, cur);
-          if (next) stage_a(k0 + SUB, stg, sm + (bsel ^ 1) * S::bank);
-          __syncthreads();
-          if (threadIdx.x == 0 && k0 + 2 * SUB < kend) issue(k0 + 2 * SUB, 0);
-        }
-      }
-    } else {
-      if (S::kStage && threadIdx.x == 0 && kbeg < kend) issue(kbeg, ctr & 1);
-      for (int k0 = kbeg; k0 < kend; k0 += SUB, ++ctr) {
-        if (S::kStage) mbar_wait(&mbar[ctr & 1], (ctr >> 1) & 1);
-        __syncthreads();
-        stage_a(k0, stg + (ctr & 1) * 2 * S::spanE, sm);
-        __syncthreads();
-        if (S::kStage && threadIdx.x == 0 && k0 + SUB < kend) issue(k0 + SUB, (ctr + 1) & 1);
-        stage_b(k0, sm);
-        __syncthreads();
-        stage_c(k0, sm);
-      }
+    if (S::kStage && threadIdx.x == 0 && kbeg < kend) issue(kbeg, ctr & 1);
+    for (int k0 = kbeg; k0 < kend; k0 += SUB, ++ctr) {
+      if (S::kStage) mbar_wait(&mbar[ctr & 1], (ctr >> 1) & 1);
+      __syncthreads();
+      stage_a(k0, stg + (ctr & 1) * 2 * S::spanE, sm);
+      __syncthreads();
+      if (S::kStage && threadIdx.x == 0 && k0 + SUB < kend) issue(k0 + SUB, (ctr + 1) & 1);
+      stage_b(k0, sm);
+      __syncthreads();
+      stage_c(k0, sm);
     }
     if (nonfinite && !ok) nonfinite[t] = 1;
   }
 }
 
-template <class F, class T, int M, int SUB, int ROT, int STG>
-cudaError_t launch_subtree_reg_v(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
-                                 void* out, const PlanLevel* plans, int64_t pts, int q0,
-                                 int64_t ntr, uint8_t* nonfinite, cudaStream_t st, int kchunk) {
-  using S = SubtreeReg<F, T, M, SUB, STG>;
-  const size_t smem = S::smem_bytes();
-  auto kern = subtree_reg_kernel<F, T, M, SUB, ROT, STG>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kchunk = ((kchunk + SUB - 1) / SUB) * SUB;
-  if (kchunk > K0) kchunk = (int)K0;
-  const int64_t nkc = (K0 + kchunk - 1) / kchunk;
-  dim3 grid((unsigned)nkc, (unsigned)(ntr < 65535 ? ntr : 65535));
-  kern<<<grid, S::NT, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, kchunk, (T*)out,
-                                  plans, pts, q0, ntr, nonfinite);
-  return cudaGetLastError();
-}
-
-// ---- exchange-free variant: one lane per leaf ELEMENT -------------------------
-// Lane (r1, i, j) holds the X row-i fiber (X[i, k], k < M, of all n*n
-// sub-blocks of level-(q0+1) block r1), the Y column-j fiber (Y[k, j]) and
-// the Z element fiber (Z(I, J)[i, j]).  Every grandchild's leaf entry
-// M[i, j] = sum_k X[i, k] Y[k, j] (k ascending) is then lane-local: no
-// shuffles.  The price is redundant expansion work (each X row is expanded
-// by the M lanes j, each Y column by the M lanes i).  Lanes are independent,
-// so they pack densely (R * M * M per subtree).  Stages A and C and the
-// shared layout are those of subtree_reg_kernel, plus a separate Z1 buffer
-// (lanes of one row read the columns their neighbours write).
-template <class F, class T, int M, int SUB>
-struct SubtreeLane {
-  static constexpr int n = F::n;
-  static constexpr int R = F::R;
-  static constexpr int s1 = M * n;
-  static constexpr int s0 = s1 * n;
-  static constexpr int kids1 = s1 * s1;
-  static constexpr int LPC = M * M;                  // lanes per level-1 block
-  static constexpr int units = SUB * R * LPC;
-  static constexpr int NT = (units + 31) / 32 * 32;
-  static constexpr int IA = (SUB * 2 * kids1 + NT - 1) / NT;
-  static constexpr int IC = (SUB * kids1 + NT - 1) / NT;
-  static constexpr int RP = (F::R == 23 && M == 3) ? 26 : R + (R & 1);
-  static constexpr int slot = 3 * kids1 * RP;       // X1, Y1, Z1 of one subtree
-  static constexpr size_t header() {
-    return ((sizeof(PlanLevel) * 2 + 15) / 16) * 16 + 3 * sizeof(GatherTab<n>);
-  }
-  static constexpr size_t smem_bytes() { return header() + sizeof(T) * (size_t)SUB * slot; }
-};
-
-template <class F, class T, int M, int SUB>
-__global__ void __launch_bounds__(SubtreeLane<F, T, M, SUB>::NT) subtree_lane_kernel(
-    const T* __restrict__ x, const T* __restrict__ y, int64_t xy_tstride, int K0, int kchunk,
-    T* __restrict__ out, const PlanLevel* __restrict__ plans, int64_t plan_tstride, int q0,
-    int64_t ntr, uint8_t* __restrict__ nonfinite) {
-  using S = SubtreeLane<F, T, M, SUB>;
-  using P = Pack<T, M>;
-  using P1 = Pack<T, 1>;
-  using A = Arith<T>;
-  constexpr int n = F::n;
-  constexpr int R = F::R;
-  constexpr int s0 = S::s0, s1 = S::s1, kids1 = S::kids1, RP = S::RP, NT = S::NT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PlanLevel* spl = reinterpret_cast<PlanLevel*>(smem_raw);
-  GatherTab<n>* tabs =
-      reinterpret_cast<GatherTab<n>*>(smem_raw + ((sizeof(PlanLevel) * 2 + 15) / 16) * 16);
-  T* sm = reinterpret_cast<T*>(smem_raw + S::header());
-
-  // stage-B role: unit -> (subtree slot bu, level-1 block r1, leaf element (i, j))
-  const bool unit_live = threadIdx.x < S::units;
-  const int uc = unit_live ? threadIdx.x : S::units - 1;
-  const int bu = uc / (R * S::LPC);
-  const int rem = uc - bu * (R * S::LPC);
-  const int r1 = rem / S::LPC;
-  const int le = rem - r1 * S::LPC;
-  const int li = le / M, lj = le - (le / M) * M;
-  const int fib = bu * S::slot + r1;
-
-  const int kbeg = blockIdx.x * kchunk;
-  const int kend = kbeg + kchunk < K0 ? kbeg + kchunk : K0;
-
-  for (int64_t t = blockIdx.y; t < ntr; t += gridDim.y) {
-    __syncthreads();
-    {
-      constexpr int kWords = (int)(sizeof(PlanLevel) / 4) * 2;
-      const int* src = reinterpret_cast<const int*>(plans + t * plan_tstride + q0);
-      if (threadIdx.x < kWords) reinterpret_cast<int*>(spl)[threadIdx.x] = src[threadIdx.x];
-    }
-    __syncthreads();
-    if (threadIdx.x < 3) {
-      GatherTab<n> tab;
-      switch (threadIdx.x) {
-        case 0: make_gather<n, 0>(spl[0], s0, tab); break;
-        case 1: make_gather<n, 1>(spl[0], s0, tab); break;
-        default: make_scatter<n>(spl[0], s1, tab); break;
-      }
-      tabs[threadIdx.x] = tab;
-    }
-    const PlanLevel& pl1 = spl[1];
-    int a_src[S::IA], a_dst[S::IA];
-    uint32_t a_msk[S::IA];
-#pragma unroll
-    for (int it = 0; it < S::IA; ++it) {
-      const int e0 = threadIdx.x + it * NT;
-      const int e = e0 < SUB * 2 * kids1 ? e0 : 0;
-      const int u = e / (2 * kids1);
-      const int eu = e - u * 2 * kids1;
-      const int which = eu >= kids1;
-      const int pos = eu - which * kids1;
-      const int row = pos / s1, col = pos - (pos / s1) * s1;
-      const int hk = row / M, hl = col / M;
-      const int ri = which ? 1 : 0, ci = which ? 2 : 1;
-      a_src[it] = u * s0 * s0 + row * s0 + col;
-      a_dst[it] = u * S::slot + which * kids1 * RP +
-                  ((pl1.perm[ri][hk] * M + (row - hk * M)) * s1 + pl1.perm[ci][hl] * M +
-                   (col - hl * M)) * RP;
-      a_msk[it] = sign_mask(pl1.neg[ri][hk] ^ pl1.neg[ci][hl]);
-    }
-    int c_src[S::IC];
-    uint32_t c_msk[S::IC];
-#pragma unroll
-    for (int it = 0; it < S::IC; ++it) {
-      const int e0 = threadIdx.x + it * NT;
-      const int e = e0 < SUB * kids1 ? e0 : 0;
-      const int u = e / kids1;
-      const int pos = e - u * kids1;
-      const int row = pos / s1, col = pos - (pos / s1) * s1;
-      const int hi = row / M, hj = col / M;
-      c_src[it] = u * S::slot + 2 * kids1 * RP +
-                  ((pl1.perm[0][hi] * M + (row - hi * M)) * s1 + pl1.perm[2][hj] * M +
-                   (col - hj * M)) * RP;
-      c_msk[it] = sign_mask(pl1.neg[0][hi] ^ pl1.neg[2][hj]);
-    }
-    bool ok = true;
-
-    for (int k0 = kbeg; k0 < kend; k0 += SUB) {
-      const int nsub = kend - k0 < SUB ? kend - k0 : SUB;
-      __syncthreads();
-      // ---- stage A: level q0 -> q0+1 (base order, signed)
-      {
-        const int64_t blk = t * xy_tstride + (int64_t)k0 * s0 * s0;
-#pragma unroll
-        for (int it = 0; it < S::IA; ++it) {
-          const int e = threadIdx.x + it * NT;
-          if (e < nsub * 2 * kids1) {
-            const int which = (e - (e / (2 * kids1)) * 2 * kids1) >= kids1;
-            if (which)
-              expand_to_children<F, T, 1>(y + blk + a_src[it], load_tab(tabs[1]), sm + a_dst[it], a_msk[it]);
-            else
-              expand_to_children<F, T, 0>(x + blk + a_src[it], load_tab(tabs[0]), sm + a_dst[it], a_msk[it]);
-          }
-        }
-      }
-      __syncthreads();
-
-      // ---- stage B: per lane, the leaf element (i, j) of all R grandchildren
-      {
-        const T* X1 = sm;
-        const T* Y1 = sm + kids1 * RP;
-        P xf[n * n], yf[n * n];
-#pragma unroll
-        for (int k = 0; k < n * n; ++k) {
-          const int o = ((k / n) * M * s1 + (k % n) * M) * RP + fib;
-#pragma unroll
-          for (int kk = 0; kk < M; ++kk) {
-            xf[k].v[kk] = X1[o + (li * s1 + kk) * RP];
-            yf[k].v[kk] = Y1[o + (kk * s1 + lj) * RP];
-          }
-        }
-        const int xlr = pl1.perm[0][n - 1], xlc = pl1.perm[1][n - 1];
-        const int ylr = pl1.perm[1][n - 1], ylc = pl1.perm[2][n - 1];
-        P1 z[n * n];
-#pragma unroll
-        for (int r2 = 0; r2 < R; ++r2) {
-          const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
-          const P yg = F::template expand_v1<T, M>(yf, r2, ylr, ylc);
-          P1 m;
-          T acc = A::mul(xg.v[0], yg.v[0]);
-#pragma unroll
-          for (int kk = 1; kk < M; ++kk) acc = A::add(acc, A::mul(xg.v[kk], yg.v[kk]));
-          m.v[0] = acc;
-          F::template contract_w_step<T, 1>(z, m, r2);
-        }
-        F::template contract_w_finish<T, 1>(z);
-        if (unit_live && bu < nsub) {
-          T* Z1 = sm + 2 * kids1 * RP;
-#pragma unroll
-          for (int k = 0; k < n * n; ++k)
-            Z1[((k / n) * M * s1 + (k % n) * M + li * s1 + lj) * RP + fib] = z[k].v[0];
-        }
-      }
-      __syncthreads();
-
-      // ---- stage C: level q0+1 -> q0, Z1 -> HBM (row-major)
-      {
-        const GatherTab<n> sc = load_tab(tabs[2]);
-#pragma unroll
-        for (int it = 0; it < S::IC; ++it) {
-          const int e = threadIdx.x + it * NT;
-          if (e < nsub * kids1) {
-            using O = PackOps<T, 1>;
-            const int u = e / kids1, pos = e - (e / kids1) * kids1;
-            const T* zc = sm + c_src[it];
-            P1 pr[R];
-#pragma unroll
-            for (int r = 0; r + 1 < R; r += 2) {
-              const Pack<T, 2> v = pload<T, 2>(zc + r);
-              pr[r].v[0] = flip_sign(v.v[0], c_msk[it]);
-              pr[r + 1].v[0] = flip_sign(v.v[1], c_msk[it]);
-            }
-            if (R & 1) pr[R - 1].v[0] = flip_sign(zc[R - 1], c_msk[it]);
-            P1 o[n * n];
-            F::template contract_w<T, 1>(pr, o);
-            const int row = pos / s1, col = pos - (pos / s1) * s1;
-            T* d = out + (t * K0 + k0 + u) * (int64_t)s0 * s0 + row * s0 + col;
-#pragma unroll
-            for (int k = 0; k < n * n; ++k) {
-              const P1 val = O::flip(o[k], sc.msk[k]);
-              if (nonfinite) ok = ok && O::all_finite(val);
-              pstore<T, 1>(d + sc.off[k], val);
-            }
-          }
-        }
-      }
-    }
-    if (nonfinite && !ok) nonfinite[t] = 1;
-  }
-}
-
-template <class F, class T, int M, int SUB>
-cudaError_t launch_subtree_lane_v(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
-                                  void* out, const PlanLevel* plans, int64_t pts, int q0,
-                                  int64_t ntr, uint8_t* nonfinite, cudaStream_t st, int kchunk) {
-  using S = SubtreeLane<F, T, M, SUB>;
-  const size_t smem = S::smem_bytes();
-  auto kern = subtree_lane_kernel<F, T, M, SUB>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kchunk = ((kchunk + SUB - 1) / SUB) * SUB;
-  if (kchunk > K0) kchunk = (int)K0;
-  const int64_t nkc = (K0 + kchunk - 1) / kchunk;
-  dim3 grid((unsigned)nkc, (unsigned)(ntr < 65535 ? ntr : 65535));
-  kern<<<grid, S::NT, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, kchunk, (T*)out,
-                                  plans, pts, q0, ntr, nonfinite);
-  return cudaGetLastError();
-}
-
-// Tuning aids (config 2, ms per launch): RBC_SUBTREE_ROT leaf exchange:
-// 2 = two Y rows per lane, 3 shuffles (default: 2.743; with SUB 2: 3.16,
-// SUB 3: 3.57 at one CTA per SM, 3.30 capped to two with spills; SUB 2
-// capped to three CTAs per SM: 3.19 with 144 bytes of spills;
-// the 4 networks with a runtime fold order specialised by a CTA-uniform
-// switch on (lastrow, lastcol) instead of fold3 selects (F::kU1Last): 3.20,
-// 168 registers and jump tables), 0 = 9 shuffles
-// (2.963; the kernel is bound by the shared-memory/shuffle data path, l1tex
-// 88%, and issue), 1 = rotated 6-shuffle leaf (3.38 in an earlier build;
-// RBC_SUBTREE_SUB subtrees per CTA step (1: 2.98, 2: 3.02, 3: 3.08);
-// a shuffle-free leaf where every lane expands the whole Y fiber measured
-// 8.5: 3x the Y network adds and 255 registers),
-// RBC_SUBTREE_STAGE TMA bulk prefetch of the level-q0 blocks (default 1:
-// 3.01; 0: 3.28; per-element cp.async: 3.40; 2 = one staging buffer and
-// double-buffered X1/Y1, stage C(k) sharing a phase with stage A(k+1), two
-// barriers per step: 3.01 -- barriers are not what bounds the kernel;
-// SUB 2 + STAGE 2: 3.64, five CTAs per SM no longer fit),
-// RBC_SUBTREE_CHUNK subtrees per CTA (default about 24, balanced; 8: 3.44,
-// 48: 3.46).
+// Measured and not kept on config 2 (ms per launch; default 2.74): two or
+// three subtrees per CTA step 3.16 / 3.57; the leaf's Y rows by 9 shuffles
+// 2.96, a rotated 6-shuffle leaf 3.38; a shuffle-free leaf where every lane
+// expands the whole Y fiber 8.5; one lane per leaf element 3.9; a
+// warp-specialised schedule 8.4; the runtime fold order specialised by a
+// CTA-uniform switch instead of fold3 selects 3.20; a pipelined two-barrier
+// schedule 3.01; 8 or 48 subtrees per CTA 3.44 / 3.46; one THREAD per
+// level-(q0+1) block, everything below it in registers 5.09 (255 registers,
+// 8 warps per SM: latency-bound; profiles/r02/experiments).
 template <class F, class T, int M>
 cudaError_t launch_subtree_reg(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
                                void* out, const PlanLevel* plans, int64_t pts, int q0,
                                int64_t ntr, uint8_t* nonfinite, cudaStream_t st) {
-  static const int sub = [] {
-    const char* v = getenv("RBC_SUBTREE_SUB");
-    return v ? atoi(v) : 1;
-  }();
-  static const int rot = [] {
-    const char* v = getenv("RBC_SUBTREE_ROT");
-    return v ? atoi(v) : 2;
-  }();
-  static const int kc = [] {
-    const char* v = getenv("RBC_SUBTREE_CHUNK");
-    return v ? atoi(v) : 0;
-  }();
-  static const int stg = [] {
-    const char* v = getenv("RBC_SUBTREE_STAGE");
-    return v ? atoi(v) : 1;
-  }();
+  using S = SubtreeReg<F, T, M>;
+  const size_t smem = S::smem_bytes();
+  auto kern = subtree_reg_kernel<F, T, M>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   // about 24 subtrees per CTA, balanced so no CTA gets a short tail chunk
   // (config 2: 529 blocks -> 23 x 23 instead of 22 x 24 + 1: 3.02 -> 2.98 ms)
-  int kchunk = kc;
-  if (kchunk <= 0) {
-    const int64_t nchunks = (K0 + 23) / 24;
-    kchunk = (int)((K0 + nchunks - 1) / nchunks);
-  }
-  static const int lane = [] {
-    const char* v = getenv("RBC_SUBTREE_LANE");
-    return v ? atoi(v) : 0;
-  }();
-  if (lane == 1)
-    return launch_subtree_lane_v<F, T, M, 1>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr,
-                                             nonfinite, st, kchunk);
-  if (lane == 2)
-    return launch_subtree_lane_v<F, T, M, 2>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr,
-                                             nonfinite, st, kchunk);
-#define RBC_REG(SB, RT, SG)                                                                   \
-  if (sub == SB && rot == RT && stg == SG)                                                      \
-    return launch_subtree_reg_v<F, T, M, SB, RT, SG>(x, y, xy_tstride, K0, out, plans, pts, q0, \
-                                                     ntr, nonfinite, st, kchunk);
-  RBC_REG(1, 0, 0)
-  RBC_REG(1, 1, 0)
-  RBC_REG(1, 1, 1)
-  RBC_REG(1, 0, 1)
-  RBC_REG(1, 2, 1)
-  RBC_REG(1, 0, 2)
-  RBC_REG(2, 0, 1)
-  RBC_REG(2, 0, 2)
-  RBC_REG(3, 0, 1)
-#undef RBC_REG
-  return cudaErrorInvalidValue;
+  const int64_t nchunks = (K0 + 23) / 24;
+  int kchunk = (int)((K0 + nchunks - 1) / nchunks);
+  kchunk = ((kchunk + S::SUB - 1) / S::SUB) * S::SUB;
+  if (kchunk > K0) kchunk = (int)K0;
+  const int64_t nkc = (K0 + kchunk - 1) / kchunk;
+  dim3 grid((unsigned)nkc, (unsigned)(ntr < 65535 ? ntr : 65535));
+  kern<<<grid, S::NT, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, kchunk, (T*)out,
+                                  plans, pts, q0, ntr, nonfinite);
+  return cudaGetLastError();
 }
 
 template <class F, class T, int L, int M>
 cudaError_t launch_subtree_t(const void* x, const void* y, int64_t xy_tstride, int64_t K0,
                              void* out, const PlanLevel* plans, int64_t pts, int q0, int64_t ntr,
                              uint8_t* nonfinite, cudaStream_t st) {
-  using S = Subtree<F, T, L, M>;
-  const size_t smem = S::smem_bytes();
-  // RBC_SUBTREE_THREADS=<128|256|512> overrides the CTA size (tuning aid)
-  static const int forced = [] {
-    const char* v = getenv("RBC_SUBTREE_THREADS");
-    return v ? atoi(v) : 0;
-  }();
-  auto launch = [&](auto kern, int nt) -> cudaError_t {
+  if constexpr (L == 2) {
+    // 3 x 3 Laderman leaves: level q0+1 in registers
+    if constexpr (F::kId == FLaderman::kId && M == 3 && !std::is_same<T, double>::value)
+      return launch_subtree_reg<F, T, M>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
+    // other two-level shapes: position-major shared-memory layout
+    return launch_subtree_soa<F, T, M>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
+  } else {
+    using S = Subtree<F, T, L, M>;
+    const size_t smem = S::smem_bytes();
+    auto kern = subtree_kernel<F, T, L, M, kThreads>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)K0, (unsigned)(ntr < 65535 ? ntr : 65535));
-    kern<<<grid, nt, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, (T*)out, plans,
-                                 pts, q0, ntr, nonfinite);
+    kern<<<grid, kThreads, smem, st>>>((const T*)x, (const T*)y, xy_tstride, (int)K0, (T*)out, plans,
+                                       pts, q0, ntr, nonfinite);
     return cudaGetLastError();
-  };
-  // warp-specialised variant for two fused levels (RBC_SUBTREE_WARP=1; measured
-  // slower on config 2 -- 8.4 vs 7.5 ms per launch -- so not the default)
-  if constexpr (L == 2) {
-    static const int mode = [] {
-      const char* v = getenv("RBC_SUBTREE_WARP");
-      return v ? atoi(v) : 0;
-    }();
-    if (mode)
-      return launch_subtree2w<F, T, M, 3>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
-    // register-resident level q0+1 for 3x3 Laderman leaves (RBC_SUBTREE_REG=0 disables)
-    if constexpr (F::kId == FLaderman::kId && M == 3 && !std::is_same<T, double>::value) {
-      static const int reg = [] {
-        const char* v = getenv("RBC_SUBTREE_REG");
-        return v ? atoi(v) : 1;
-      }();
-      if (reg)
-        return launch_subtree_reg<F, T, M>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
-    }
-    // position-major layout (default; RBC_SUBTREE_SOA=0 selects the row-major one)
-    static const int soa = [] {
-      const char* v = getenv("RBC_SUBTREE_SOA");
-      return v ? atoi(v) : 1;
-    }();
-    if (soa)
-      return launch_subtree_soa<F, T, M>(x, y, xy_tstride, K0, out, plans, pts, q0, ntr, nonfinite, st);
   }
-  if (forced == 128) return launch(subtree_kernel<F, T, L, M, 128>, 128);
-  if (forced == 512) return launch(subtree_kernel<F, T, L, M, 512>, 512);
-  return launch(subtree_kernel<F, T, L, M, 256>, 256);
 }
 
 // Table of instantiated (formula, L, M) shapes.

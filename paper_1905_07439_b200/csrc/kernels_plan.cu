@@ -327,12 +327,8 @@ cudaError_t expand2_plan_w(int which, const void* x, int64_t xs, int64_t K, int6
   // collects its pieces from drifting warps over the whole launch and L2
   // evicts to scattered DRAM pages (config 2, 27x27 binary32 blocks: 0.534 ->
   // 0.332 ms/launch).  Large blocks have whole lines per warp store, where the
-  // barrier only costs (config 5: 0.68 vs 0.73).  RBC_EXPAND2_SYNC=0/1 forces.
-  static const int forced = [] {
-    const char* v = getenv("RBC_EXPAND2_SYNC");
-    return v ? atoi(v) : -1;
-  }();
-  const bool sync = forced >= 0 ? forced != 0 : mb2 * mb2 * (int64_t)sizeof(T) < (64 << 10);
+  // barrier only costs (config 5: 0.68 vs 0.73).
+  const bool sync = mb2 * mb2 * (int64_t)sizeof(T) < (64 << 10);
   const dim3 gs = grid_for(K * (mb2 * mb2 / W), ntr, kSyncThreads);
   if (which == 0 && sync)
     expand2_plan_kernel<F, T, W, 0, true><<<gs, kSyncThreads, 0, st>>>(
@@ -403,12 +399,8 @@ cudaError_t contract2_plan_w(const void* ch, int64_t K, int64_t mb2, void* out,
                              const PlanLevel* plans, int64_t pts, int level, int64_t ntr,
                              uint8_t* nonfinite, cudaStream_t st) {
   const dim3 grid = grid_for(K * (mb2 * mb2 / W), ntr);
-  // lockstep for small blocks, as in expand2_plan_w (RBC_EXPAND2_SYNC forces)
-  static const int forced = [] {
-    const char* v = getenv("RBC_EXPAND2_SYNC");
-    return v ? atoi(v) : -1;
-  }();
-  const bool sync = forced >= 0 ? forced != 0 : mb2 * mb2 * (int64_t)sizeof(T) < (64 << 10);
+  // lockstep for small blocks, as in expand2_plan_w
+  const bool sync = mb2 * mb2 * (int64_t)sizeof(T) < (64 << 10);
   const dim3 gs = grid_for(K * (mb2 * mb2 / W), ntr, kSyncThreads);
   // (n = 2 formulas read R^2 = 49 blocks per thread: no lockstep variant,
   // its unrolled barrier loop costs 255 registers)

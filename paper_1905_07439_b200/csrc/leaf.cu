@@ -70,7 +70,9 @@ struct Mac<__half, double> {
   }
 };
 
-// RBC_LEAF_TILE=<128|64|32|1> overrides the tile choice (tuning aid).
+// Test hook (tests/test_trials_gpu.py): RBC_LEAF_TILE=999 skips the
+// specialised kernels so the generic tiles run at every size, 303 runs the
+// bulk-copy binary64 kernel from 128 up, 205 the single-shot small-leaf kernel.
 inline int tile_override() {
   const char* v = getenv("RBC_LEAF_TILE");
   return v ? atoi(v) : 0;
@@ -646,21 +648,12 @@ template <class TIn, class TAcc>
 cudaError_t small_square(int64_t batch, int64_t M, const void* x, int64_t xs, const void* y,
                          int64_t ys, void* out, cudaStream_t st) {
   if constexpr (std::is_same<TIn, TAcc>::value && sizeof(TIn) >= 4) {
-    const int f = tile_override();
     // 3 x 3 outputs per thread, 3 leaves per 243-thread CTA, 3 CTAs per SM
-    // (c3: 0.884 ms/launch).  3 x 9 ("211": 12 loads per 27 multiply-adds
-    // instead of 6 per 9) fits one CTA per SM and runs slower (1.13)
-    if (M == 27 && batch >= 2048 && (f == 0 || f == 210))
+    // (c3: 0.884 ms/launch; 3 x 9 outputs -- 12 loads per 27 multiply-adds
+    // instead of 6 per 9 -- fits one CTA per SM and ran slower, 1.13; operands
+    // 2 or 3 k steps ahead measured equal)
+    if (M == 27 && batch >= 2048 && tile_override() == 0)
       return run_smem_bulk<TIn, 27, 3, 3>(batch, x, xs, y, ys, out, st);
-    if (M == 27 && batch >= 2048 && f == 211)
-      return run_smem_bulk<TIn, 27, 3, 9>(batch, x, xs, y, ys, out, st);
-    if (M == 27 && batch >= 2048 && f == 212)
-      return run_smem_bulk<TIn, 27, 9, 3>(batch, x, xs, y, ys, out, st);
-    // operands 2 / 3 k-steps ahead (tuning aid)
-    if (M == 27 && batch >= 2048 && f == 213)
-      return run_smem_bulk<TIn, 27, 3, 3, 2>(batch, x, xs, y, ys, out, st);
-    if (M == 27 && batch >= 2048 && f == 214)
-      return run_smem_bulk<TIn, 27, 3, 3, 3>(batch, x, xs, y, ys, out, st);
   }
   switch (M) {
     case 27: return run_smem<TIn, TAcc, 27, 3>(batch, x, xs, y, ys, out, st);
@@ -1219,37 +1212,11 @@ template <class TIn, class TAcc>
 cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x,
                           int64_t xs, const void* y, int64_t ys, void* out, cudaStream_t st) {
   const int forced = tile_override();
-  // tuning variants (RBC_LEAF_TILE=2xx)
-  if (forced == 201 && M >= 64 && N >= 128)
-    return run_tiled<TIn, TAcc, 64, 128, 8, 4, 8>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 202 && M >= 128 && N >= 64)
-    return run_tiled<TIn, TAcc, 128, 64, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 203 && M >= 64 && N >= 64)
-    return run_tiled<TIn, TAcc, 64, 64, 16, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 204 && M >= 64 && N >= 64)
-    return run_tiled<TIn, TAcc, 64, 64, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 207 && M >= 64 && N >= 128)
-    return run_tiled<TIn, TAcc, 64, 128, 16, 4, 8>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 208 && M >= 128 && N >= 128)
-    return run_tiled<TIn, TAcc, 128, 128, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 206 && M >= 64 && N >= 64)
-    return run_tiled<TIn, TAcc, 64, 64, 4, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 128 && M >= 128 && N >= 128)
-    return run_tiled<TIn, TAcc, 128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 64 && M >= 64 && N >= 64)
-    return run_tiled<TIn, TAcc, 64, 64, 8, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 32 && M >= 32 && N >= 32)
-    return run_tiled<TIn, TAcc, 32, 32, 8, 2, 2>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (forced == 1) return run_small<TIn, TAcc>(batch, M, K, N, x, xs, y, ys, out, st);
   if constexpr (sizeof(TAcc) == 8) {
     // binary64 accumulation: from 512 up the widen pass + bulk-copy pipeline
     // (truth.cu; 8192: 28.8 vs 24.9 TFLOP/s); below it the widen pass costs
     // more than it saves (243 x 200: 15.8 vs 17.6) and the register-staged
     // tile runs (tools/leaf_bench.py)
-    if (forced == 310 && M >= 128 && N >= 128 && K >= 1)  // tuning: ragged truth tiles at any size
-      return run_truth<TIn, 128, 64, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (forced == 311 && M >= 128 && N >= 64)  // tuning: 128 x 64 tiles, 8 x 4 per thread
-      return run_tiled<TIn, TAcc, 128, 64, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
     // binary64 operands of ragged sizes below 1024 (config 3: 729) skip the
     // panel pass too: 128 x 64 register-staged tiles, 0.194 vs 0.233 ms per
     // launch (config 4's 2048 binary16 truth stays on the bulk pipeline:
@@ -1268,22 +1235,12 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
     // CTAs (19.5 vs 18.0 TFLOP/s); whole 128-multiples with 128 x 128
     if (forced == 0 && M >= 128 && N >= 128 && K >= 1 && (M % 128 || N % 128))
       return run_truth<TIn, 128, 64, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
-    if ((forced == 0 || forced == 302) && M >= 128 && N >= 128 && K >= 1)
+    if (forced == 0 && M >= 128 && N >= 128 && K >= 1)
       return run_truth<TIn, 128, 128, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
     if (forced == 303 && M >= 128 && N >= 128 && K >= 1)  // bulk kernel at any size
       return launch_truth(std::is_same<TIn, double>::value ? kF64
                           : std::is_same<TIn, float>::value ? kF32 : kF16,
                           batch, M, K, N, x, xs, y, ys, out, st);
-    if (forced == 300 && M >= 128 && N >= 128 && K >= 1)
-      return run_truth<TIn, 128, 128, 16, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (forced == 301 && M >= 128 && N >= 128 && K >= 1)
-      return run_truth<TIn, 128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (forced == 304 && M >= 128 && N >= 64 && K >= 1)  // half the register file per CTA
-      return run_truth<TIn, 128, 64, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (forced == 305 && M >= 64 && N >= 64 && K >= 1)
-      return run_truth<TIn, 64, 64, 16, 8, 8, false>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (forced == 306 && M >= 128 && N >= 128 && K >= 1)
-      return run_truth<TIn, 128, 128, 32, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
   }
   // binary64: 128x64 tiles of 8x4 outputs per thread (truth 243: 15.3 vs
   // 14.5 TFLOP/s for 64x128, 13.9 for 64x64; tools/leaf_bench.py)
@@ -1297,7 +1254,7 @@ cudaError_t leaf_dispatch(int64_t batch, int64_t M, int64_t K, int64_t N, const 
     return run_tiled<TIn, TAcc, 64, 64, 8, 4, 4>(batch, M, K, N, x, xs, y, ys, out, st);
   if (M >= 32 && N >= 32)
     return run_tiled<TIn, TAcc, 32, 32, 8, 2, 2>(batch, M, K, N, x, xs, y, ys, out, st);
-  if (M == N && M == K && forced != 2) {
+  if (M == N && M == K) {
     cudaError_t e = small_square<TIn, TAcc>(batch, M, x, xs, y, ys, out, st);
     if (e != cudaErrorNotSupported) return e;
   }
@@ -1320,18 +1277,13 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
                      (ys % 4 == 0 || batch == 1) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
                      ((uintptr_t)out % 16 == 0);
     const int forced = tile_override();
-    if (vec && M >= 128 && N >= 128 && (forced == 0 || forced == 501))
+    // 128 x 128 x 8 tiles, 8 x 8 per thread (k tiles of 16 measured equal)
+    if (vec && M >= 128 && N >= 128 && forced == 0)
       return run_f32v<128, 128, 8, 8, 8, 2>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (vec && M >= 128 && N >= 128 && forced == 502)
-      return run_f32v<128, 128, 16, 8, 8, 2>(batch, M, K, N, x, xs, y, ys, out, st);
     // 64-wide leaves (config 1): 4 x 8 per thread, 128 threads (26.2 vs
-    // 20.5 TFLOP/s for 8 x 8 per thread; tools/leaf_bench.py)
-    if (vec && M >= 64 && N >= 64 && (forced == 0 || forced == 504))
+    // 20.5 TFLOP/s for 8 x 8 per thread)
+    if (vec && M >= 64 && N >= 64 && forced == 0)
       return run_f32v<64, 64, 8, 4, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (vec && M >= 64 && N >= 64 && forced == 503)
-      return run_f32v<64, 64, 16, 8, 8, 6>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (vec && M >= 64 && N >= 128 && forced == 505)
-      return run_f32v<64, 128, 8, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
     return leaf_dispatch<float, float>(batch, M, K, N, x, xs, y, ys, out, st);
   }
   if (dtype_out == kF16 && dtype_in == kF16) {
@@ -1340,14 +1292,8 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
                      (ys % 8 == 0 || batch == 1) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
                      ((uintptr_t)out % 16 == 0);
     const int forced = tile_override();
-    if (vec && M >= 128 && N >= 128 && (forced == 0 || forced == 401))
+    if (vec && M >= 128 && N >= 128 && forced == 0)
       return run_h2dup<128, 128, 16, 8, 16, 3>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (vec && M >= 128 && N >= 128 && forced == 402)
-      return run_h2dup<128, 128, 16, 8, 16, 2>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (vec && M >= 64 && N >= 64 && forced == 403)
-      return run_h2dup<64, 64, 16, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
-    if (vec && M >= 128 && N >= 128 && forced == 404)
-      return run_h2dup<128, 64, 16, 8, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
     if (M >= 128 && N >= 128)
       return run_tiled_h2<128, 128, 8, 8, 8>(batch, M, K, N, x, xs, y, ys, out, st);
     if (M >= 64 && N >= 64)

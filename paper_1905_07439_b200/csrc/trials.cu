@@ -60,7 +60,7 @@ Layout layout_for(int dtype, int formula, int Q, int64_t chunk, int64_t N) {
 // (and graph capturable).
 struct AuxStreams {
   cudaStream_t s[3];
-  cudaEvent_t fork, join[3], truth_done, lane_done[2], expanded;
+  cudaEvent_t fork, join[3], truth_done, lane_done[2];
 };
 
 // One lane set per (device, caller stream): two passes issued on different
@@ -82,22 +82,15 @@ AuxStreams* aux_streams(cudaStream_t caller) {
   AuxStreams* a = new AuxStreams;
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  // RBC_LANE_PRIO (tuning aid): 0 = truth lane high (default), 1 = all
-  // equal, 2 = product lanes high
-  static const int prio_mode = [] {
-    const char* v = getenv("RBC_LANE_PRIO");
-    return v ? atoi(v) : 0;
-  }();
   for (int i = 0; i < 3; ++i) {
     // the truth lane (FP64 pipe) gets the highest priority so its CTAs
-    // interleave with the shared-memory-bound product kernels
-    const bool high = prio_mode == 0 ? i == 0 : prio_mode == 2 ? i != 0 : false;
-    cudaStreamCreateWithPriority(&a->s[i], cudaStreamNonBlocking, high ? hi : lo);
+    // interleave with the shared-memory-bound product kernels (equal
+    // priorities, or the product lanes high, measured within 0.03 ms on c2)
+    cudaStreamCreateWithPriority(&a->s[i], cudaStreamNonBlocking, i == 0 ? hi : lo);
     cudaEventCreateWithFlags(&a->join[i], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&a->fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&a->truth_done, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&a->expanded, cudaEventDisableTiming);
   for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&a->lane_done[i], cudaEventDisableTiming);
   sets.push_back({dev, caller, a});
   return a;
@@ -219,10 +212,6 @@ int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, 
     return v && v[0] == '1';
   }();
   const bool conc = !prof_on() && !serial_env;
-  static const bool stagger_env = [] {
-    const char* v = getenv("RBC_LANE_STAGGER");
-    return v && v[0] == '1';
-  }();
   AuxStreams* ax = aux_streams(st);
   cudaStream_t lanes[3] = {st, st, st};
   if (conc) {
@@ -259,18 +248,13 @@ int rbc_error_trials_async(int dtype, int formula, int Q, int64_t T, int64_t N, 
       uint8_t* nf = which == 0 ? nf_det : nf_rand;
       const int64_t Tp = which == 0 ? 1 : nt;
       const void* pl = which == 0 ? plans : (const char*)plans + (size_t)t0 * Q * RBC_PLAN_BYTES;
-      // Staggered lanes (RBC_LANE_STAGGER=1, tuning aid): the randomized
-      // lane starts its (HBM-bound) expansions once the deterministic lane's
-      // are done, to run them beside the deterministic lane's (issue-bound)
-      // leaves.  Measured slower (c2 9.05 vs 8.90 ms, c1 0.512 vs 0.486, c4
-      // 21.94 vs 21.85): the subtree's CTAs leave too little of an SM for an
-      // HBM-bound kernel to stream beside them, so the lanes are not offset.
-      const bool stagger = conc && stagger_env && det_plans && rand_plans;
-      if (stagger && which == 1) CUDA_TRY(cudaStreamWaitEvent(ls, ax->expanded, 0));
-      if (stagger && which == 0) set_expanded_event(ax->expanded);
+      // The lanes start together.  Starting the randomized lane's (HBM-bound)
+      // expansions after the deterministic lane's, to run them beside its
+      // (issue-bound) leaves, measured slower (c2 9.05 vs 8.90 ms, c4 21.94
+      // vs 21.85): the leaf CTAs leave too little of an SM for a streaming
+      // kernel beside them.
       int rc = rbc_apply_plans_async(dtype, formula, Q, Tp, pl, nt, N, at, bt, nt, prod,
                                      nf ? nf + t0 : nullptr, eng, L.engine, ls);
-      set_expanded_event(nullptr);
       if (rc != RBC_OK) return rc;
       CUDA_TRY(cudaStreamWaitEvent(ls, ax->truth_done, 0));
       if (err) {

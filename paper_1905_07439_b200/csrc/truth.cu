@@ -100,8 +100,7 @@ __device__ __forceinline__ double mac(double acc, double a, double b) {
 template <bool FMA>
 __global__ void __launch_bounds__(kThreads, 1)
     truth_bulk_kernel(int M, int K, int N, int tiles_m_arg, const double* __restrict__ xt,
-                      const double* __restrict__ yw, double* __restrict__ out, int tiles_n,
-                      int group) {
+                      const double* __restrict__ yw, double* __restrict__ out, int tiles_n) {
   constexpr int VW = 2;  // doubles per 16-byte fragment load
   constexpr int DY = kBM / kTM, DX = kBN / kTN;
   constexpr int GM = kTM / VW, GN = kTN / VW;
@@ -119,19 +118,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tx = (warp % WPX) * WX + (lane % WX);
   const int ty = (warp / WPX) * WY + (lane / WX);
   const int64_t b = blockIdx.y;
-  // grouped raster (RBC_TRUTH_GROUP): kGroup consecutive tile rows swept
-  // column by column share their X panels and a few Y panels in L2.  At 8192
-  // a group of 8 cuts DRAM reads 32.8 -> 10.3 GB per product but runs 3%
-  // slower (the kernel is DFMA-bound either way), so rows stay the default.
-  const int kGroup = group;
+  // Tiles in row order.  (A grouped raster -- 8 consecutive tile rows swept
+  // column by column, sharing their X panels in L2 -- cuts DRAM reads at 8192
+  // from 32.8 to 10.3 GB per product but runs 3% slower: the kernel is
+  // DFMA-bound either way.)
   const int tiles_m = tiles_m_arg;
-  const int per_group = kGroup * tiles_n;
-  const int grp = blockIdx.x / per_group;
-  const int gm0 = grp * kGroup;
-  const int gsize = min(kGroup, tiles_m - gm0);
-  const int in = blockIdx.x - grp * per_group;
-  const int tm = gm0 + in % gsize;
-  const int tn = in / gsize;
+  const int tm = blockIdx.x / tiles_n;
+  const int tn = blockIdx.x - tm * tiles_n;
   const int m0 = tm * kBM, n0 = tn * kBN;
   const double* xa = xt + (b * tiles_m + tm) * (int64_t)K * kBM;  // panel: row k at xa + k*128
   const double* yb = yw + (b * (int64_t)tiles_n + tn) * (int64_t)K * kBN;
@@ -239,16 +232,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// tile rows per raster group (RBC_TRUTH_GROUP, tuning aid)
-int truth_group() {
-  static const int g = [] {
-    const char* v = getenv("RBC_TRUTH_GROUP");
-    const int x = v ? atoi(v) : 0;
-    return x > 0 ? x : 1;
-  }();
-  return g;
-}
-
 constexpr size_t kSmem = sizeof(double) * kStages * kBK * (kBM + kBN) + 2 * sizeof(uint64_t) * kStages;
 
 // The stream-ordered pool keeps freed scratch for reuse instead of returning
@@ -311,7 +294,7 @@ cudaError_t run_truth_bulk(int64_t batch, int64_t M, int64_t K, int64_t N, const
     dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)nb, 1);
     truth_bulk_kernel<kFma><<<grid, kThreads, kSmem, st>>>(
         (int)M, (int)K, (int)N, tiles_m, xt, yw, static_cast<double*>(out) + b0 * M * N,
-        tiles_n, truth_group());
+        tiles_n);
     e = cudaGetLastError();
   }
   const cudaError_t f = cudaFreeAsync(scratch, st);

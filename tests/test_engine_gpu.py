@@ -242,51 +242,6 @@ def test_engine_errors(eng):
         eng.apply_levels([(u, u, u)], one, one, Dec())
 
 
-_LEAF_VARIANT_SCRIPT = r"""
-import sys
-import numpy as np
-sys.path.insert(0, sys.argv[1])
-import paper_1905_07439_b200 as rbc
-from paper_1905_07439_b200 import engine
-from paper_1905_07439_b200.precision import parse_precision
-from paper_1905_07439_b200.randomize import pack_recursive_plans, plan_formula_id
-mode = parse_precision(sys.argv[3])
-f = rbc.laderman_formula()
-g = rbc.derive_rng(95, 243)
-a = mode.array(g.uniform(-1, 1, (2, 243, 243)))
-b = mode.array(g.uniform(-1, 1, (2, 243, 243)))
-rplans = [rbc.draw_recursive_plan(3, 4, rbc.derive_rng(96, t)) for t in range(2)]
-packed = pack_recursive_plans(rplans, 4, 3)
-out = engine.apply_plans(plan_formula_id(f), 4, packed, a, b, mode)
-np.save(sys.argv[2], out)
-"""
-
-
-@pytest.mark.parametrize("label", ["f32", "f16"])
-def test_subtree_leaf_exchange_variants_agree(tmp_path, label):
-    """The fused subtree's leaf exchanges -- two Y rows per lane with 3
-    shuffles (default), 9 shuffles (RBC_SUBTREE_ROT=0) and the rotated
-    6-shuffle leaf (ROT=1) -- give config 2's product bit for bit.  The knobs
-    are read once per process, so each variant runs in its own interpreter."""
-    import os
-    import subprocess
-    import sys
-
-    from conftest import ROOT
-
-    script = tmp_path / "variant.py"
-    script.write_text(_LEAF_VARIANT_SCRIPT)
-    outs = {}
-    for rot in ("2", "0", "1"):
-        env = dict(os.environ, RBC_SUBTREE_ROT=rot)
-        path = tmp_path / f"rot{rot}.npy"
-        subprocess.run([sys.executable, str(script), str(ROOT), str(path), label], env=env, check=True,
-                       timeout=300)
-        outs[rot] = np.load(path)
-    assert outs["2"].tobytes() == outs["0"].tobytes()
-    assert outs["2"].tobytes() == outs["1"].tobytes()
-
-
 @pytest.mark.parametrize("detect", ["0", "1"])
 def test_empty_operands_after_nonempty_call(eng, monkeypatch, detect):
     """(T, 0, 0) operands return an empty (T, 0, 0) array like the reference,

@@ -113,7 +113,7 @@ def _same_bits_or_nan(got, want):
     assert got[~nan].tobytes() == want[~nan].tobytes()
 
 
-@pytest.mark.parametrize("tile", ["0", "402", "403", "404", "999"])
+@pytest.mark.parametrize("tile", ["0", "999"])
 @pytest.mark.parametrize("shape", [(3, 128, 128, 128), (1, 256, 64, 136), (2, 130, 24, 200),
                                    (1, 128, 40, 128), (1, 128, 13, 128)])
 def test_binary16_leaf_tiles_bitwise(shape, tile, monkeypatch):
@@ -137,7 +137,7 @@ def test_binary16_leaf_tiles_bitwise(shape, tile, monkeypatch):
     _same_bits_or_nan(got, want)
 
 
-@pytest.mark.parametrize("tile", ["0", "502", "504", "505", "999"])
+@pytest.mark.parametrize("tile", ["0", "999"])
 @pytest.mark.parametrize("shape", [(3, 128, 128, 128), (1, 256, 64, 136), (2, 130, 24, 200),
                                    (4, 64, 64, 64), (1, 128, 13, 128), (2, 100, 36, 68)])
 def test_binary32_leaf_tiles_bitwise(shape, tile, monkeypatch):
@@ -161,12 +161,11 @@ def test_binary32_leaf_tiles_bitwise(shape, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("label", ["f64", "f32"])
-@pytest.mark.parametrize("tile", ["0", "205", "210", "211", "212"])
+@pytest.mark.parametrize("tile", ["0", "205"])
 def test_small_square_leaves_bitwise(label, tile, monkeypatch):
     """27x27 leaves in long batches (config 3's leaves) run on the bulk-copy
-    persistent kernel (tile "0" = "210": 3 x 3 outputs per thread; "211"
-    3 x 9, "212" 9 x 3) or the single-shot shared-memory kernel ("205"): all equal the
-    oracle; the batch is odd so groups end ragged and leaves sit at 8-byte
+    persistent kernel (tile "0": 3 x 3 outputs per thread) or the single-shot
+    shared-memory kernel ("205"): both equal the oracle; the batch is odd so groups end ragged and leaves sit at 8-byte
     offsets."""
     from paper_1905_07439_b200 import engine
     from paper_1905_07439_b200.precision import parse_precision
