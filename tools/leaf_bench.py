@@ -39,6 +39,7 @@ def main():
         x = torch.randn(batch, m, m, device="cuda").to(TORCH[di])
         y = torch.randn(batch, m, m, device="cuda").to(TORCH[di])
         out = torch.empty(batch, m, m, device="cuda", dtype=TORCH[do])
+        first = None
         for t in tiles:
             os.environ["RBC_LEAF_TILE"] = t
             st = torch.cuda.current_stream()
@@ -47,7 +48,11 @@ def main():
                                                ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
                                                ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream))
                 _lib.check(rc)
+            out.zero_()
             run(); torch.cuda.synchronize()
+            if first is None:
+                first = out.clone()
+            same = torch.equal(out.view(torch.uint8), first.view(torch.uint8))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(5):
@@ -55,7 +60,7 @@ def main():
             e1.record(); torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 5
             tf = 2.0 * batch * m ** 3 / (ms / 1e3) / 1e12
-            print(f"{label:24s} tile={t:>4s} {ms:9.3f} ms {tf:7.2f} TFLOP/s", flush=True)
+            print(f"{label:24s} tile={t:>4s} {ms:9.3f} ms {tf:7.2f} TFLOP/s  bits==first:{same}", flush=True)
 
 
 if __name__ == "__main__":
