@@ -127,6 +127,13 @@ int rbc_rescaled_multiply(int dtype, int formula, int Q, const int32_t* n, const
                           int nsteps, const int32_t* steps, int64_t N, const void* a,
                           const void* b, void* out);
 
+/* experiments._rel_errors (reference experiments.py:258-261) on host buffers:
+ * err[t] = ||widen(c[t]) - ref[t or 0]||_F / ||ref[t or 0]||_F in binary64;
+ * c: (T, N, N) in the mode, ref: (N, N) (ref_tstride 0) or (T, N, N) binary64.
+ * Copies H2D, reduces on the device, copies the T errors back. */
+int rbc_rel_errors(int dtype, int64_t T, int64_t N, const void* c, const double* ref,
+                   int64_t ref_tstride, double* err);
+
 /* ---- device-pointer twins (stream ordered, no synchronisation) ------------ */
 
 size_t rbc_levels_workspace_bytes(int dtype, int Q, const int32_t* n, const int32_t* R,

@@ -32,7 +32,7 @@ from .formula import (
     strassen_formula,
 )
 from .matgen import MATRIX_KINDS, MatrixSpec, generate
-from .multiply import apply_bc, crop, mode_tensors, pad_to_shape, recursive_apply, standard_multiply
+from .multiply import apply_bc, mode_tensors, recursive_apply, standard_multiply
 from .precision import DOUBLE, HALF, SINGLE, Mode, parse_precision
 from .randomize import (
     VARIANTS,

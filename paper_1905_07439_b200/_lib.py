@@ -43,6 +43,7 @@ EXPORTS = (
     "rbc_truth_async",
     "rbc_rel_errors_scratch_bytes",
     "rbc_rel_errors_async",
+    "rbc_rel_errors",
     "rbc_nonfinite_async",
     "rbc_error_trials",
     "rbc_error_trials_workspace_bytes",
@@ -82,6 +83,7 @@ def _declare(lib):
              c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_u64p],
         ),
         "rbc_leaf_matmul": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+        "rbc_rel_errors": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp]),
         "rbc_pack_plans": (c_int, [c_int, c_i64, c_vp, c_vp, c_vp]),
         "rbc_apply_plans": (
             c_int,

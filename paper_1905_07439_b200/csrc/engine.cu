@@ -912,6 +912,32 @@ int rbc_rescaled_multiply(int dtype, int formula, int Q, const int32_t* n, const
   return RBC_OK;
 }
 
+int rbc_rel_errors(int dtype, int64_t T, int64_t N, const void* c, const double* ref,
+                   int64_t ref_tstride, double* err) {
+  if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);
+  if (ref_tstride != 0 && ref_tstride != N * N)
+    return set_error(RBC_EVALUE, "ref_tstride must be 0 or N*N");
+  if (T == 0) return RBC_OK;
+  RBC_TRY(check_device());
+  const size_t N2 = (size_t)N * N;
+  const size_t cb = (size_t)T * N2 * dtype_size(dtype);
+  const size_t rb = (ref_tstride ? (size_t)T : 1) * N2 * sizeof(double);
+  const size_t eb = (size_t)T * sizeof(double);
+  const size_t sb = error_scratch_bytes(T);
+  std::lock_guard<std::mutex> lock(arena().mu);
+  RBC_TRY(arena().reserve(align_up(cb) + align_up(rb) + align_up(eb) + align_up(sb) + 1024));
+  Arena& A = arena();
+  void* dc = A.take(cb);
+  double* dref = (double*)A.take(rb);
+  double* derr = (double*)A.take(eb);
+  void* dscratch = A.take(sb);
+  CUDA_TRY(cudaMemcpy(dc, c, cb, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dref, ref, rb, cudaMemcpyHostToDevice));
+  RBC_TRY(finish_sync(rbc_rel_errors_async(dtype, T, N, dc, dref, ref_tstride, derr, dscratch, nullptr)));
+  CUDA_TRY(cudaMemcpy(err, derr, eb, cudaMemcpyDeviceToHost));
+  return RBC_OK;
+}
+
 int rbc_leaf_matmul(int dtype, int64_t batch, int64_t xs, int64_t ys, int64_t M, int64_t K,
                     int64_t N, const void* x, const void* y, void* out) {
   if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);

@@ -26,7 +26,8 @@ import numpy as np
 from . import _lib
 from .precision import dtype_code, mode_of
 
-__all__ = ["apply_levels", "leaf_matmul", "apply_plans", "pack_plans", "install", "uninstall"]
+__all__ = ["apply_levels", "leaf_matmul", "apply_plans", "pack_plans", "rel_errors", "install",
+           "uninstall"]
 
 
 def _ptr(a: np.ndarray) -> ctypes.c_void_p:
@@ -386,20 +387,79 @@ def truth(A, B, mode, device="cuda:0") -> np.ndarray:
     return ref.cpu().numpy()
 
 
+def rel_errors(results, ref, refnorm, mode) -> np.ndarray:
+    """Per-trial relative Frobenius errors of a (T, N, N) mode-typed stack
+    against the binary64 product ``ref`` -- the reference's
+    ``experiments._rel_errors(results, ref, refnorm, mode)``
+    (experiments.py:258-261), reduced on the device (C ABI rbc_rel_errors).
+
+    ``refnorm`` is accepted for the reference's signature; the device computes
+    ||ref||_F itself in binary64 (it differs from ``np.linalg.norm`` by an ulp
+    at most, like one BLAS from another)."""
+    del refnorm
+    m = mode_of(mode)
+    res = _as_mode_array(results, np.dtype(m.dtype))
+    ref = np.ascontiguousarray(ref, dtype=np.float64)
+    if res.ndim != 3 or ref.shape != res.shape[1:] or res.shape[1] != res.shape[2]:
+        raise ValueError("results must be (T, N, N) and ref (N, N)")
+    T, N, _ = res.shape
+    err = np.empty(T, dtype=np.float64)
+    rc = _lib.load().rbc_rel_errors(dtype_code(m), T, N, _ptr(res), _ptr(ref), 0, _ptr(err))
+    _lib.check(rc)
+    return err
+
+
 _saved = {}
+_saved_wide = []
 
 
-def install(module=None):
+def _install_wide() -> None:
+    """Also route the reference's callers of the engine -- the L2 entry points
+    of SURVEY §8 rows a9, a10, a12 and §8f row 2 -- to this package's mirrors,
+    which hand plans to the device instead of hatted tables (no host hatting,
+    no table recognition) and reduce the errors on the device."""
+    import randbc.experiments as rexp  # noqa: PLC0415
+    import randbc.multiply as rmul  # noqa: PLC0415
+    import randbc.randomize as rrand  # noqa: PLC0415
+    import randbc.rescale as rresc  # noqa: PLC0415
+
+    from . import multiply, randomize, rescale  # noqa: PLC0415
+
+    targets = {
+        "recursive_randomized_apply_many": randomize.recursive_randomized_apply_many,
+        "recursive_randomized_apply": randomize.recursive_randomized_apply,
+        "randomized_apply": randomize.randomized_apply,
+        "recursive_apply": multiply.recursive_apply,
+        "rescaled_multiply": rescale.rescaled_multiply,
+        "_rel_errors": rel_errors,
+    }
+    for mod in (rexp, rmul, rrand, rresc):
+        for name, fn in targets.items():
+            if hasattr(mod, name):
+                _saved_wide.append((mod, name, getattr(mod, name)))
+                setattr(mod, name, fn)
+
+
+def install(module=None, wide: bool = False):
     """Route ``randbc._engine.apply_levels`` / ``leaf_matmul`` to the GPU.
 
     ``module`` defaults to ``randbc._engine`` (the reference must be
     importable).  Returns the module; ``uninstall`` restores the originals.
+
+    ``wide=True`` additionally replaces the reference's L2 functions
+    (``recursive_randomized_apply[_many]``, ``randomized_apply``,
+    ``recursive_apply``, ``rescaled_multiply``) and
+    ``experiments._rel_errors`` in every reference module that binds them, so
+    a whole ``run_experiment`` keeps plans, scalings and error reductions on
+    the device side of the C ABI.
     """
     if module is None:
         import randbc._engine as module  # noqa: PLC0415  (reference package)
     _saved[id(module)] = (module, module.apply_levels, module.leaf_matmul)
     module.apply_levels = apply_levels
     module.leaf_matmul = leaf_matmul
+    if wide:
+        _install_wide()
     return module
 
 
@@ -409,3 +469,6 @@ def uninstall(module=None) -> None:
     saved = _saved.pop(id(module), None)
     if saved is not None:
         _, module.apply_levels, module.leaf_matmul = saved
+    while _saved_wide:
+        mod, name, fn = _saved_wide.pop()
+        setattr(mod, name, fn)
