@@ -64,6 +64,44 @@ __global__ void __launch_bounds__(256) mixed(u64* out, float seed, u64 negz, int
   }
 }
 
+// same split, the non-DFMA warps run 32-bit integer multiply-add / xor chains
+__global__ void __launch_bounds__(256) mixed_int(u64* out, unsigned seed, int num, int den, int iti,
+                                                 int it64) {
+  const int warp = threadIdx.x >> 5;
+  if ((warp % den) < num) {
+    unsigned a[kChains];
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) a[i] = threadIdx.x * 2654435761u + i * 40503u + seed;
+    for (int it = 0; it < iti; ++it) {
+#pragma unroll
+      for (int i = 0; i < kChains; ++i) {
+        a[i] = a[i] * 1664525u + 1013904223u;  // IMAD
+        a[i] ^= a[i] >> 7;                      // SHF + LOP3
+      }
+    }
+    unsigned s = 0;
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) s ^= a[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  } else {
+    double acc[kChains], a[kChains];
+    const double b = seed * 1e-3;
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) {
+      acc[i] = 0.0;
+      a[i] = 1.0 + threadIdx.x * 1e-3 + i * 1e-4;
+    }
+    for (int it = 0; it < it64; ++it) {
+#pragma unroll
+      for (int i = 0; i < kChains; ++i) acc[i] = __fma_rn(acc[i], b, a[i]);
+    }
+    double s = acc[0];
+#pragma unroll
+    for (int i = 1; i < kChains; ++i) s += acc[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = __double_as_longlong(s);
+  }
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -96,6 +134,26 @@ int main() {
     printf("%s{\"f32_warps\": \"%d/%d\", \"it32\": %d, \"it64\": %d, \"ms\": %.3f, \"f32x2_tflops\": %.2f, "
            "\"dfma_tflops\": %.2f}",
            c ? ",\n " : "", num, den, it32, it64, best, t32, t64);
+  }
+  printf("]\n");
+  // DFMA beside integer chains: ms alone and mixed
+  const int icfg[][4] = {{1, 2, 8192, 0}, {1, 2, 0, 8192}, {1, 2, 8192, 8192}, {1, 2, 16384, 8192},
+                         {1, 2, 4096, 8192}};
+  printf("[");
+  for (int c = 0; c < 5; ++c) {
+    const int num = icfg[c][0], den = icfg[c][1], iti = icfg[c][2], it64 = icfg[c][3];
+    float best = 1e30f;
+    for (int r = 0; r < 6; ++r) {
+      cudaEventRecord(e0);
+      mixed_int<<<blocks, threads>>>((u64*)buf, 1u, num, den, iti, it64);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r && ms < best) best = ms;
+    }
+    printf("%s{\"int_warps\": \"%d/%d\", \"it_int\": %d, \"it64\": %d, \"ms\": %.3f}", c ? ",\n " : "",
+           num, den, iti, it64, best);
   }
   printf("]\n");
   cudaError_t e = cudaGetLastError();
