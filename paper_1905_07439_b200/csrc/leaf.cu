@@ -779,10 +779,14 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 #pragma unroll
     for (int j = 0; j < TN2; ++j) {
       const int gn = n0 + tx * TN + 2 * j;
-      if (gn + 1 < N) {
-        *reinterpret_cast<__half2*>(&ob[(int64_t)gm * N + gn]) = acc[i][j];
-      } else if (gn < N) {
-        ob[(int64_t)gm * N + gn] = __low2half(acc[i][j]);
+      __half* o = &ob[(int64_t)gm * N + gn];
+      // one 4-byte store where the pair is aligned (odd N puts every other
+      // row, and odd M * N every other leaf, on a 2-byte boundary)
+      if (gn + 1 < N && (reinterpret_cast<uintptr_t>(o) & 3) == 0) {
+        *reinterpret_cast<__half2*>(o) = acc[i][j];
+      } else {
+        if (gn < N) o[0] = __low2half(acc[i][j]);
+        if (gn + 1 < N) o[1] = __high2half(acc[i][j]);
       }
     }
   }
