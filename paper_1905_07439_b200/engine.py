@@ -310,6 +310,10 @@ def apply_plans(formula_id: int, Q: int, packed: np.ndarray, a, b, mode, stats=N
 
 
 def _vp(t):
+    """Device pointer of a torch tensor handed to the C ABI, which assumes
+    dense row-major storage: a strided view would be read as garbage."""
+    if not t.is_contiguous():
+        raise ValueError("device tensors passed to librbc must be contiguous")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -349,7 +353,7 @@ class DeviceEngine:
         n_arr = (ctypes.c_int32 * Q)(*[lv[0].shape[2] for lv in levels])
         R_arr = (ctypes.c_int32 * Q)(*[lv[0].shape[1] for lv in levels])
         Tc = (ctypes.c_int64 * Q)(*[lv[0].shape[0] for lv in levels])
-        ptrs = [(ctypes.c_void_p * Q)(*[lv[k].data_ptr() for lv in levels]) for k in range(3)]
+        ptrs = [(ctypes.c_void_p * Q)(*[_vp(lv[k]).value for lv in levels]) for k in range(3)]
         lib = _lib.load()
         ws = self._workspace(lib.rbc_levels_workspace_bytes(self.code, Q, n_arr, R_arr, T, N))
         rc = lib.rbc_apply_levels_async(

@@ -179,7 +179,9 @@ def plan_levels(f: BilinearFormula, plans, mode):
         return g * (S[:, a][:, :, None] * S[:, b][:, None, :])[:, None]
 
     uh, vh, wh = hat(f.u, 0, 1), hat(f.v, 1, 2), hat(f.w, 0, 2) * c
-    return m.array(uh), m.array(vh), m.array(wh)
+    # C-contiguous (T, R, n, n): the gathers leave an (R, T, ...) memory order
+    # that a dtype conversion preserves, and device uploads keep strides
+    return tuple(np.ascontiguousarray(m.array(t)) for t in (uh, vh, wh))
 
 
 _plan_level_alias = plan_levels  # reference name: _plan_levels
@@ -281,7 +283,8 @@ def _hatted_batch(f, perms, signs, m):
         g = np.moveaxis(g, 0, 1)
         return g * (signs[:, a][:, :, None] * signs[:, b][:, None, :])[:, None]
 
-    return m.array(hat(f.u, 0, 1)), m.array(hat(f.v, 1, 2)), m.array(hat(f.w, 0, 2) * c)
+    return tuple(np.ascontiguousarray(m.array(t))
+                 for t in (hat(f.u, 0, 1), hat(f.v, 1, 2), hat(f.w, 0, 2) * c))
 
 
 def enumerate_expectation(f, A, B, mode=DOUBLE, chunk_elements: int = DEFAULT_CHUNK_ELEMENTS,

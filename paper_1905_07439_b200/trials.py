@@ -123,7 +123,8 @@ class DeviceAverageTrials:
         out = []
         for q in range(self.Q):
             u, v, w = plan_levels(self.f, [rp.levels[q] for rp in rplans], self.m)
-            out.append(tuple(self.torch.from_numpy(t).to(self.device) for t in (u, v, w)))
+            out.append(tuple(self.torch.from_numpy(np.ascontiguousarray(t)).to(self.device)
+                             for t in (u, v, w)))
         return out
 
     def capture(self, a, b, tables, with_det: bool = True):
@@ -141,7 +142,11 @@ class DeviceAverageTrials:
         torch = self.torch
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         Q = self.Q
-        vp = lambda ts: (ctypes.c_void_p * Q)(*[t.data_ptr() for t in ts])  # noqa: E731
+        def vp(ts):
+            if not all(t.is_contiguous() for t in ts):
+                raise ValueError("coefficient tables must be contiguous (T, R, n, n) tensors")
+            return (ctypes.c_void_p * Q)(*[t.data_ptr() for t in ts])
+
         u = vp([tb[0] for tb in tables])
         v = vp([tb[1] for tb in tables])
         w = vp([tb[2] for tb in tables])

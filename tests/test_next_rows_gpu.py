@@ -28,7 +28,8 @@ def _oracle_expectation(f, A, B, mode):
 
 
 @pytest.mark.parametrize("label,which,size", [("f64", "strassen", 4), ("f32", "strassen", 6),
-                                              ("f64", "perturbed", 4)])
+                                              ("f64", "perturbed", 4), ("f32", "perturbed", 6),
+                                              ("f16", "perturbed", 4)])
 def test_enumerate_expectation_matches_oracle(label, which, size):
     import paper_1905_07439_b200 as rbc
     from paper_1905_07439_b200.precision import parse_precision

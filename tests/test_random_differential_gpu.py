@@ -206,3 +206,108 @@ def test_truth_random_shapes_bitwise(eng, seed):
     for t in range(T):
         want = oracle.standard_multiply(A[t].astype(np.float64), B[t].astype(np.float64))
         assert got[t].tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_rescaled_multiply_random_problem_bitwise(seed):
+    """Device-resident diagonal rescaling (csrc/rescale.cu) on random sizes,
+    schedules, modes and formulas (exact and perturbed) against the CPU oracle
+    of reference rescale.py:36-99."""
+    import paper_1905_07439_b200 as rbc
+    from oracle import rescale as oracle_rescale
+    from paper_1905_07439_b200 import _lib
+    from paper_1905_07439_b200.formula import perturb
+    from paper_1905_07439_b200.multiply import mode_tensors
+    from paper_1905_07439_b200.rescale import INSIDE, OUTSIDE, rescaled_multiply
+
+    _lib.require_device()
+    g = np.random.default_rng(6000 + seed)
+    mode = mode_for(LABELS[seed % 3])
+    f = rbc.strassen_formula() if seed % 2 else rbc.laderman_formula()
+    if seed % 4 >= 2:
+        f = perturb(f, 1e-3, 2, rbc.derive_rng(6000 + seed, 0))
+    Q = int(g.integers(0, 4 if f.n == 2 else 3))
+    N = int(g.integers(1, 6)) * f.n ** Q
+    schedule = tuple(g.choice([OUTSIDE, INSIDE], size=int(g.integers(0, 5))))
+    scale = np.exp(g.uniform(-2, 2, size=(N, 1)))
+    A = mode.array(g.standard_normal((N, N)) * scale)
+    B = mode.array(g.standard_normal((N, N)) * scale.T)
+    u, v, w = (t[0] for t in mode_tensors(f, mode))
+    try:
+        with np.errstate(all="ignore"):
+            want = oracle_rescale.rescaled_multiply(A, B, Q, schedule, mode, u, v, w)
+    except (OverflowError, ValueError) as exc:
+        with pytest.raises(type(exc)):
+            rescaled_multiply(A, B, Q, schedule, mode, f)
+        return
+    got = rescaled_multiply(A, B, Q, schedule, mode, f)
+    assert got.dtype == want.dtype and np.array_equal(got, want, equal_nan=True)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_device_matgen_random_draws_bitwise(seed):
+    """The device generator (Philox4x64-10 + numpy's ziggurat, csrc/matgen.cu)
+    on random sizes (odd ones too), families, modes and seeds against the host
+    draw through numpy (reference matgen.py:55-97)."""
+    from paper_1905_07439_b200 import _lib
+    from paper_1905_07439_b200.matgen import BUILDER_KINDS, MATRIX_KINDS, MatrixSpec, generate, generate_device
+
+    _lib.require_device()
+    g = np.random.default_rng(7000 + seed)
+    mode = mode_for(LABELS[seed % 3])
+    kinds = MATRIX_KINDS + BUILDER_KINDS
+    kind = kinds[seed % len(kinds)]
+    n = int(g.choice([2, 3, 4, 7, 16, 31, 64, 100, 129, 257]))
+    if kind == "quadrant100":
+        n += n % 2
+    seeds = [int(s) for s in g.integers(0, 2 ** 63, size=int(g.integers(1, 5)))]
+    try:
+        want = [[mode.array(m) for m in generate(MatrixSpec(kind, n, s))] for s in seeds]
+    except OverflowError:
+        with pytest.raises(OverflowError):
+            generate_device(kind, n, seeds, mode)
+        return
+    A, B = generate_device(kind, n, seeds, mode)
+    for i in range(len(seeds)):
+        assert A[i].cpu().numpy().tobytes() == np.ascontiguousarray(want[i][0]).tobytes(), (kind, n, i)
+        assert B[i].cpu().numpy().tobytes() == np.ascontiguousarray(want[i][1]).tobytes(), (kind, n, i)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_average_trials_random_problem_vs_oracle(seed):
+    """The averaging pipeline (dense tables, running binary64 mean at the
+    reference's checkpoints, experiments.py:264-296) on random small problems."""
+    import paper_1905_07439_b200 as rbc
+    from paper_1905_07439_b200 import _lib
+    from paper_1905_07439_b200.formula import perturb
+    from paper_1905_07439_b200.multiply import mode_tensors
+    from paper_1905_07439_b200.trials import average_trials, checkpoint_grid
+
+    _lib.require_device()
+    g = np.random.default_rng(8000 + seed)
+    mode = mode_for(LABELS[seed % 2])  # f64 / f32
+    base = rbc.strassen_formula() if seed % 2 else rbc.laderman_formula()
+    f = perturb(base, 1e-3, 3, rbc.derive_rng(8000 + seed, 0))
+    Q = int(g.integers(1, 3))
+    N = int(g.integers(1, 4)) * f.n ** Q
+    P, G = int(g.integers(1, 4)), int(g.integers(1, 14))
+    A, B = _operand(g, mode, P, N), _operand(g, mode, P, N)
+    rplans = [rbc.draw_recursive_plan(f.n, Q, rbc.derive_rng(8000 + seed, 1, t)) for t in range(P * G)]
+    got = average_trials(f, Q, A, B, mode, rplans, G)
+    cps = checkpoint_grid(G)
+    for p in range(P):
+        ref = oracle.standard_multiply(A[p].astype(np.float64), B[p].astype(np.float64))
+        refnorm = float(np.linalg.norm(ref.ravel()))
+        det = oracle.apply_levels([mode_tensors(f, mode)] * Q, A[p][None], B[p][None], mode)
+        assert np.isclose(got["err_det"][p], oracle.rel_errors(det, ref)[0], rtol=1e-12, atol=0)
+        mine = rplans[p * G:(p + 1) * G]
+        levels = [rbc.plan_levels(f, [rp.levels[q] for rp in mine], mode) for q in range(Q)]
+        C = oracle.apply_levels(levels, A[p][None], B[p][None], mode)
+        np.testing.assert_allclose(got["err_rand"][p], oracle.rel_errors(C, ref), rtol=1e-12)
+        total = np.zeros(ref.shape)
+        want = []
+        for t in range(G):
+            np.add(total, C[t].astype(np.float64), out=total)
+            if t + 1 in cps:
+                want.append(float(np.linalg.norm((total / (t + 1) - ref).ravel())) / refnorm)
+        np.testing.assert_allclose(got["err_mean"][p], want, rtol=1e-12)
