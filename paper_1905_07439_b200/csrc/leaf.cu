@@ -509,136 +509,150 @@ cudaError_t run_smem(int64_t batch, const void* x, int64_t xs, const void* y, in
   return cudaGetLastError();
 }
 
-// Persistent variant for long batches of small square leaves whose operand
-// type equals the accumulation type: LPB leaves per group arrive by bulk
-// copies (the TMA engine; each leaf's X and Y are copied as the 16-byte
-// aligned spans enclosing them) into a 2-stage ring completed on mbarriers,
-// issued by one thread one group ahead -- no load instructions in the
-// threads, loads overlap the FP work inside every CTA.  Same per-element
-// chains as leaf_smem_kernel.
-template <class T, int M, int TM, int TN>
-struct SmemBulk {
-  static_assert(M % TM == 0 && M % TN == 0, "leaf tiling");
-  static constexpr int TPL = (M / TM) * (M / TN);
-  static constexpr int LPB = 256 / TPL;
+// Long batches of small square leaves whose operand type equals the
+// accumulation type (config 3's 27 x 27 binary64 leaves): one warp per leaf,
+// TM x TN outputs per lane, leaves streamed through a CTA-wide ring of NSLOT
+// bulk-copy slots (the TMA engine; each leaf's X and Y are copied as the
+// 16-byte aligned spans enclosing them).  A producer lane fills the slots in
+// order behind per-slot "empty" mbarriers; consumer warp w takes leaves
+// w, w + NW, ... of the CTA's chunk behind the "full" mbarriers.  There is
+// no CTA barrier in the steady state and no load instruction from global
+// memory in the consumers.
+//
+// Why this shape: an 8-byte shared-memory load moves 256 bytes per warp, two
+// cycles of the 128 B/clk crossbar, whatever the broadcast; with 3 x 3
+// outputs per thread (6 loads per 9 multiply-adds) the crossbar was 93% busy
+// with the FP64 pipe at 56% (9.5 TFLOP/s, round-1/2 kernel, three leaves per
+// 243-thread CTA and a CTA barrier per group).  9 x 3 outputs need 12 loads
+// per 27 multiply-adds; 27 of a warp's 32 lanes then hold one whole leaf, so
+// a warp needs no partner and the ring replaces the barriers: 12.1 TFLOP/s
+// = 66% of DMUL+DADD at 5.4 TB/s = 83% of HBM, which is this leaf's tighter
+// roofline (2.25 flop per byte).  3 x 9 measured 10.1; k loops unrolled by 2
+// and 6 instead of fully: 8.2 and 9.2; 8 to 16 consumer warps equal.
+//
+// Slot release: the consumers read the slot through the generic proxy and
+// the refill writes it through the async proxy, so the arrive on "empty" is
+// preceded by fence.proxy.async.  Without it the compiler placed the arrive
+// right after the last LDS issue and the refill overtook loads still in
+// flight: about one wrong output row per 10^5 leaves (found with the
+// 3 x 9 variant, tools/experiments/leaf27_warp.cu).
+template <class T, int M, int NSLOT>
+struct LeafRing {
   static constexpr int E = M * M;
-  static constexpr int SPAN0 = ((E * (int)sizeof(T) + 16) + 15) / 16 * 16;
-  // bytes per operand slot, padded to 4 (mod 16) words for binary64: the
-  // same operand of consecutive leaves then sits 8 banks apart, so a warp
-  // that straddles two leaves reads their A rows without bank conflicts
-  static constexpr int SPAN =
-      sizeof(T) == 8 ? SPAN0 + ((4 - (SPAN0 / 4) % 16 + 16) % 16) * 4 : SPAN0;
-  static constexpr size_t stage_bytes = (size_t)LPB * 2 * SPAN;
-  static constexpr size_t smem = 2 * stage_bytes + 2 * sizeof(uint64_t);
+  static constexpr int SPAN = ((E * (int)sizeof(T) + 16) + 15) / 16 * 16;
+  static constexpr size_t smem = (size_t)NSLOT * 2 * SPAN + 2 * NSLOT * sizeof(uint64_t);
 };
 
-template <class T, int M, int TM, int TN, int PF = 1>
-__global__ void __launch_bounds__(256) leaf_smem_bulk_kernel(int64_t batch, const T* __restrict__ x,
-                                                             int64_t xs, const T* __restrict__ y,
-                                                             int64_t ys, T* __restrict__ out) {
-  using S = SmemBulk<T, M, TM, TN>;
-  constexpr int TPL = S::TPL, LPB = S::LPB, E = S::E;
+template <class T, int M, int TM, int TN, int NW, int NSLOT>
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    leaf_ring_kernel(int64_t batch, const T* __restrict__ x, int64_t xs, const T* __restrict__ y,
+                     int64_t ys, T* __restrict__ out) {
+  using S = LeafRing<T, M, NSLOT>;
   using A = Arith<T>;
-  extern __shared__ __align__(128) unsigned char bulk_smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(bulk_smem + 2 * S::stage_bytes);
-  const int64_t groups = (batch + LPB - 1) / LPB;
+  constexpr int E = S::E, SPAN = S::SPAN;
+  constexpr int CJ = M / TN;  // lanes along N; a lane's columns are jt + CJ * j
+  constexpr int TPL = (M / TM) * CJ;
+  static_assert(M % TM == 0 && M % TN == 0 && TPL <= 32, "one warp per leaf");
+  static_assert(M % 2 == 1, "the k loop below is written for odd M");
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring_smem + (size_t)NSLOT * 2 * SPAN);
+  uint64_t* empty = full + NSLOT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
     mbar_init_fence();
   }
   __syncthreads();
-  // operand slot (stage, leaf, which) and the element offset of the block in it
-  auto slot = [&](int stg, int l, int which) {
-    return bulk_smem + (size_t)stg * S::stage_bytes + (size_t)(l * 2 + which) * S::SPAN;
-  };
-  auto issue = [&](int64_t g, int stg) {  // one thread
-    const int64_t b0 = g * LPB;
-    const int nl = batch - b0 < LPB ? (int)(batch - b0) : LPB;
-    unsigned bytes = 0;
-    for (int l = 0; l < nl; ++l) {
-      bytes += span_bytes(x + (b0 + l) * xs, E * sizeof(T));
-      bytes += span_bytes(y + (b0 + l) * ys, E * sizeof(T));
+  // this CTA's leaves: one contiguous chunk
+  const int64_t per = (batch + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * per;
+  const int64_t hi = lo + per < batch ? lo + per : batch;
+  const int n = hi > lo ? (int)(hi - lo) : 0;
+  if (warp == NW) {  // producer
+    if (lane == 0) {
+      for (int i = 0; i < n; ++i) {
+        const int s = i % NSLOT, round = i / NSLOT;
+        if (round > 0) mbar_wait(&empty[s], (unsigned)((round - 1) & 1));
+        const T* gx = x + (lo + i) * xs;
+        const T* gy = y + (lo + i) * ys;
+        const unsigned bx = span_bytes(gx, E * sizeof(T)), by = span_bytes(gy, E * sizeof(T));
+        mbar_expect_tx(&full[s], bx + by);
+        unsigned char* slot = ring_smem + (size_t)s * 2 * SPAN;
+        bulk_g2s(slot, span_start(gx), bx, &full[s]);
+        bulk_g2s(slot + SPAN, span_start(gy), by, &full[s]);
+      }
+    }
+    return;
+  }
+  const int r = lane < TPL ? lane : 0;  // spare lanes shadow lane 0 and do not store
+  const int it = r / CJ, jt = r % CJ;
+  for (int i = warp; i < n; i += NW) {
+    const int s = i % NSLOT;
+    mbar_wait(&full[s], (unsigned)((i / NSLOT) & 1));
+    const T* gx = x + (lo + i) * xs;
+    const T* gy = y + (lo + i) * ys;
+    unsigned char* slot = ring_smem + (size_t)s * 2 * SPAN;
+    const T* Xr = reinterpret_cast<const T*>(slot + (reinterpret_cast<uintptr_t>(gx) & 15)) + TM * it * M;
+    const T* Yc = reinterpret_cast<const T*>(slot + SPAN + (reinterpret_cast<uintptr_t>(gy) & 15)) + jt;
+    // operands of step k + 1 load while step k multiplies (two register
+    // sets, k fully unrolled); every output keeps its sequential k chain
+    T acc[TM][TN], a[2][TM], b[2][TN];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int ii = 0; ii < TM; ++ii) a[h][ii] = Xr[ii * M + h];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[h][j] = Yc[h * M + CJ * j];
+    }
+#pragma unroll
+    for (int ii = 0; ii < TM; ++ii)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[ii][j] = A::mul(a[0][ii], b[0][j]);
+#pragma unroll
+    for (int k = 1; k < M; ++k) {
+      const int c = k & 1, nx = c ^ 1;
+      if (k + 1 < M) {
+#pragma unroll
+        for (int ii = 0; ii < TM; ++ii) a[nx][ii] = Xr[ii * M + k + 1];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) b[nx][j] = Yc[(k + 1) * M + CJ * j];
+      }
+#pragma unroll
+      for (int ii = 0; ii < TM; ++ii)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[ii][j] = A::add(acc[ii][j], A::mul(a[c][ii], b[c][j]));
     }
     fence_proxy_async();
-    mbar_expect_tx(&full[stg], bytes);
-    for (int l = 0; l < nl; ++l) {
-      const T* gx = x + (b0 + l) * xs;
-      const T* gy = y + (b0 + l) * ys;
-      bulk_g2s(slot(stg, l, 0), span_start(gx), span_bytes(gx, E * sizeof(T)), &full[stg]);
-      bulk_g2s(slot(stg, l, 1), span_start(gy), span_bytes(gy, E * sizeof(T)), &full[stg]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane < TPL) {
+      T* o = out + (lo + i) * (int64_t)E + TM * it * M + jt;
+#pragma unroll
+      for (int ii = 0; ii < TM; ++ii)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) o[ii * M + CJ * j] = acc[ii][j];
     }
-  };
-  const int l = threadIdx.x / TPL;
-  const int r = threadIdx.x - l * TPL;
-  const int ti = (r / (M / TN)) * TM, tj = (r % (M / TN)) * TN;
-  int64_t g = blockIdx.x;
-  if (threadIdx.x == 0 && g < groups) issue(g, 0);
-  for (int it = 0; g < groups; g += gridDim.x, ++it) {
-    const int stg = it & 1;
-    if (threadIdx.x == 0 && g + gridDim.x < groups) issue(g + gridDim.x, stg ^ 1);
-    mbar_wait(&full[stg], (unsigned)((it >> 1) & 1));
-    const int64_t b0 = g * LPB;
-    const int nl = batch - b0 < LPB ? (int)(batch - b0) : LPB;
-    if (l < nl) {
-      const T* gx = x + (b0 + l) * xs;
-      const T* gy = y + (b0 + l) * ys;
-      const T* Xs = reinterpret_cast<const T*>(slot(stg, l, 0) + (reinterpret_cast<uintptr_t>(gx) & 15));
-      const T* Ys = reinterpret_cast<const T*>(slot(stg, l, 1) + (reinterpret_cast<uintptr_t>(gy) & 15));
-      // operands of step k + PF are loaded while step k multiplies (k fully
-      // unrolled, a ring of PF + 1 register slots); every output keeps its
-      // sequential k chain
-      constexpr int NS = PF + 1;
-      T acc[TM][TN], a[NS][TM], bb[NS][TN];
-#pragma unroll
-      for (int p = 0; p < PF && p < M; ++p) {
-#pragma unroll
-        for (int i = 0; i < TM; ++i) a[p][i] = Xs[(ti + i) * M + p];
-#pragma unroll
-        for (int j = 0; j < TN; ++j) bb[p][j] = Ys[p * M + tj + j];
-      }
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        const int c = k % NS;
-        if (k + PF < M) {
-          const int nx = (k + PF) % NS;
-#pragma unroll
-          for (int i = 0; i < TM; ++i) a[nx][i] = Xs[(ti + i) * M + k + PF];
-#pragma unroll
-          for (int j = 0; j < TN; ++j) bb[nx][j] = Ys[(k + PF) * M + tj + j];
-        }
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j)
-            acc[i][j] = k == 0 ? A::mul(a[c][i], bb[c][j]) : A::add(acc[i][j], A::mul(a[c][i], bb[c][j]));
-      }
-      T* o = out + (b0 + l) * (int64_t)E;
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) o[(ti + i) * M + tj + j] = acc[i][j];
-    }
-    __syncthreads();  // stage stg is refilled next iteration (issued above it)
   }
 }
 
-template <class T, int M, int TM, int TN, int PF = 1>
-cudaError_t run_smem_bulk(int64_t batch, const void* x, int64_t xs, const void* y, int64_t ys,
+template <class T, int M, int TM, int TN>
+cudaError_t run_leaf_ring(int64_t batch, const void* x, int64_t xs, const void* y, int64_t ys,
                           void* out, cudaStream_t st) {
-  using S = SmemBulk<T, M, TM, TN>;
-  auto kern = leaf_smem_bulk_kernel<T, M, TM, TN, PF>;
+  constexpr int NW = 12, NSLOT = 16;
+  using S = LeafRing<T, M, NSLOT>;
+  auto kern = leaf_ring_kernel<T, M, TM, TN, NW, NSLOT>;
   static const cudaError_t attr =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem);
   if (attr != cudaSuccess) return attr;
-  int per_sm = 0, dev = 0, sms = 148;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, S::smem);
-  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t groups = (batch + S::LPB - 1) / S::LPB;
-  const int64_t blocks = std::min<int64_t>(groups, (int64_t)sms * std::max(1, per_sm));
-  kern<<<(unsigned)blocks, 256, S::smem, st>>>(batch, (const T*)x, xs, (const T*)y, ys, (T*)out);
+  const int64_t blocks = std::min<int64_t>((batch + NW - 1) / NW, sms);
+  kern<<<(unsigned)blocks, (NW + 1) * 32, S::smem, st>>>(batch, (const T*)x, xs, (const T*)y, ys,
+                                                          (T*)out);
   return cudaGetLastError();
 }
 
@@ -648,12 +662,9 @@ template <class TIn, class TAcc>
 cudaError_t small_square(int64_t batch, int64_t M, const void* x, int64_t xs, const void* y,
                          int64_t ys, void* out, cudaStream_t st) {
   if constexpr (std::is_same<TIn, TAcc>::value && sizeof(TIn) >= 4) {
-    // 3 x 3 outputs per thread, 3 leaves per 243-thread CTA, 3 CTAs per SM
-    // (c3: 0.884 ms/launch; 3 x 9 outputs -- 12 loads per 27 multiply-adds
-    // instead of 6 per 9 -- fits one CTA per SM and ran slower, 1.13; operands
-    // 2 or 3 k steps ahead measured equal)
+    // one warp per leaf, 9 x 3 outputs per lane (leaf_ring_kernel above)
     if (M == 27 && batch >= 2048 && tile_override() == 0)
-      return run_smem_bulk<TIn, 27, 3, 3>(batch, x, xs, y, ys, out, st);
+      return run_leaf_ring<TIn, 27, 9, 3>(batch, x, xs, y, ys, out, st);
   }
   switch (M) {
     case 27: return run_smem<TIn, TAcc, 27, 3>(batch, x, xs, y, ys, out, st);

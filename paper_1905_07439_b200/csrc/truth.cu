@@ -202,6 +202,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         kstep();
       }
     }
+    // The warp read stage s through the generic proxy and the refill writes
+    // it through the async proxy: order the two before the release (the
+    // compiler is free to place the arrive right after the last LDS issue,
+    // ahead of the DFMAs that wait for those loads; see leaf_ring_kernel).
+    fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     if (tid == 0 && kt + kStages < ktiles) {

@@ -163,10 +163,10 @@ def test_binary32_leaf_tiles_bitwise(shape, tile, monkeypatch):
 @pytest.mark.parametrize("label", ["f64", "f32"])
 @pytest.mark.parametrize("tile", ["0", "205"])
 def test_small_square_leaves_bitwise(label, tile, monkeypatch):
-    """27x27 leaves in long batches (config 3's leaves) run on the bulk-copy
-    persistent kernel (tile "0": 3 x 3 outputs per thread) or the single-shot
-    shared-memory kernel ("205"): both equal the oracle; the batch is odd so groups end ragged and leaves sit at 8-byte
-    offsets."""
+    """27x27 leaves in long batches (config 3's leaves) run on the warp-per-leaf
+    ring kernel (tile "0": 9 x 3 outputs per lane, bulk-copy slots) or the
+    single-shot shared-memory kernel ("205"): both equal the oracle; the batch
+    is odd so chunks end ragged and leaves sit at 8-byte offsets."""
     from paper_1905_07439_b200 import engine
     from paper_1905_07439_b200.precision import parse_precision
 
@@ -180,6 +180,49 @@ def test_small_square_leaves_bitwise(label, tile, monkeypatch):
     got = engine.leaf_matmul(x, y, mode)
     want = oracle.leaf(x, y)
     assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("label", ["f64", "f32"])
+def test_ring_leaves_long_batch_equal_single_shot(label, monkeypatch):
+    """The ring kernel's slot reuse on a config-3 sized batch (146,004 leaves:
+    every slot is refilled about 60 times per CTA), three launches, against the
+    single-shot kernel on the device and the oracle on a sample.  A release
+    that lets the refill overtake loads in flight shows up here as a few wrong
+    rows per launch."""
+    import ctypes
+
+    import torch
+
+    from paper_1905_07439_b200 import _lib
+    from paper_1905_07439_b200.precision import parse_precision
+
+    _lib.require_device()
+    lib = _lib.load()
+    mode = parse_precision(label)
+    code = {"f64": 0, "f32": 1}[label]
+    dt = {"f64": torch.float64, "f32": torch.float32}[label]
+    T = 12167 * 12
+    gen = torch.Generator(device="cuda").manual_seed(27)
+    x = torch.randn(T, 27, 27, device="cuda", dtype=dt, generator=gen)
+    y = torch.randn(T, 27, 27, device="cuda", dtype=dt, generator=gen)
+
+    def run(tile):
+        monkeypatch.setenv("RBC_LEAF_TILE", tile)
+        out = torch.full((T, 27, 27), float("nan"), device="cuda", dtype=dt)
+        st = torch.cuda.current_stream()
+        _lib.check(lib.rbc_leaf_matmul_async(code, code, T, 729, 729, 27, 27, 27,
+                                             ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
+        torch.cuda.synchronize()
+        return out
+
+    want = run("205")
+    for _ in range(3):
+        got = run("0")
+        assert torch.equal(got.view(torch.uint8), want.view(torch.uint8))
+    pick = [0, 1, 4098, T - 2, T - 1]
+    ref = oracle.leaf(mode.array(x[pick].cpu().numpy()), mode.array(y[pick].cpu().numpy()))
+    assert want[pick].cpu().numpy().tobytes() == ref.tobytes()
 
 
 def test_device_runner_matches_host_call():
