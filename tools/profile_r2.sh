@@ -26,7 +26,7 @@ for c in "$@"; do
     c5_expand) cap c5_expand c5 "expand_plan" 1 ;;
     c2_subtree) cap c2_subtree c2 subtree 2 ;;
     # per pair: the deterministic product (1 product) then the 32 randomized ones
-    c3_leaf) cap c3_leaf c3 leaf_smem 5 ;;
+    c3_leaf) cap c3_leaf c3 leaf_ring 5 ;;
     c3_expand) cap c3_expand c3 expand_dense 8 ;;
     c3_contract) cap c3_contract c3 contract_dense 3 ;;
     c4_leaf) cap c4_leaf c4 h2dup 1 ;;
