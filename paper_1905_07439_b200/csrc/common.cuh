@@ -167,6 +167,68 @@ template <class T, int W> struct PackOps {
   }
 };
 
+// binary32 packs of three (the 3 x 3 leaf rows of the fused subtree): elements
+// 0 and 1 travel as one f32x2 pair, element 2 as a scalar, so an add or a
+// subtract of a pack is two instructions instead of three.  Each packed lane
+// rounds exactly like the scalar instruction.  Negation of the pair is
+// fma(a, (-1, -1), (-0, -0)): exact, signed zeros included; the two constants
+// sit in constant memory so that ptxas sees run-time values (it would fold a
+// literal -0 addend and contract a packed multiply into the next add).
+__device__ __constant__ uint64_t kcF2NegZero = 0x8000000080000000ull;
+__device__ __constant__ uint64_t kcF2MinusOne = 0xbf800000bf800000ull;
+
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+#ifndef RBC_NO_F32X2_PACK3
+template <> struct PackOps<float, 3> {
+  using P = Pack<float, 3>;
+  static __device__ __forceinline__ uint64_t pr(const P& a) { return f2_pack(a.v[0], a.v[1]); }
+  static __device__ __forceinline__ P un(uint64_t p01, float c) {
+    P r;
+    r.v[0] = f2_lo(p01);
+    r.v[1] = f2_hi(p01);
+    r.v[2] = c;
+    return r;
+  }
+  static __device__ __forceinline__ P add(const P& a, const P& b) {
+    return un(f2_add(pr(a), pr(b)), __fadd_rn(a.v[2], b.v[2]));
+  }
+  static __device__ __forceinline__ P sub(const P& a, const P& b) {
+    return un(f2_sub(pr(a), pr(b)), __fsub_rn(a.v[2], b.v[2]));
+  }
+  static __device__ __forceinline__ P neg(const P& a) {
+    return un(f2_fma(pr(a), kcF2MinusOne, kcF2NegZero), -a.v[2]);
+  }
+  static __device__ __forceinline__ P mul_scalar(float c, const P& a) {
+    return un(f2_mul_bcast(c, pr(a), kcF2NegZero), __fmul_rn(c, a.v[2]));
+  }
+  static __device__ __forceinline__ P flip(const P& a, uint32_t m) {
+    P r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r.v[i] = flip_sign(a.v[i], m);
+    return r;
+  }
+  static __device__ __forceinline__ P select(bool c, const P& a, const P& b) {
+    P r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r.v[i] = c ? a.v[i] : b.v[i];
+    return r;
+  }
+  static __device__ __forceinline__ bool all_finite(const P& a) {
+    return isfinite(a.v[0]) && isfinite(a.v[1]) && isfinite(a.v[2]);
+  }
+};
+#endif
+
 #define RBC_HALF2_PACK(W)                                                              \
   template <> struct PackOps<__half, W> {                                              \
     using P = Pack<__half, W>;                                                         \

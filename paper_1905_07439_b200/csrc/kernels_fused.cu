@@ -721,12 +721,24 @@ subtree_reg_kernel(
           const P xg = F::template expand_u1<T, M>(xf, r2, xlr, xlc);
           const P yag = F::template expand_v1<T, M>(ya, r2, ylr, ylc);
           const P ycg = F::template expand_v1<T, M>(yc, r2, ylr, ylc);
-          P m;
+          P m, ybg;
 #pragma unroll
-          for (int j = 0; j < M; ++j) {
-            const T yb = shfl_val(yag.v[j], gbase + rb);
-            m.v[j] = A::add(A::add(A::mul(xg.v[0], yag.v[j]), A::mul(xg.v[1], yb)),
-                            A::mul(xg.v[2], ycg.v[j]));
+          for (int j = 0; j < M; ++j) ybg.v[j] = shfl_val(yag.v[j], gbase + rb);
+          if constexpr (std::is_same<T, float>::value && M == 3) {
+            // columns 0 and 1 as one f32x2 pair (each lane rounds like the
+            // scalar FMUL / FADD), column 2 scalar
+            using O3 = PackOps<float, 3>;
+            const uint64_t p01 = f2_add(
+                f2_add(f2_mul_bcast(xg.v[0], O3::pr(yag), kcF2NegZero),
+                       f2_mul_bcast(xg.v[1], O3::pr(ybg), kcF2NegZero)),
+                f2_mul_bcast(xg.v[2], O3::pr(ycg), kcF2NegZero));
+            m = O3::un(p01, A::add(A::add(A::mul(xg.v[0], yag.v[2]), A::mul(xg.v[1], ybg.v[2])),
+                                   A::mul(xg.v[2], ycg.v[2])));
+          } else {
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+              m.v[j] = A::add(A::add(A::mul(xg.v[0], yag.v[j]), A::mul(xg.v[1], ybg.v[j])),
+                              A::mul(xg.v[2], ycg.v[j]));
           }
           F::template contract_w_step<T, M>(z, m, r2);
         }
