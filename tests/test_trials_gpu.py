@@ -161,19 +161,20 @@ def test_binary32_leaf_tiles_bitwise(shape, tile, monkeypatch):
 
 
 @pytest.mark.parametrize("label", ["f64", "f32"])
-@pytest.mark.parametrize("tile", ["0", "205"])
-def test_small_square_leaves_bitwise(label, tile, monkeypatch):
+@pytest.mark.parametrize("tile,T", [("0", 4099), ("205", 4099), ("0", 2048), ("0", 2051), ("0", 3553)])
+def test_small_square_leaves_bitwise(label, tile, T, monkeypatch):
     """27x27 leaves in long batches (config 3's leaves) run on the warp-per-leaf
     ring kernel (tile "0": 9 x 3 outputs per lane, bulk-copy slots) or the
-    single-shot shared-memory kernel ("205"): both equal the oracle; the batch
-    is odd so chunks end ragged and leaves sit at 8-byte offsets."""
+    single-shot shared-memory kernel ("205"): both equal the oracle; odd batches
+    end the chunks ragged and put leaves at 8-byte offsets, 2048 is the
+    smallest batch the ring kernel takes (its last CTA gets no leaf), 2051 and
+    3553 leave CTAs with fewer leaves than consumer warps / a short last chunk."""
     from paper_1905_07439_b200 import engine
     from paper_1905_07439_b200.precision import parse_precision
 
     monkeypatch.setenv("RBC_LEAF_TILE", tile)
     mode = parse_precision(label)
     g = np.random.default_rng(27)
-    T = 4099
     x = mode.array(g.standard_normal((T, 27, 27)))
     y = mode.array(g.standard_normal((T, 27, 27)))
     x[7, :2, :] = -0.0
