@@ -742,32 +742,23 @@ class ErrorTrialWorkload:
         """Fresh inputs every step: the step's operand pairs drawn on the GPU
         (rbc_matgen from keys of the native SeedSequence), its plans drawn on
         the host (native draw_plan) and copied H2D, the error trials run, the
-        per-trial errors copied D2H; wall clock per step.  Pairs continue
-        after the resident set (no pair is reused)."""
+        per-trial errors copied D2H; wall clock per step over a run of steps
+        (trials.run_trial_set: the next step's pairs are drawn on a second
+        stream while a step computes).  Pairs continue after the resident set
+        (no pair is reused)."""
         import torch
 
-        from paper_1905_07439_b200.configs import make_pairs_device, packed_plans
+        from paper_1905_07439_b200.trials import run_trial_set
 
         cfg, T = self.cfg, len(self.pair_ids)
-        nxt = [self.pair_ids[-1] + 1]
+        p0 = self.pair_ids[-1] + 1
         dev = self.a.device
-        bufs = (torch.empty_like(self.a), torch.empty_like(self.b))  # drawn into every step
-
-        def step():
-            p0 = nxt[0]
-            nxt[0] += T
-            a, b = make_pairs_device(cfg, p0, T, dev, out=bufs)
-            pl = torch.from_numpy(packed_plans(cfg, [cfg.plan_key(p) for p in range(p0, p0 + T)]))
-            self.runner.run(a, b, pl.to(dev, non_blocking=True))
-            return self.runner.err_rand.cpu(), self.runner.err_det.cpu()
-
-        for _ in range(warmup):
-            step()
+        runners = {T: self.runner}
+        run_trial_set(cfg, p0, warmup * T, T, dev, True, runners)
         torch.cuda.synchronize()
         with no_gc():
             t0 = time.perf_counter()
-            for _ in range(steps):
-                step()
+            run_trial_set(cfg, p0 + warmup * T, steps * T, T, dev, True, runners)
             torch.cuda.synchronize()
             ms = (time.perf_counter() - t0) / steps * 1e3
         return ms
@@ -1110,44 +1101,35 @@ def time_to_solution(cfg, T_step, dev, rank, world, coll=None):
     import torch
 
     from paper_1905_07439_b200 import distributed
-    from paper_1905_07439_b200.configs import make_pairs_device
-    from paper_1905_07439_b200.configs import packed_plans
-    from paper_1905_07439_b200.trials import DeviceErrorTrials
 
     total = cfg.trials
     per = -(-total // world)
     lo, hi = 1 + rank * per, min(total, (rank + 1) * per)
-    f = cfg.formula_obj()
     runners = {}
-    errs = []
+    from paper_1905_07439_b200.trials import run_trial_set
 
-    def chunk(p0, cnt):
-        a, b = make_pairs_device(cfg, p0, cnt, dev)
-        packed = packed_plans(cfg, [cfg.plan_key(p) for p in range(p0, p0 + cnt)])
-        pl = torch.from_numpy(packed).to(dev)
-        if cnt not in runners:
-            runners[cnt] = DeviceErrorTrials(f, cfg.Q, cfg.N, cfg.mode, cnt, device=dev)
-        r = runners[cnt]
-        r.run(a, b, pl)
-        return np.stack([r.err_rand.cpu().numpy(), r.err_det.cpu().numpy()])
+    def whole(pipelined):
+        run_trial_set(cfg, lo, min(T_step, hi - lo + 1), T_step, dev, pipelined, runners)  # warm-up
+        torch.cuda.synchronize()
+        distributed.barrier_if(world)
+        t0 = time.perf_counter()
+        er, ed, _, _ = run_trial_set(cfg, lo, hi - lo + 1, T_step, dev, pipelined, runners)
+        sec = time.perf_counter() - t0
+        return float(distributed.max_over_ranks([sec], device=coll)[0]), np.stack([er, ed])
 
-    chunk(lo, min(T_step, hi - lo + 1))  # warm-up (kernel attributes, pools)
-    torch.cuda.synchronize()
-    distributed.barrier_if(world)
-    t0 = time.perf_counter()
-    for p0 in range(lo, hi + 1, T_step):
-        errs.append(chunk(p0, min(T_step, hi - p0 + 1)))
-    torch.cuda.synchronize()
-    sec = time.perf_counter() - t0
-    sec = float(distributed.max_over_ranks([sec], device=coll)[0])
-    e = np.concatenate(errs, axis=1)
+    serial_sec, e_serial = whole(False)
+    sec, e = whole(True)
+    same = bool(np.array_equal(e, e_serial, equal_nan=True))
     if total % world == 0:  # equal shards: gather in rank (= pair) order
         e = distributed.gather_trials(e, device=coll)
     return {
         "pairs": total, "products": 2 * total, "seconds": round(sec, 3), "scaling": "strong",
         "n_gpus": world, "pairs_per_launch": T_step,
         "what": "wall clock, all pairs: device input generation, plans, binary64 truth, "
-                "deterministic + randomized products, errors copied to the host (max over ranks)",
+                "deterministic + randomized products, errors copied to the host (max over ranks); "
+                "the next pass's inputs are drawn on a second stream while a pass computes "
+                "(trials.run_trial_set)",
+        "seconds_unpipelined": round(serial_sec, 3), "pipelined_equals_unpipelined": same,
         "err_rand_mean": float(np.nanmean(e[0])), "err_det_mean": float(np.nanmean(e[1])),
         "_errors": e,
     }

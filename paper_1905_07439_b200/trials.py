@@ -247,3 +247,73 @@ class DeviceErrorTrials:
             ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(), ctypes.c_void_p(st.cuda_stream),
         )
         _lib.check(rc)
+
+
+def run_trial_set(cfg, first: int, total: int, T_step: int, device="cuda:0", pipelined: bool = True,
+                  runners=None):
+    """Error trials of pairs first .. first+total-1 of a trial config, T_step
+    pairs per pass, with fresh inputs: each pass's operand pairs are drawn on
+    the GPU (rbc_matgen, bit-identical to the host draw, reference
+    experiments.py:237-239), its plans drawn natively (experiments.py:242-245),
+    the truth and both products run (experiments.py:248-261) and the per-trial
+    errors copied back.  Returns (err_rand, err_det, nf_rand, nf_det) host
+    arrays in pair order.
+
+    ``pipelined``: pass s+1's inputs are drawn on a second stream into the other
+    of two operand buffers while pass s computes -- the generator is integer /
+    DP-issue work that co-issues with the truth's DFMAs and the leaves' packed
+    FMAs, and its host half (tail samples) runs while the GPU
+    is busy.  Values do not depend on the schedule.  ``runners``: optional
+    dict reused across calls (keyed by pass size)."""
+    import torch
+
+    from .configs import make_pairs_device, packed_plans
+
+    dev = torch.device(device)
+    f = cfg.formula_obj()
+    runners = {} if runners is None else runners
+    chunks = [(p0, min(T_step, first + total - p0)) for p0 in range(first, first + total, T_step)]
+    if not chunks:
+        z = np.zeros(0)
+        return z, z.copy(), np.zeros(0, np.uint8), np.zeros(0, np.uint8)
+    tdt = {"double": torch.float64, "single": torch.float32, "half": torch.float16}[cfg.mode.kind]
+    nbuf = 2 if pipelined and len(chunks) > 1 else 1
+    bufs = [tuple(torch.empty((T_step, cfg.N, cfg.N), dtype=tdt, device=dev) for _ in range(2))
+            for _ in range(nbuf)]
+    main = torch.cuda.current_stream(dev)
+    # high priority: the draw's CTAs take SM slots as the (much larger) compute
+    # grids retire theirs, instead of queueing behind every pending CTA
+    gen = torch.cuda.Stream(device=dev, priority=-1) if nbuf == 2 else main
+    ready = [torch.cuda.Event() for _ in range(nbuf)]
+    consumed = [torch.cuda.Event() for _ in range(nbuf)]
+    host = torch.empty((len(chunks), 4, T_step), dtype=torch.float64).pin_memory()
+
+    def draw(i):
+        p0, cnt = chunks[i]
+        slot = i % nbuf
+        with torch.cuda.stream(gen):
+            if i >= nbuf:
+                gen.wait_event(consumed[slot])  # the pass that read this buffer is done
+            a, b = make_pairs_device(cfg, p0, cnt, dev, out=tuple(t[:cnt] for t in bufs[slot]))
+            ready[slot].record(gen)
+        packed = packed_plans(cfg, [cfg.plan_key(p) for p in range(p0, p0 + cnt)])
+        return a, b, torch.from_numpy(packed)
+
+    nxt = draw(0)
+    for i, (p0, cnt) in enumerate(chunks):
+        a, b, pl = nxt
+        slot = i % nbuf
+        if cnt not in runners:
+            runners[cnt] = DeviceErrorTrials(f, cfg.Q, cfg.N, cfg.mode, cnt, device=dev)
+        r = runners[cnt]
+        main.wait_event(ready[slot])
+        r.run(a, b, pl.to(dev, non_blocking=True))
+        consumed[slot].record(main)
+        res = torch.stack([r.err_rand, r.err_det, r.nf_rand.to(torch.float64), r.nf_det.to(torch.float64)])
+        host[i, :, :cnt].copy_(res, non_blocking=True)
+        if i + 1 < len(chunks):
+            nxt = draw(i + 1)  # overlaps pass i when pipelined
+    torch.cuda.synchronize(dev)
+    out = [np.concatenate([host[i, k, :cnt].numpy() for i, (_, cnt) in enumerate(chunks)])
+           for k in range(4)]
+    return out[0], out[1], out[2].astype(np.uint8), out[3].astype(np.uint8)

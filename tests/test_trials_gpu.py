@@ -293,3 +293,27 @@ def test_graph_replay_matches_eager(name, N, Q, T):
         torch.cuda.synchronize()
         assert np.array_equal(got[0], r.err_rand.cpu().numpy())
         assert np.array_equal(got[1], r.err_det.cpu().numpy())
+
+
+@pytest.mark.parametrize("name,N,Q", [("c2", 81, 3), ("c1", 64, 2)])
+def test_trial_set_pipelined_equals_serial_and_host_call(name, N, Q):
+    """trials.run_trial_set (fresh pairs drawn on the GPU for every pass; the
+    next pass's draw on a second stream while a pass computes) returns the
+    same per-trial errors pipelined and unpipelined, equal to the host-buffer
+    call on host-drawn pairs (ragged last pass)."""
+    from dataclasses import replace
+
+    from paper_1905_07439_b200.configs import get_config, make_pairs
+    from paper_1905_07439_b200.randomize import pack_recursive_plans
+    from paper_1905_07439_b200.trials import error_trials, run_trial_set
+
+    cfg = replace(get_config(name), N=N, Q=Q)
+    total, T_step = 10, 4
+    runs = [run_trial_set(cfg, 3, total, T_step, "cuda:0", pipelined=p) for p in (True, False, True)]
+    for r in runs[1:]:
+        for got, want in zip(r, runs[0]):
+            assert got.tobytes() == want.tobytes()
+    A, B = make_pairs(cfg, 3, total)
+    packed = pack_recursive_plans([cfg.plan(p) for p in range(3, 3 + total)], cfg.Q, cfg.n)
+    host = error_trials(cfg.formula_obj(), cfg.Q, A, B, cfg.mode, packed=packed)
+    assert np.array_equal(runs[0][0], host["err_rand"]) and np.array_equal(runs[0][1], host["err_det"])
