@@ -34,6 +34,16 @@
 // decision could differ only if the uniform fell within that ulp, p < 1e-15
 // per test).
 //
+// Memory shape of the parse (round 2: 59.7 -> see DESIGN section 4.4 ms for
+// config 5's four 8192^2 matrices).  One thread parses one chunk, so the raw
+// words are stored chunk-interleaved: word p of chunk j lives at
+// ((j / 32) * 64 + p) * 32 + j % 32, and the 32 lanes of a warp -- 32
+// consecutive chunks, all near the same p -- read one 256-byte row per step
+// instead of 32 separate lines.  The ziggurat tables sit in shared memory (a
+// constant-memory lookup by a per-lane strip index serialises over the lanes),
+// and the emitting kernel stages each CTA's samples in shared memory and
+// writes its contiguous output range coalesced.
+//
 // Post-processing follows matgen.generate per family, in binary64, then one
 // rounding into the mode (ScalarMode.array, precision.py:131-158): non-finite
 // results set the matrix's flag (the host raises OverflowError).
@@ -62,6 +72,34 @@ constexpr int kChunk = 64;     // words per parsed chunk
 constexpr int kEntries = 8;    // entry offsets tabulated per chunk
 constexpr int kTailWords = 64; // words fetched per tail candidate
 constexpr int kScanThreads = 256;
+constexpr int kGroup = 32;                       // chunks interleaved together (one warp)
+constexpr int64_t kGroupWords = kGroup * kChunk;  // 2048: per-matrix word counts are multiples
+
+// storage index of logical stream word i (chunk-interleaved, see above)
+__device__ __forceinline__ int64_t wat(int64_t i) {
+  const int64_t j = i >> 6;
+  return ((j >> 5) << 11) | ((i & 63) << 5) | (j & 31);
+}
+// logical stream position of storage index q
+__device__ __forceinline__ int64_t wlogical(int64_t q) {
+  return ((((q >> 11) << 5) | (q & 31)) << 6) | ((q >> 5) & 63);
+}
+
+// ziggurat tables in shared memory (filled by zig_load at kernel start)
+struct ZigTabs {
+  const uint64_t* ki;
+  const double* wi;
+  const double* fi;
+};
+__device__ __forceinline__ ZigTabs zig_load(uint64_t* ski, double* swi, double* sfi) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    ski[i] = c_ki[i];
+    swi[i] = c_wi[i];
+    sfi[i] = c_fi[i];
+  }
+  __syncthreads();
+  return ZigTabs{ski, swi, sfi};
+}
 
 __device__ __forceinline__ void philox4x64_10(uint64_t c[4], uint64_t k0, uint64_t k1) {
   constexpr uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
@@ -172,20 +210,23 @@ __global__ void __launch_bounds__(256) fill_words_kernel(int64_t Wn, const uint6
   const int m = blockIdx.y;
   const uint64_t k0 = keys[2 * m], k1 = keys[2 * m + 1];
   uint64_t* o = W + (int64_t)m * Wn;
-  for (int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; blk * 4 < Wn;
-       blk += (int64_t)gridDim.x * blockDim.x) {
+  // thread t -> (group g, block-in-chunk b4, lane l): Philox block (g*32+l)*16 + b4,
+  // i.e. words 4*b4 .. 4*b4+3 of chunk g*32+l; a warp writes four 256-byte rows
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t * 4 < Wn;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = t >> 9;
+    const int b4 = (int)((t >> 5) & 15), l = (int)(t & 31);
+    const int64_t blk = ((g << 5) + l) * 16 + b4;
     uint64_t c[4] = {(uint64_t)blk + 1, 0, 0, 0};
     philox4x64_10(c, k0, k1);
-    reinterpret_cast<ulonglong2*>(o + blk * 4)[0] = make_ulonglong2(c[0], c[1]);
-    reinterpret_cast<ulonglong2*>(o + blk * 4)[1] = make_ulonglong2(c[2], c[3]);
+    uint64_t* d = o + (g << 11) + ((int64_t)(4 * b4) << 5) + l;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q << 5] = c[q];
   }
 }
 
-__device__ __forceinline__ bool tail_candidate(uint64_t w) {
-  return (w & 0xff) == 0 && ((w >> 9) & kMask52) >= c_ki[0];
-}
-
-// positions of tail candidates (strip 0, outside the base rectangle)
+// positions of tail candidates (strip 0, outside the base rectangle); the
+// words are scanned in storage order, the list holds logical positions
 __global__ void __launch_bounds__(256) tail_candidates_kernel(int64_t Wn, int64_t Wparse,
                                                               const uint64_t* __restrict__ W,
                                                               int64_t* __restrict__ list,
@@ -193,11 +234,17 @@ __global__ void __launch_bounds__(256) tail_candidates_kernel(int64_t Wn, int64_
                                                               int64_t cap) {
   const int m = blockIdx.y;
   const uint64_t* w = W + (int64_t)m * Wn;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < Wparse;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    if (tail_candidate(w[p])) {
-      const unsigned long long slot = atomicAdd(count, 1ull);
-      if ((int64_t)slot < cap) list[slot] = (int64_t)m * Wn + p;
+  const uint64_t ki0 = c_ki[0];
+  const int64_t Wscan = (Wparse + kGroupWords - 1) / kGroupWords * kGroupWords;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Wscan;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = w[q];
+    if ((v & 0xff) == 0 && ((v >> 9) & kMask52) >= ki0) {
+      const int64_t p = wlogical(q);
+      if (p < Wparse) {
+        const unsigned long long slot = atomicAdd(count, 1ull);
+        if ((int64_t)slot < cap) list[slot] = (int64_t)m * Wn + p;
+      }
     }
   }
 }
@@ -205,9 +252,11 @@ __global__ void __launch_bounds__(256) tail_candidates_kernel(int64_t Wn, int64_
 // words p .. p+kTailWords-1 of every candidate: the r word (its bit 17 signs
 // the tail sample) and the uniforms of the host tail loop
 __global__ void __launch_bounds__(kTailWords) gather_tail_words_kernel(
-    const uint64_t* __restrict__ W, const int64_t* __restrict__ list, uint64_t* __restrict__ words) {
+    int64_t Wn, const uint64_t* __restrict__ W, const int64_t* __restrict__ list,
+    uint64_t* __restrict__ words) {
   const int64_t c = blockIdx.x;
-  words[c * kTailWords + threadIdx.x] = W[list[c] + threadIdx.x];
+  const int64_t m = list[c] / Wn, p = list[c] - m * Wn;
+  words[c * kTailWords + threadIdx.x] = W[m * Wn + wat(p + threadIdx.x)];
 }
 
 struct TailTab {
@@ -233,14 +282,14 @@ __device__ __forceinline__ int64_t tail_find(const TailTab& t, int64_t key) {
 template <class Emit>
 __device__ __forceinline__ int64_t parse_words(const uint64_t* __restrict__ w, int64_t base,
                                                int64_t p, int64_t end, const TailTab& tt,
-                                               int& cnt, Emit emit) {
+                                               const ZigTabs& z, int& cnt, Emit emit) {
   while (p < end) {
-    const uint64_t r = w[p];
+    const uint64_t r = w[wat(p)];
     const int idx = (int)(r & 0xff);
     const uint64_t rabs = (r >> 9) & kMask52;
-    double x = __dmul_rn((double)rabs, c_wi[idx]);
+    double x = __dmul_rn((double)rabs, z.wi[idx]);
     if ((r >> 8) & 1) x = -x;
-    if (rabs < c_ki[idx]) {
+    if (rabs < z.ki[idx]) {
       emit(cnt++, x);
       p += 1;
     } else if (idx == 0) {
@@ -248,8 +297,8 @@ __device__ __forceinline__ int64_t parse_words(const uint64_t* __restrict__ w, i
       emit(cnt++, tt.value[t]);
       p += tt.used[t];
     } else {
-      const double u = unit_double(w[p + 1]);
-      const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(c_fi[idx - 1], c_fi[idx]), u), c_fi[idx]);
+      const double u = unit_double(w[wat(p + 1)]);
+      const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(z.fi[idx - 1], z.fi[idx]), u), z.fi[idx]);
       const double rhs = exp(__dmul_rn(__dmul_rn(-0.5, x), x));
       p += 2;
       if (lhs < rhs) emit(cnt++, x);
@@ -272,6 +321,9 @@ __global__ void __launch_bounds__(256) chunk_maps_kernel(int64_t Wn, int64_t J,
                                                          const uint64_t* __restrict__ W, TailTab tt,
                                                          int* __restrict__ exits,
                                                          int* __restrict__ cnts) {
+  __shared__ uint64_t ski[256];
+  __shared__ double swi[256], sfi[256];
+  const ZigTabs z = zig_load(ski, swi, sfi);
   const int m = blockIdx.y;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= J) return;
@@ -287,7 +339,7 @@ __global__ void __launch_bounds__(256) chunk_maps_kernel(int64_t Wn, int64_t J,
     const int at = (int)(p - c0);
     rmask |= 1ull << at;
     int one = 0;
-    const int64_t q = parse_words(w, base, p, p + 1, tt, one, NoEmit{});
+    const int64_t q = parse_words(w, base, p, p + 1, tt, z, one, NoEmit{});
     if (one) emask |= 1ull << at;
     cnt0 += one;
     p = q;
@@ -306,7 +358,7 @@ __global__ void __launch_bounds__(256) chunk_maps_kernel(int64_t Wn, int64_t J,
         merged = true;
         break;
       }
-      q = parse_words(w, base, q, q + 1, tt, cnt, NoEmit{});
+      q = parse_words(w, base, q, q + 1, tt, z, cnt, NoEmit{});
     }
     exits[o + e] = merged ? exit0 : (int)(q - end);
     cnts[o + e] = cnt;
@@ -324,7 +376,7 @@ __device__ __forceinline__ bool map_constant(const int* ex) {
 // exit does not depend on its entry), then forward through the maps.
 // Entries >= kEntries (a long tail spilling over) are parsed directly.
 __device__ int chunk_entry(const uint64_t* __restrict__ w, int64_t base, int64_t j,
-                           const int* __restrict__ exits, const TailTab& tt) {
+                           const int* __restrict__ exits, const TailTab& tt, const ZigTabs& z) {
   int64_t i = j - 1;
   while (i >= 0 && !map_constant(exits + i * kEntries)) --i;
   int entry = i >= 0 ? exits[i * kEntries] : 0;
@@ -334,7 +386,7 @@ __device__ int chunk_entry(const uint64_t* __restrict__ w, int64_t base, int64_t
     } else {
       int cnt = 0;
       const int64_t end = (k + 1) * kChunk;
-      entry = (int)(parse_words(w, base, k * kChunk + entry, end, tt, cnt, NoEmit{}) - end);
+      entry = (int)(parse_words(w, base, k * kChunk + entry, end, tt, z, cnt, NoEmit{}) - end);
     }
   }
   return entry;
@@ -345,6 +397,9 @@ __global__ void __launch_bounds__(kScanThreads) chunk_entries_kernel(
     int64_t Wn, int64_t J, const uint64_t* __restrict__ W, TailTab tt,
     const int* __restrict__ exits, const int* __restrict__ cnts, int* __restrict__ entry_out,
     int* __restrict__ cnt_out, long long* __restrict__ bsum) {
+  __shared__ uint64_t ski[256];
+  __shared__ double swi[256], sfi[256];
+  const ZigTabs z = zig_load(ski, swi, sfi);
   const int m = blockIdx.y;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t* w = W + (int64_t)m * Wn;
@@ -352,11 +407,11 @@ __global__ void __launch_bounds__(kScanThreads) chunk_entries_kernel(
   const int* ct = cnts + (int64_t)m * J * kEntries;
   int cnt = 0;
   if (j < J) {
-    const int entry = chunk_entry(w, (int64_t)m * Wn, j, ex, tt);
+    const int entry = chunk_entry(w, (int64_t)m * Wn, j, ex, tt, z);
     if (entry < kEntries) {
       cnt = ct[j * kEntries + entry];
     } else {
-      parse_words(w, (int64_t)m * Wn, j * kChunk + entry, (j + 1) * kChunk, tt, cnt, NoEmit{});
+      parse_words(w, (int64_t)m * Wn, j * kChunk + entry, (j + 1) * kChunk, tt, z, cnt, NoEmit{});
     }
     entry_out[(int64_t)m * J + j] = entry;
     cnt_out[(int64_t)m * J + j] = cnt;
@@ -402,37 +457,76 @@ __global__ void __launch_bounds__(1024) scan_bsum_kernel(int nblk, long long* __
   }
 }
 
+// Emits the samples of emit_threads<T>() consecutive chunks.  Their outputs form
+// one contiguous range of the matrix (the scan gives its start), so each
+// thread stages its samples -- post-processed and rounded into the mode -- in
+// shared memory at their offset inside the range, and the CTA then writes the
+// range with coalesced stores.
 template <class T>
-__global__ void __launch_bounds__(kScanThreads) emit_normals_kernel(
+constexpr int emit_threads() { return sizeof(T) == 8 ? 64 : 128; }  // 32 KB of staged samples
+template <class T>
+__global__ void __launch_bounds__(emit_threads<T>()) emit_normals_kernel(
     int64_t Wn, int64_t J, int64_t S, const uint64_t* __restrict__ W, TailTab tt,
     const int* __restrict__ entries, const int* __restrict__ cnts,
     const long long* __restrict__ bsum, const int* __restrict__ which, Post p, T* __restrict__ out,
     uint8_t* __restrict__ flags) {
+  constexpr int kEmitThreads = emit_threads<T>();
+  static_assert(kScanThreads % kEmitThreads == 0, "emit CTAs subdivide the scan blocks");
+  constexpr int kSub = kScanThreads / kEmitThreads;
+  __shared__ uint64_t ski[256];
+  __shared__ double swi[256], sfi[256];
+  __shared__ int sc[kEmitThreads];
+  __shared__ long long sbase;
+  __shared__ T stage[kEmitThreads * kChunk];
+  const ZigTabs z = zig_load(ski, swi, sfi);
   const int m = blockIdx.y;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int cnt = j < J ? cnts[(int64_t)m * J + j] : 0;
   // block-exclusive scan of the chunk counts
-  __shared__ long long sc[kScanThreads];
   sc[threadIdx.x] = cnt;
   __syncthreads();
-  for (int s = 1; s < kScanThreads; s <<= 1) {
-    const long long v = threadIdx.x >= s ? sc[threadIdx.x - s] : 0;
+  for (int s = 1; s < kEmitThreads; s <<= 1) {
+    const int v = threadIdx.x >= s ? sc[threadIdx.x - s] : 0;
     __syncthreads();
     sc[threadIdx.x] += v;
     __syncthreads();
   }
-  if (j >= J || cnt == 0) return;
-  const long long off = bsum[(int64_t)m * gridDim.x + blockIdx.x] + sc[threadIdx.x] - cnt;
-  if (off >= S) return;
+  // start of this CTA's range: the scan block's offset plus the counts of the
+  // emit CTAs before this one inside the scan block
+  if (threadIdx.x == 0)
+    sbase = bsum[(int64_t)m * ((gridDim.x + kSub - 1) / kSub) + blockIdx.x / kSub];
+  __syncthreads();
+  {
+    const int64_t j0 = (int64_t)(blockIdx.x / kSub) * kScanThreads;
+    int pre = 0;
+    for (int64_t k = j0 + threadIdx.x; k < (int64_t)blockIdx.x * kEmitThreads && k < J;
+         k += kEmitThreads)
+      pre += cnts[(int64_t)m * J + k];
+    if (pre) atomicAdd(reinterpret_cast<unsigned long long*>(&sbase), (unsigned long long)pre);
+  }
+  __syncthreads();
+  const long long base = sbase;
+  const int total = sc[kEmitThreads - 1];
+  const int loc = sc[threadIdx.x] - cnt;
+  if (base >= S || total == 0) return;  // CTA-uniform
   const uint64_t* w = W + (int64_t)m * Wn;
-  T* o = out + (int64_t)m * S;
   const int wh = which[m];
-  int k = 0;
-  parse_words(w, (int64_t)m * Wn, j * kChunk + entries[(int64_t)m * J + j], (j + 1) * kChunk, tt, k,
-              [&](int q, double x) {
-                const int64_t e = off + q;
-                if (e < S) store_sample<T>(o, flags, m, wh, p, e, x);
-              });
+  if (j < J && cnt > 0) {
+    int k = 0;
+    parse_words(w, (int64_t)m * Wn, j * kChunk + entries[(int64_t)m * J + j], (j + 1) * kChunk, tt, z,
+                k, [&](int q, double x) {
+                  const int64_t e = base + loc + q;
+                  if (e < S) {
+                    const T r = round_into<T>(post_value(p, wh, e, x));
+                    stage[loc + q] = r;
+                    if (flags && !finite_of(r)) flags[m] = 1;
+                  }
+                });
+  }
+  __syncthreads();
+  T* o = out + (int64_t)m * S + base;
+  const int lim = (int)(S - base < total ? S - base : total);
+  for (int t = threadIdx.x; t < lim; t += kEmitThreads) o[t] = stage[t];
 }
 
 // Host half of the tail: numpy's loop
@@ -461,7 +555,8 @@ int run_normals(int64_t count, int64_t n, const uint64_t* dkeys, const int* dwhi
   // expected consumption is ~1.0125 words per sample; 1/32 + 4096 spare
   int64_t Wparse = ((S + S / 32 + 4096) + kChunk - 1) / kChunk * kChunk;
   for (int attempt = 0; attempt < 4; ++attempt, Wparse *= 2) {
-    const int64_t Wn = Wparse + 2 * kTailWords + 64;  // readable past the last chunk
+    // readable past the last chunk; whole interleave groups per matrix
+    const int64_t Wn = (Wparse + 2 * kTailWords + 64 + kGroupWords - 1) / kGroupWords * kGroupWords;
     const int64_t J = Wparse / kChunk;
     const int nblk = (int)((J + kScanThreads - 1) / kScanThreads);
     const int64_t cap = std::max<int64_t>(4096, count * Wparse / 512);
@@ -523,7 +618,7 @@ int run_normals(int64_t count, int64_t n, const uint64_t* dkeys, const int* dwhi
       CUDA_TRY(cudaStreamSynchronize(st));
       std::sort(pos.begin(), pos.end());
       CUDA_TRY(cudaMemcpyAsync(tpos, pos.data(), sizeof(int64_t) * ncand, cudaMemcpyHostToDevice, st));
-      gather_tail_words_kernel<<<(unsigned)ncand, kTailWords, 0, st>>>(W, tpos, twords);
+      gather_tail_words_kernel<<<(unsigned)ncand, kTailWords, 0, st>>>(Wn, W, tpos, twords);
       CUDA_TRY(cudaMemcpyAsync(words.data(), twords, sizeof(uint64_t) * ncand * kTailWords,
                                cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
@@ -551,9 +646,12 @@ int run_normals(int64_t count, int64_t n, const uint64_t* dkeys, const int* dwhi
     CUDA_TRY(cudaMemcpyAsync(tot.data(), total, sizeof(long long) * count, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     const bool enough = std::all_of(tot.begin(), tot.end(), [&](long long t) { return t >= S; });
-    if (enough)
-      emit_normals_kernel<T><<<gj, kScanThreads, 0, st>>>(Wn, J, S, W, tt, ent, cn, bsum, dwhich,
+    if (enough) {
+      constexpr int kEmitThreads = emit_threads<T>();
+      const dim3 ge((unsigned)((J + kEmitThreads - 1) / kEmitThreads), (unsigned)count);
+      emit_normals_kernel<T><<<ge, kEmitThreads, 0, st>>>(Wn, J, S, W, tt, ent, cn, bsum, dwhich,
                                                           post, static_cast<T*>(out), flags);
+    }
     const cudaError_t e = cudaGetLastError();
     cudaFreeAsync(twords, st);
     cudaFreeAsync(tpos, st);
