@@ -983,6 +983,10 @@ def run_ours(args):
         line["errors"]["running_mean_at_G"] = {
             "mean": float(np.nanmean(me[:, -1])), "checkpoints": wl.runner.cps}
     if hasattr(wl, "fresh") and not args.no_e2e:
+        # the host-buffer calls above keep an arena sized to most of the free
+        # memory; give it back before the device-resident runner allocates
+        from paper_1905_07439_b200 import _lib as _rbclib
+        _rbclib.check(_rbclib.load().rbc_release_device_memory())
         barrier()
         fresh_ms = float(distributed.max_over_ranks([wl.fresh(args.steps)], device=coll)[0])
         line["e2e_fresh_inputs"] = {
@@ -1130,7 +1134,9 @@ def time_to_solution(cfg, T_step, dev, rank, world, coll=None):
                 "the next pass's inputs are drawn on a second stream while a pass computes "
                 "(trials.run_trial_set)",
         "seconds_unpipelined": round(serial_sec, 3), "pipelined_equals_unpipelined": same,
-        "err_rand_mean": float(np.nanmean(e[0])), "err_det_mean": float(np.nanmean(e[1])),
+        # None when every trial overflowed (config 4's deterministic products)
+        "err_rand_mean": float(np.nanmean(e[0])) if np.isfinite(e[0]).any() else None,
+        "err_det_mean": float(np.nanmean(e[1])) if np.isfinite(e[1]).any() else None,
         "_errors": e,
     }
 

@@ -76,6 +76,13 @@ int rbc_abi_version(void);
 const char* rbc_last_error(void);
 int rbc_device_count(void);
 
+/* Give back the device memory the host-buffer calls keep between calls (one
+ * arena per process, grown to the largest call) and the unused part of the
+ * stream-ordered scratch pool.  Synchronises the device.  The next host-buffer
+ * call allocates again.  For processes that alternate host-buffer calls with
+ * device-resident pipelines of their own (rbc_*_async) on a full GPU. */
+int rbc_release_device_memory(void);
+
 /* Stage profiler: when enabled, every engine launch is bracketed by CUDA
  * events on its own stream and tagged with its algorithmic bytes and flops.
  * rbc_profile_summary synchronises the recorded events and writes a JSON

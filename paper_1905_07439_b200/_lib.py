@@ -29,6 +29,7 @@ EXPORTS = (
     "rbc_abi_version",
     "rbc_last_error",
     "rbc_device_count",
+    "rbc_release_device_memory",
     "rbc_profile_enable",
     "rbc_profile_summary",
     "rbc_apply_levels",
@@ -75,6 +76,7 @@ def _declare(lib):
         "rbc_abi_version": (c_int, []),
         "rbc_last_error": (ctypes.c_char_p, []),
         "rbc_device_count": (c_int, []),
+        "rbc_release_device_memory": (c_int, []),
         "rbc_profile_enable": (None, [c_int]),
         "rbc_profile_summary": (c_i64, [ctypes.c_char_p, c_size]),
         "rbc_apply_levels": (

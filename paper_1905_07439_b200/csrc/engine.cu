@@ -495,6 +495,22 @@ int rbc_device_count(void) {
   return c;
 }
 
+int rbc_release_device_memory(void) {
+  std::lock_guard<std::mutex> lock(arena().mu);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return fail_cuda(e, "cudaDeviceSynchronize", __FILE__, __LINE__);
+  Arena& A = arena();
+  if (A.ptr) cudaFree(A.ptr);
+  A.ptr = nullptr;
+  A.cap = A.off = 0;
+  ++A.gen;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+    cudaMemPoolTrimTo(pool, 0);
+  return RBC_OK;
+}
+
 size_t rbc_levels_workspace_bytes(int dtype, int Q, const int32_t* n, const int32_t* R, int64_t T,
                                   int64_t N) {
   Geometry g;

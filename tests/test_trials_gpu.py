@@ -317,3 +317,24 @@ def test_trial_set_pipelined_equals_serial_and_host_call(name, N, Q):
     packed = pack_recursive_plans([cfg.plan(p) for p in range(3, 3 + total)], cfg.Q, cfg.n)
     host = error_trials(cfg.formula_obj(), cfg.Q, A, B, cfg.mode, packed=packed)
     assert np.array_equal(runs[0][0], host["err_rand"]) and np.array_equal(runs[0][1], host["err_det"])
+
+
+def test_release_device_memory_then_host_call_again():
+    """rbc_release_device_memory frees the host-call arena; the next host-buffer
+    call allocates again and returns the same values."""
+    import paper_1905_07439_b200 as rbc
+    from paper_1905_07439_b200 import _lib, engine
+    from paper_1905_07439_b200.multiply import mode_tensors
+    from paper_1905_07439_b200.precision import SINGLE
+
+    _lib.require_device()
+    g = np.random.default_rng(5)
+    f = rbc.strassen_formula()
+    levels = [mode_tensors(f, SINGLE)] * 2
+    a = SINGLE.array(g.standard_normal((3, 16, 16)))
+    b = SINGLE.array(g.standard_normal((3, 16, 16)))
+    first = engine.apply_levels(levels, a, b, SINGLE)
+    _lib.check(_lib.load().rbc_release_device_memory())
+    _lib.check(_lib.load().rbc_release_device_memory())  # idempotent
+    again = engine.apply_levels(levels, a, b, SINGLE)
+    assert again.tobytes() == first.tobytes()
