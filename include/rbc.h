@@ -234,6 +234,22 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
                      const void* b, const void* rand_plans, int with_det, double* err_rand,
                      double* err_det, uint8_t* nonfinite_rand, uint8_t* nonfinite_det);
 
+/* The same call in two halves, so that consecutive calls overlap: _begin
+ * enqueues the copies, kernels and result copies of one call and returns a
+ * ticket; _end(ticket) waits for them and reports failures.  At most two
+ * calls are in flight.  With a second call begun before the first is ended,
+ * its operands are copied while the first call still computes (one call alone
+ * leaves the GPU idle during its first copy).  All host buffers of a call
+ * (operands, plans, results; pinned for the copies to be asynchronous) must
+ * stay valid and untouched until its _end.  Calls of one shape share a device
+ * layout; a call of another shape, and every other host-buffer entry point of
+ * this library, first waits for the calls in flight.  rbc_error_trials is
+ * _begin followed by _end. */
+int rbc_error_trials_begin(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
+                           const void* b, const void* rand_plans, int with_det, double* err_rand,
+                           double* err_det, uint8_t* nf_rand, uint8_t* nf_det, int64_t* ticket);
+int rbc_error_trials_end(int64_t ticket);
+
 size_t rbc_error_trials_workspace_bytes(int dtype, int formula, int Q, int64_t T, int64_t N);
 
 /* ---- averaging trials (experiments.py:264-296; BASELINE config 3) --------

@@ -47,6 +47,8 @@ EXPORTS = (
     "rbc_rel_errors",
     "rbc_nonfinite_async",
     "rbc_error_trials",
+    "rbc_error_trials_begin",
+    "rbc_error_trials_end",
     "rbc_error_trials_workspace_bytes",
     "rbc_error_trials_async",
     "rbc_average_trials_workspace_bytes",
@@ -116,6 +118,12 @@ def _declare(lib):
             c_int,
             [c_int, c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp],
         ),
+        "rbc_error_trials_begin": (
+            c_int,
+            [c_int, c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp,
+             P(c_i64)],
+        ),
+        "rbc_error_trials_end": (c_int, [c_i64]),
         "rbc_error_trials_workspace_bytes": (c_size, [c_int, c_int, c_int, c_i64, c_i64]),
         "rbc_average_trials_workspace_bytes": (c_size, [c_int, c_int, P(c_i32), P(c_i32), c_i64, c_i64]),
         "rbc_average_trials_async": (

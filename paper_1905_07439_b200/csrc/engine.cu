@@ -379,7 +379,11 @@ struct Arena {
   size_t cap = 0;
   size_t off = 0;
   unsigned gen = 0;  // bumped whenever the allocation moves
+  unsigned epoch = 0;  // bumped by every reserve(): a layout made earlier is stale
+  void (*drain)() = nullptr;  // waits for host-buffer calls still in flight (begin/end)
   int reserve(size_t bytes) {
+    if (drain) drain();
+    ++epoch;
     if (bytes <= cap) {
       off = 0;
       return RBC_OK;
@@ -504,6 +508,7 @@ int rbc_release_device_memory(void) {
   A.ptr = nullptr;
   A.cap = A.off = 0;
   ++A.gen;
+  ++A.epoch;
   int dev = 0;
   cudaMemPool_t pool;
   if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
@@ -1008,9 +1013,62 @@ static cudaEvent_t pipe_event(int i) {
 // kernels.  (Measured and dropped in round 1: more slots, a second copy
 // stream, ramped chunk sizes and per-chunk CUDA graphs -- all equal or
 // slower.)
-int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
-                     const void* b, const void* rand_plans, int with_det, double* err_rand,
-                     double* err_det, uint8_t* nf_rand, uint8_t* nf_det) {
+//
+// The call comes in two halves so that the ring runs ACROSS calls:
+// rbc_error_trials_begin enqueues a call's copies, kernels and result copies
+// and returns; rbc_error_trials_end waits for them.  With a second call begun
+// before the first is ended, its first chunks are copied while the first
+// call's last chunks compute (a single call leaves the GPU idle for its first
+// copy: 9.8 ms of config 5's 176 ms).  Two calls may be in flight; calls of
+// one shape share the arena layout, a call of another shape -- or any other
+// host-buffer API that takes the arena -- first waits for the calls in flight.
+struct HostPipe {
+  bool valid = false;
+  unsigned epoch = 0;  // arena epoch of the layout
+  int dtype = 0, formula = 0, Q = 0, with_det = 0, has_plans = 0;
+  int64_t T = 0, N = 0, C = 0;
+  int64_t k = 0;       // chunks enqueued on this layout (ring position)
+  int64_t serial = 0;  // tickets handed out
+  bool busy[2] = {false, false};
+  int64_t ticket[2] = {-1, -1};
+  void* da[kSlots];
+  void* dbb[kSlots];
+  void* dpl[kSlots];
+  void* ddet = nullptr;
+  void* dws[2] = {nullptr, nullptr};
+  size_t ws = 0;
+  double* derr_r[2];
+  double* derr_d[2];
+  uint8_t* dnf_r[2];
+  uint8_t* dnf_d[2];
+};
+
+static HostPipe& host_pipe() {
+  static HostPipe p;
+  return p;
+}
+
+static cudaEvent_t done_event(int i) {
+  static cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (!ev[i]) cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+  return ev[i];
+}
+
+// everything a begun call queued has run (arena lock held by the caller)
+static void drain_host_pipe() {
+  HostPipe& P = host_pipe();
+  if (!P.busy[0] && !P.busy[1] && !P.valid) return;
+  cudaStreamSynchronize(copy_stream(0));
+  cudaStreamSynchronize(host_stream(0));
+  cudaStreamSynchronize(host_stream(1));
+  cudaStreamSynchronize(copy_stream(1));
+}
+
+int rbc_error_trials_begin(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
+                           const void* b, const void* rand_plans, int with_det, double* err_rand,
+                           double* err_det, uint8_t* nf_rand, uint8_t* nf_det, int64_t* ticket) {
+  if (!ticket) return set_error(RBC_EVALUE, "ticket pointer is null");
+  *ticket = -1;
   if (dtype < 0 || dtype > 2) return set_error(RBC_EVALUE, "bad dtype %d", dtype);
   const int n = formula_n(formula);
   if (!n) return set_error(RBC_EVALUE, "unknown formula id %d", formula);
@@ -1025,11 +1083,20 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   }
   if (!rand_plans && !with_det) return set_error(RBC_EVALUE, "no product requested");
   RBC_TRY(check_device());
-  if (T == 0 || N == 0) return RBC_OK;
+  std::lock_guard<std::mutex> lock(arena().mu);
+  HostPipe& P = host_pipe();
+  if (P.busy[0] && P.busy[1]) return set_error(RBC_EVALUE, "two host-buffer calls already in flight");
+  const int slotp = P.busy[(int)(P.serial & 1)] ? (int)((P.serial + 1) & 1) : (int)(P.serial & 1);
+  if (T == 0 || N == 0) {  // nothing to do: a ticket that is already complete
+    P.busy[slotp] = true;
+    P.ticket[slotp] = P.serial;
+    *ticket = P.serial++;
+    cudaEventRecord(done_event(slotp), copy_stream(1));
+    return RBC_OK;
+  }
   const size_t es = dtype_size(dtype);
   const size_t N2 = (size_t)N * N;
   const size_t db = (size_t)Q * RBC_PLAN_BYTES;
-  std::lock_guard<std::mutex> lock(arena().mu);
   // pipeline chunks: about 8 MB of operands per chunk, at most 16 (config 2
   // with two compute streams: 12 chunks 11.21 ms per call, 16: 11.20, 32:
   // 11.4)
@@ -1044,47 +1111,65 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
   const bool two = N < 512;
   auto need = [&](int64_t c) {
     const size_t slot = 2 * align_up(c * N2 * es) + align_up(c * Q * RBC_PLAN_BYTES);
-    return kSlots * slot + align_up(db) + 2 * align_up(T * 8) + 2 * align_up(T) + 4096 +
+    return kSlots * slot + align_up(db) + 2 * (2 * align_up(T * 8) + 2 * align_up(T)) + 4096 +
            (two ? 2 : 1) * align_up(rbc_error_trials_workspace_bytes(dtype, formula, Q, c, N));
   };
-  // The device memory query runs only when the arena must grow: in steady
-  // state an earlier call's arena already holds this chunking, and
-  // cudaMemGetInfo can stall the host for tens of ms behind concurrent
-  // driver queries (NVML polling; a host phase trace showed 31 and 97 ms
-  // "setup" phases in 30 calls).
-  if (need(C) > arena().cap) {
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const size_t budget = (size_t)((double)(free_b + arena().cap) * 0.85);
-    while (C > 1 && need(C) > budget) C = (C + 1) / 2;
-    if (need(C) > budget) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
-  }
-  RBC_TRY(arena().reserve(need(C) + 256));
   Arena& A = arena();
-  void* da[kSlots];
-  void* dbb[kSlots];
-  void* dpl[kSlots];
-  for (int k = 0; k < kSlots; ++k) {
-    da[k] = A.take(C * N2 * es);
-    dbb[k] = A.take(C * N2 * es);
-    dpl[k] = A.take(C * Q * RBC_PLAN_BYTES);
-  }
-  void* ddet = A.take(db);
-  double* derr_r = (double*)A.take(T * 8);
-  double* derr_d = (double*)A.take(T * 8);
-  uint8_t* dnf_r = (uint8_t*)A.take(T);
-  uint8_t* dnf_d = (uint8_t*)A.take(T);
-  const size_t ws = rbc_error_trials_workspace_bytes(dtype, formula, Q, C, N);
-  void* dws[2] = {A.take(ws), two ? A.take(ws) : nullptr};
   cudaStream_t scs[2] = {host_stream(0), host_stream(1)};
   cudaStream_t sc = scs[0];
   cudaStream_t sx = copy_stream(0);
-  std::vector<PlanLevel> ident(Q);
-  for (int q = 0; q < Q; ++q) {
-    memset(&ident[q], 0, sizeof(PlanLevel));
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < n; ++j) ident[q].perm[i][j] = ident[q].inv[i][j] = (int8_t)j;
+  cudaStream_t sr = copy_stream(1);  // result copies
+  const bool same = P.valid && P.epoch == A.epoch && P.dtype == dtype && P.formula == formula &&
+                    P.Q == Q && P.T == T && P.N == N && P.with_det == with_det &&
+                    P.has_plans == (rand_plans != nullptr);
+  if (!same) {
+    // The device memory query runs only when the arena must grow: in steady
+    // state an earlier call's arena already holds this chunking, and
+    // cudaMemGetInfo can stall the host for tens of ms behind concurrent
+    // driver queries (NVML polling; a host phase trace showed 31 and 97 ms
+    // "setup" phases in 30 calls).
+    if (need(C) > A.cap) {
+      drain_host_pipe();
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const size_t budget = (size_t)((double)(free_b + A.cap) * 0.85);
+      while (C > 1 && need(C) > budget) C = (C + 1) / 2;
+      if (need(C) > budget) return set_error(RBC_ERUNTIME, "not enough device memory for one trial");
+    }
+    P.valid = false;
+    RBC_TRY(A.reserve(need(C) + 256));  // waits for calls in flight (Arena::drain)
+    for (int k = 0; k < kSlots; ++k) {
+      P.da[k] = A.take(C * N2 * es);
+      P.dbb[k] = A.take(C * N2 * es);
+      P.dpl[k] = A.take(C * Q * RBC_PLAN_BYTES);
+    }
+    P.ddet = A.take(db);
+    for (int h = 0; h < 2; ++h) {
+      P.derr_r[h] = (double*)A.take(T * 8);
+      P.derr_d[h] = (double*)A.take(T * 8);
+      P.dnf_r[h] = (uint8_t*)A.take(T);
+      P.dnf_d[h] = (uint8_t*)A.take(T);
+    }
+    P.ws = rbc_error_trials_workspace_bytes(dtype, formula, Q, C, N);
+    P.dws[0] = A.take(P.ws);
+    P.dws[1] = two ? A.take(P.ws) : nullptr;
+    std::vector<PlanLevel> ident(Q);
+    for (int q = 0; q < Q; ++q) {
+      memset(&ident[q], 0, sizeof(PlanLevel));
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < n; ++j) ident[q].perm[i][j] = ident[q].inv[i][j] = (int8_t)j;
+    }
+    // the identity plans of the deterministic product: uploaded once per layout
+    CUDA_TRY(cudaMemcpyAsync(P.ddet, ident.data(), db, cudaMemcpyHostToDevice, sc));
+    CUDA_TRY(cudaStreamSynchronize(sc));  // ident is a local
+    P.dtype = dtype, P.formula = formula, P.Q = Q, P.with_det = with_det;
+    P.has_plans = rand_plans != nullptr;
+    P.T = T, P.N = N, P.C = C, P.k = 0;
+    P.epoch = A.epoch;
+    P.valid = true;
+    A.drain = drain_host_pipe;
   }
+  C = P.C;
   // Chunk sizes: C, ..., C, then the remainder cut in halves (multiples of
   // 8): the copies are the critical path (PCIe), so after the last copy only
   // a small chunk is left to compute.
@@ -1102,55 +1187,94 @@ int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const 
     }
     if (rem > 0) sizes.push_back(rem);
   }
+  double* derr_r = P.derr_r[slotp];
+  double* derr_d = P.derr_d[slotp];
+  uint8_t* dnf_r = P.dnf_r[slotp];
+  uint8_t* dnf_d = P.dnf_d[slotp];
   auto enqueue = [&]() -> int {
-    CUDA_TRY(cudaMemcpyAsync(ddet, ident.data(), db, cudaMemcpyHostToDevice, sc));
-    CUDA_TRY(cudaEventRecord(pipe_event(2 * kSlots), sc));
-    CUDA_TRY(cudaStreamWaitEvent(scs[1], pipe_event(2 * kSlots), 0));
     int64_t t0 = 0;
-    for (int64_t k = 0; k < (int64_t)sizes.size(); t0 += sizes[k], ++k) {
-      const int64_t nt = sizes[k];
+    for (int64_t i = 0; i < (int64_t)sizes.size(); t0 += sizes[i], ++i, ++P.k) {
+      const int64_t nt = sizes[i];
+      const int64_t k = P.k;  // ring position, continuing across calls
       const int slot = (int)(k % kSlots);
-      cudaStream_t sk = scs[two ? (k & 1) : 0];
+      const int lane = two ? (int)(k & 1) : 0;
+      cudaStream_t sk = scs[lane];
       cudaEvent_t copied = pipe_event(slot), computed = pipe_event(kSlots + slot);
       if (k >= kSlots) CUDA_TRY(cudaStreamWaitEvent(sx, computed, 0));  // slot free again
-      CUDA_TRY(cudaMemcpyAsync(da[slot], (const char*)a + t0 * N2 * es, nt * N2 * es,
+      CUDA_TRY(cudaMemcpyAsync(P.da[slot], (const char*)a + t0 * N2 * es, nt * N2 * es,
                                cudaMemcpyHostToDevice, sx));
-      CUDA_TRY(cudaMemcpyAsync(dbb[slot], (const char*)b + t0 * N2 * es, nt * N2 * es,
+      CUDA_TRY(cudaMemcpyAsync(P.dbb[slot], (const char*)b + t0 * N2 * es, nt * N2 * es,
                                cudaMemcpyHostToDevice, sx));
       if (rand_plans)
-        CUDA_TRY(cudaMemcpyAsync(dpl[slot], (const char*)rand_plans + t0 * Q * RBC_PLAN_BYTES,
+        CUDA_TRY(cudaMemcpyAsync(P.dpl[slot], (const char*)rand_plans + t0 * Q * RBC_PLAN_BYTES,
                                  nt * Q * RBC_PLAN_BYTES, cudaMemcpyHostToDevice, sx));
       CUDA_TRY(cudaEventRecord(copied, sx));
       CUDA_TRY(cudaStreamWaitEvent(sk, copied, 0));
-      RBC_TRY(rbc_error_trials_async(dtype, formula, Q, nt, N, da[slot], dbb[slot],
-                                     rand_plans ? dpl[slot] : nullptr, with_det ? ddet : nullptr,
-                                     derr_r + t0, derr_d + t0, dnf_r + t0, dnf_d + t0,
-                                     dws[two ? (k & 1) : 0], ws, sk));
+      RBC_TRY(rbc_error_trials_async(dtype, formula, Q, nt, N, P.da[slot], P.dbb[slot],
+                                     rand_plans ? P.dpl[slot] : nullptr,
+                                     with_det ? P.ddet : nullptr, derr_r + t0, derr_d + t0,
+                                     dnf_r + t0, dnf_d + t0, P.dws[lane], P.ws, sk));
       CUDA_TRY(cudaEventRecord(computed, sk));
     }
-    CUDA_TRY(cudaEventRecord(pipe_event(2 * kSlots), scs[1]));
-    CUDA_TRY(cudaStreamWaitEvent(sc, pipe_event(2 * kSlots), 0));
+    // results: copied back on their own stream once both compute streams have
+    // passed this call's chunks, so the next call's chunks queue right behind
+    for (int l = 0; l < (two ? 2 : 1); ++l) {
+      CUDA_TRY(cudaEventRecord(pipe_event(2 * kSlots), scs[l]));
+      CUDA_TRY(cudaStreamWaitEvent(sr, pipe_event(2 * kSlots), 0));
+    }
     if (rand_plans) {
-      CUDA_TRY(cudaMemcpyAsync(err_rand, derr_r, T * 8, cudaMemcpyDeviceToHost, sc));
-      if (nf_rand) CUDA_TRY(cudaMemcpyAsync(nf_rand, dnf_r, T, cudaMemcpyDeviceToHost, sc));
+      CUDA_TRY(cudaMemcpyAsync(err_rand, derr_r, T * 8, cudaMemcpyDeviceToHost, sr));
+      if (nf_rand) CUDA_TRY(cudaMemcpyAsync(nf_rand, dnf_r, T, cudaMemcpyDeviceToHost, sr));
     }
     if (with_det) {
-      CUDA_TRY(cudaMemcpyAsync(err_det, derr_d, T * 8, cudaMemcpyDeviceToHost, sc));
-      if (nf_det) CUDA_TRY(cudaMemcpyAsync(nf_det, dnf_d, T, cudaMemcpyDeviceToHost, sc));
+      CUDA_TRY(cudaMemcpyAsync(err_det, derr_d, T * 8, cudaMemcpyDeviceToHost, sr));
+      if (nf_det) CUDA_TRY(cudaMemcpyAsync(nf_det, dnf_d, T, cudaMemcpyDeviceToHost, sr));
     }
+    CUDA_TRY(cudaEventRecord(done_event(slotp), sr));
     return RBC_OK;
   };
   const int rc = enqueue();
-  // On success and on failure alike, nothing that reads the caller's host
-  // buffers or the arena may still be queued when the arena lock is released.
-  const cudaError_t e0 = cudaStreamSynchronize(sx);
-  const cudaError_t e1 = cudaStreamSynchronize(scs[1]);
-  const cudaError_t e2 = cudaStreamSynchronize(sc);
-  if (rc != RBC_OK) return rc;
-  if (e0 != cudaSuccess) return fail_cuda(e0, "copy stream", __FILE__, __LINE__);
-  if (e1 != cudaSuccess) return fail_cuda(e1, "compute stream", __FILE__, __LINE__);
-  if (e2 != cudaSuccess) return fail_cuda(e2, "compute stream", __FILE__, __LINE__);
+  if (rc != RBC_OK) {
+    // nothing that reads the caller's host buffers or the arena may stay
+    // queued behind a failed call
+    drain_host_pipe();
+    P.valid = false;
+    return rc;
+  }
+  P.busy[slotp] = true;
+  P.ticket[slotp] = P.serial;
+  *ticket = P.serial++;
   return RBC_OK;
+}
+
+int rbc_error_trials_end(int64_t ticket) {
+  int slotp = -1;
+  {
+    std::lock_guard<std::mutex> lock(arena().mu);
+    HostPipe& P = host_pipe();
+    for (int h = 0; h < 2; ++h)
+      if (P.busy[h] && P.ticket[h] == ticket) slotp = h;
+  }
+  if (slotp < 0) return set_error(RBC_EVALUE, "no host-buffer call in flight with that ticket");
+  const cudaError_t e = cudaEventSynchronize(done_event(slotp));
+  {
+    std::lock_guard<std::mutex> lock(arena().mu);
+    HostPipe& P = host_pipe();
+    P.busy[slotp] = false;
+    P.ticket[slotp] = -1;
+    if (e != cudaSuccess) P.valid = false;
+  }
+  if (e != cudaSuccess) return fail_cuda(e, "host-buffer error trials", __FILE__, __LINE__);
+  return RBC_OK;
+}
+
+int rbc_error_trials(int dtype, int formula, int Q, int64_t T, int64_t N, const void* a,
+                     const void* b, const void* rand_plans, int with_det, double* err_rand,
+                     double* err_det, uint8_t* nf_rand, uint8_t* nf_det) {
+  int64_t ticket = -1;
+  RBC_TRY(rbc_error_trials_begin(dtype, formula, Q, T, N, a, b, rand_plans, with_det, err_rand,
+                                 err_det, nf_rand, nf_det, &ticket));
+  return rbc_error_trials_end(ticket);
 }
 
 }  // extern "C"

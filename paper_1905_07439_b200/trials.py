@@ -71,6 +71,68 @@ def error_trials(f, Q: int, A, B, mode, rplans=None, packed=None, with_det: bool
     return out
 
 
+class ErrorTrialStream:
+    """Host-buffer error trials as a stream of calls that overlap: ``submit``
+    enqueues one call (rbc_error_trials_begin) and returns a ticket,
+    ``result(ticket)`` waits for it (rbc_error_trials_end) and returns the same
+    dict as :func:`error_trials`.  With the next call submitted before the
+    previous result is taken, its operands are copied host->device while the
+    previous call computes; at most two calls are in flight.
+
+    A, B and packed plans are read asynchronously: pass pinned arrays (e.g.
+    ``torch.from_numpy(x).pin_memory().numpy()``) and keep them unchanged
+    until the call's ``result``.  Values are those of :func:`error_trials`."""
+
+    def __init__(self, f, Q: int, mode, with_det: bool = True):
+        self.m = mode_of(mode)
+        self.fid = plan_formula_id(f)
+        if self.fid is None:
+            raise NotImplementedError("error trials support the exact +-1 formulas (plan path)")
+        self.Q, self.n, self.with_det = Q, f.n, bool(with_det)
+        self._live = {}
+
+    def submit(self, A, B, packed=None, rplans=None) -> int:
+        m = self.m
+        A = np.ascontiguousarray(A, dtype=m.dtype)
+        B = np.ascontiguousarray(B, dtype=m.dtype)
+        T, N, _ = A.shape
+        if packed is None and rplans is not None:
+            packed = pack_recursive_plans(list(rplans), self.Q, self.n)
+        if packed is not None:
+            packed = np.ascontiguousarray(packed, dtype=np.uint8)
+            if packed.shape != (T, self.Q, _lib.PLAN_BYTES):
+                raise ValueError("packed plans must be (T, Q, 40)")
+        res = _pinned_results(T)
+        ticket = ctypes.c_int64(-1)
+        rc = _lib.load().rbc_error_trials_begin(
+            dtype_code(m), self.fid, self.Q, T, N, _vp(A), _vp(B),
+            _vp(packed) if packed is not None else None, int(self.with_det),
+            _vp(res[0]), _vp(res[1]), _vp(res[2]), _vp(res[3]), ctypes.byref(ticket))
+        _lib.check(rc)
+        self._live[ticket.value] = (res, packed is not None, (A, B, packed))
+        return ticket.value
+
+    def result(self, ticket: int):
+        res, has_plans, _keep = self._live.pop(ticket)
+        _lib.check(_lib.load().rbc_error_trials_end(ticket))
+        out = {}
+        if has_plans:
+            out["err_rand"], out["nf_rand"] = res[0].copy(), res[2].astype(bool)
+        if self.with_det:
+            out["err_det"], out["nf_det"] = res[1].copy(), res[3].astype(bool)
+        return out
+
+
+def _pinned_results(T: int):
+    """err_rand, err_det (float64) and nf_rand, nf_det (uint8) in pinned host
+    memory, so that the result copies of a begun call are asynchronous."""
+    import torch
+
+    e = torch.full((2, max(1, T)), float("nan"), dtype=torch.float64).pin_memory().numpy()
+    f = torch.zeros((2, max(1, T)), dtype=torch.uint8).pin_memory().numpy()
+    return e[0][:T], e[1][:T], f[0][:T], f[1][:T]
+
+
 def checkpoint_grid(total: int):
     """Running-average checkpoints 1..9, 10..90, ..., plus total
     (reference experiments.py:304-316)."""

@@ -338,3 +338,72 @@ def test_release_device_memory_then_host_call_again():
     _lib.check(_lib.load().rbc_release_device_memory())  # idempotent
     again = engine.apply_levels(levels, a, b, SINGLE)
     assert again.tobytes() == first.tobytes()
+
+
+def _stream_case(T, N=81, Q=3, first=1):
+    from dataclasses import replace
+
+    import torch
+
+    from paper_1905_07439_b200.configs import get_config, make_pairs
+    from paper_1905_07439_b200.randomize import pack_recursive_plans
+
+    cfg = replace(get_config("c2"), N=N, Q=Q)
+    A, B = make_pairs(cfg, first, T)
+    packed = pack_recursive_plans([cfg.plan(p) for p in range(first, first + T)], cfg.Q, cfg.n)
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
+    return cfg, pin(A), pin(B), pin(packed)
+
+
+def test_error_trial_stream_overlapped_calls_equal_single_calls():
+    """rbc_error_trials_begin / _end with two calls in flight: five steps of
+    different pairs, a shape change in the middle (the layout is rebuilt after
+    the calls in flight have drained) and another host-buffer API between a
+    submit and its result; every step equals the synchronous call bitwise."""
+    import paper_1905_07439_b200 as rbc
+    from paper_1905_07439_b200 import _lib, engine
+    from paper_1905_07439_b200.multiply import mode_tensors
+    from paper_1905_07439_b200.precision import SINGLE
+    from paper_1905_07439_b200.trials import ErrorTrialStream, error_trials
+
+    _lib.require_device()
+    steps = [_stream_case(T, first=1 + 40 * i) for i, T in enumerate([24, 24, 24, 7, 7, 24])]
+    cfg = steps[0][0]
+    f = cfg.formula_obj()
+    want = [error_trials(f, cfg.Q, A, B, cfg.mode, packed=P) for _, A, B, P in steps]
+    st = ErrorTrialStream(f, cfg.Q, cfg.mode)
+    got = [None] * len(steps)
+    prev = None
+    g = np.random.default_rng(3)
+    x = SINGLE.array(g.standard_normal((2, 16, 16)))
+    lv = [mode_tensors(rbc.strassen_formula(), SINGLE)] * 2
+    for i, (_, A, B, P) in enumerate(steps):
+        t = st.submit(A, B, packed=P)
+        if i == 2:  # takes the arena: waits for the two calls in flight first
+            engine.apply_levels(lv, x, x, SINGLE)
+        if prev is not None:
+            got[prev[0]] = st.result(prev[1])
+        prev = (i, t)
+    got[prev[0]] = st.result(prev[1])
+    for w, h in zip(want, got):
+        for key in ("err_rand", "err_det", "nf_rand", "nf_det"):
+            assert np.array_equal(w[key], h[key], equal_nan=True), key
+
+
+def test_error_trial_stream_limits():
+    """A third call in flight is refused; an unknown ticket is refused; an
+    empty call completes."""
+    from paper_1905_07439_b200 import _lib
+    from paper_1905_07439_b200.trials import ErrorTrialStream
+
+    _lib.require_device()
+    cfg, A, B, P = _stream_case(8)
+    st = ErrorTrialStream(cfg.formula_obj(), cfg.Q, cfg.mode)
+    t0, t1 = st.submit(A, B, packed=P), st.submit(A, B, packed=P)
+    with pytest.raises(ValueError):
+        st.submit(A, B, packed=P)
+    r0, r1 = st.result(t0), st.result(t1)
+    assert np.array_equal(r0["err_rand"], r1["err_rand"])
+    assert _lib.load().rbc_error_trials_end(12345) != 0
+    te = st.submit(A[:0], B[:0], packed=P[:0])
+    assert st.result(te)["err_rand"].shape == (0,)
