@@ -379,3 +379,94 @@ def run_trial_set(cfg, first: int, total: int, T_step: int, device="cuda:0", pip
     out = [np.concatenate([host[i, k, :cnt].numpy() for i, (_, cnt) in enumerate(chunks)])
            for k in range(4)]
     return out[0], out[1], out[2].astype(np.uint8), out[3].astype(np.uint8)
+
+
+def run_average_set(cfg, first: int, total: int, P_step: int, device="cuda:0", pipelined: bool = True):
+    """Averaging trials (reference experiments.py:264-296) of pairs
+    first .. first+total-1 of an averaging config (plans_per_pair = G > 1),
+    P_step pairs per pass, with fresh inputs: each pass's pairs are drawn on the
+    GPU, its P*G plans drawn natively and hatted on the host (dense
+    coefficient tables, the path of a formula that is not exact), then the
+    truth, the deterministic product, the G randomized products, their errors
+    and the running-mean errors run on the device.  Returns a dict of host
+    arrays: err_rand (total, G), err_mean (total, checkpoints), err_det
+    (total,), checkpoints.  ``pipelined``: the next pass's draw and tables are
+    prepared (second stream, host) while a pass computes."""
+    import torch
+
+    from . import hostrng
+    from .configs import ROLE_PLAN, make_pairs_device
+    from .randomize import RandomizationPlan, RecursivePlan
+
+    dev = torch.device(device)
+    f = cfg.formula_obj()
+    G = cfg.plans_per_pair
+    chunks = [(p0, min(P_step, first + total - p0)) for p0 in range(first, first + total, P_step)]
+    runners = {}
+    tdt = {"double": torch.float64, "single": torch.float32, "half": torch.float16}[cfg.mode.kind]
+    nbuf = 2 if pipelined and len(chunks) > 1 else 1
+    bufs = [tuple(torch.empty((P_step, cfg.N, cfg.N), dtype=tdt, device=dev) for _ in range(2))
+            for _ in range(nbuf)]
+    main = torch.cuda.current_stream(dev)
+    gen = torch.cuda.Stream(device=dev, priority=-1) if nbuf == 2 else main
+    ready = [torch.cuda.Event() for _ in range(nbuf)]
+    consumed = [torch.cuda.Event() for _ in range(nbuf)]
+
+    def runner_for(cnt):
+        if cnt not in runners:
+            runners[cnt] = DeviceAverageTrials(f, cfg.Q, cfg.N, cfg.mode, cnt, G, device=dev)
+        return runners[cnt]
+
+    def prepare(i):
+        p0, cnt = chunks[i]
+        slot = i % nbuf
+        keys = [cfg.plan_key(p, j) for p in range(p0, p0 + cnt) for j in range(1, G + 1)]
+        perms, signs = hostrng.draw_plans(
+            cfg.n, cfg.seed, [(ROLE_PLAN, t, q) for t in keys for q in range(cfg.Q)])
+        perms = perms.reshape(len(keys), cfg.Q, 3, cfg.n)
+        signs = signs.reshape(len(keys), cfg.Q, 3, cfg.n)
+        rplans = [RecursivePlan(tuple(RandomizationPlan(signs[t, q], perms[t, q]) for q in range(cfg.Q)))
+                  for t in range(len(keys))]
+        with torch.cuda.stream(gen):
+            if i >= nbuf:
+                gen.wait_event(consumed[slot])
+            a, b = make_pairs_device(cfg, p0, cnt, dev, out=tuple(t[:cnt] for t in bufs[slot]))
+            tables = runner_for(cnt).tables(rplans)
+            ready[slot].record(gen)
+        return a, b, tables
+
+    out = {"err_rand": [], "err_mean": [], "err_det": []}
+    ncp = len(checkpoint_grid(G))
+    pin = {"err_rand": torch.empty((P_step, G), dtype=torch.float64).pin_memory(),
+           "err_mean": torch.empty((P_step, ncp), dtype=torch.float64).pin_memory(),
+           "err_det": torch.empty(P_step, dtype=torch.float64).pin_memory()}
+    pending = None
+    nxt = prepare(0) if chunks else None
+    for i, (p0, cnt) in enumerate(chunks):
+        a, b, tables = nxt
+        slot = i % nbuf
+        r = runner_for(cnt)
+        main.wait_event(ready[slot])
+        if pending is not None:  # the runner's result buffers are reused by every pass
+            for k, v in pending.items():
+                out[k].append(v)
+            pending = None
+        r.run(a, b, tables)
+        consumed[slot].record(main)
+        res = {"err_rand": pin["err_rand"][:cnt], "err_mean": pin["err_mean"][:cnt],
+               "err_det": pin["err_det"][:cnt]}
+        res["err_rand"].copy_(r.err_rand.view(cnt, G), non_blocking=True)
+        res["err_mean"].copy_(r.err_mean.view(cnt, len(r.cps)), non_blocking=True)
+        res["err_det"].copy_(r.err_det, non_blocking=True)
+        if i + 1 < len(chunks):
+            nxt = prepare(i + 1)  # overlaps pass i when pipelined
+        torch.cuda.current_stream(dev).synchronize()  # pass i done: its results are on the host
+        pending = {k: v.numpy().copy() for k, v in res.items()}
+    if pending is not None:
+        for k, v in pending.items():
+            out[k].append(v)
+    cps = checkpoint_grid(G)
+    return {"err_rand": np.concatenate(out["err_rand"]) if chunks else np.zeros((0, G)),
+            "err_mean": np.concatenate(out["err_mean"]) if chunks else np.zeros((0, len(cps))),
+            "err_det": np.concatenate(out["err_det"]) if chunks else np.zeros(0),
+            "checkpoints": cps}

@@ -42,3 +42,26 @@ def test_average_trials_match_oracle(N, Q, P, G):
             if t + 1 in cps:
                 want.append(float(np.linalg.norm((total / (t + 1) - ref).ravel())) / refnorm)
         np.testing.assert_allclose(got["err_mean"][p], want, rtol=1e-12)
+
+
+def test_average_set_pipelined_equals_serial_and_host_call():
+    """trials.run_average_set (fresh pairs drawn on the GPU, plans drawn
+    natively, dense tables hatted on the host; the next pass prepared while a
+    pass computes) equals its unpipelined run bitwise and the host-buffer
+    average_trials call on host-drawn pairs (ragged last pass)."""
+    from dataclasses import replace
+
+    from paper_1905_07439_b200.configs import get_config, make_pairs
+    from paper_1905_07439_b200.trials import average_trials, run_average_set
+
+    cfg = replace(get_config("c3"), N=81, Q=2, plans_per_pair=5)
+    total, P_step = 7, 3
+    a = run_average_set(cfg, 2, total, P_step, "cuda:0", pipelined=True)
+    b = run_average_set(cfg, 2, total, P_step, "cuda:0", pipelined=False)
+    for k in ("err_rand", "err_mean", "err_det"):
+        assert a[k].tobytes() == b[k].tobytes(), k
+    A, B = make_pairs(cfg, 2, total)
+    rplans = [cfg.plan(cfg.plan_key(p, j)) for p in range(2, 2 + total) for j in range(1, 6)]
+    host = average_trials(cfg.formula_obj(), cfg.Q, A, B, cfg.mode, rplans, 5)
+    for k in ("err_rand", "err_mean", "err_det"):
+        assert np.array_equal(a[k], host[k]), k
