@@ -34,8 +34,8 @@
 // decision could differ only if the uniform fell within that ulp, p < 1e-15
 // per test).
 //
-// Memory shape of the parse (round 2: 59.7 -> see DESIGN section 4.4 ms for
-// config 5's four 8192^2 matrices).  One thread parses one chunk, so the raw
+// Memory shape of the parse (round 2: config 5's four 8192^2 matrices in 18.2
+// instead of 59.7 ms).  One thread parses one chunk, so the raw
 // words are stored chunk-interleaved: word p of chunk j lives at
 // ((j / 32) * 64 + p) * 32 + j % 32, and the 32 lanes of a warp -- 32
 // consecutive chunks, all near the same p -- read one 256-byte row per step
