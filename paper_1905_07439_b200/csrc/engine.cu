@@ -1109,6 +1109,17 @@ int rbc_error_trials_begin(int dtype, int formula, int Q, int64_t T, int64_t N, 
   // truth scratch comes from the stream-ordered pool, which two streams
   // fragment (config 4 calls went from 24 to 24-80 ms): one stream there.
   const bool two = N < 512;
+  if (!two) {
+    // whole-GPU jobs per chunk: a chunk should fill about four waves of
+    // 128 x 128 truth / leaf tiles, or its last wave runs half empty (config
+    // 4, 256 tiles per product: chunks of 1 / 2 / 4 pairs 23.40 / 22.69 /
+    // 22.18 ms per streamed call), while at least two chunks keep the copies
+    // of a single call behind its kernels
+    const int64_t tiles = ((N + 127) / 128) * ((N + 127) / 128);
+    int64_t cmin = 1;
+    while (cmin * tiles < 4 * 148) cmin *= 2;
+    C = std::max(C, std::min(cmin, std::max<int64_t>(1, (T + 1) / 2)));
+  }
   auto need = [&](int64_t c) {
     const size_t slot = 2 * align_up(c * N2 * es) + align_up(c * Q * RBC_PLAN_BYTES);
     return kSlots * slot + align_up(db) + 2 * (2 * align_up(T * 8) + 2 * align_up(T)) + 4096 +
