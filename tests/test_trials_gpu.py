@@ -407,3 +407,6 @@ def test_error_trial_stream_limits():
     assert _lib.load().rbc_error_trials_end(12345) != 0
     te = st.submit(A[:0], B[:0], packed=P[:0])
     assert st.result(te)["err_rand"].shape == (0,)
+    # pageable operands (plain numpy): the copies are staged, the values the same
+    tp = st.submit(np.array(A), np.array(B), packed=np.array(P))
+    assert np.array_equal(st.result(tp)["err_rand"], r0["err_rand"])
