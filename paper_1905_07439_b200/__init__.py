@@ -8,6 +8,7 @@ Public surface (mirrors the reference's names and semantics):
 
 * engine boundary : ``engine.apply_levels``, ``engine.leaf_matmul``,
                     ``engine.install`` (patches ``randbc._engine``)
+* north star      : ``bc_matmul(A, B, U, V, W, depth, randomize, seed, dtype)``
 * L2 API          : ``standard_multiply``, ``apply_bc``, ``recursive_apply``,
                     ``randomized_apply``, ``recursive_randomized_apply[_many]``
 * formulas/plans  : ``BilinearFormula``, ``strassen_formula``,
@@ -32,7 +33,7 @@ from .formula import (
     strassen_formula,
 )
 from .matgen import MATRIX_KINDS, MatrixSpec, generate
-from .multiply import apply_bc, mode_tensors, recursive_apply, standard_multiply
+from .multiply import apply_bc, bc_matmul, mode_tensors, recursive_apply, standard_multiply
 from .precision import DOUBLE, HALF, SINGLE, Mode, parse_precision
 from .randomize import (
     VARIANTS,
