@@ -17,7 +17,7 @@ namespace rbc {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kBlocksPerTrial = 64;
+constexpr int kBlocksPerTrial = 512;  // scratch stride; see rel_errors_t for the count in use
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
 #pragma unroll
@@ -103,7 +103,11 @@ cudaError_t rel_errors_t(int64_t ntr, int64_t N2, const void* c, const double* r
                          double* err, void* scratch, cudaStream_t st) {
   // blocks per trial: about 16 elements per thread, at most kBlocksPerTrial
   // (a function of N2 only, so the summation order is fixed)
-  const int nb = (int)std::min<int64_t>(kBlocksPerTrial, std::max<int64_t>(1, (N2 + 4095) / 4096));
+  // Above 2^24 elements a launch holds only a few trials (config 5: two), and
+  // 64 blocks each would leave SMs idle: 512 there (error kernels 1.40 ->
+  // 0.55 ms per config-5 step; config 4 measured better with 64: 0.24 vs 0.30).
+  const int64_t cap = N2 > ((int64_t)1 << 24) ? kBlocksPerTrial : 64;
+  const int nb = (int)std::min<int64_t>(cap, std::max<int64_t>(1, (N2 + 4095) / 4096));
   double* pn = (double*)scratch;
   double* pd = pn + ntr * kBlocksPerTrial;
   for (int64_t t0 = 0; t0 < ntr; t0 += 65535) {
