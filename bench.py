@@ -353,10 +353,16 @@ def roofline(prof: dict, config: str, cfg=None, pairs=None, sm_max_mhz=None):
         achieved = per_launch_bytes / avg_s / 1e9
         bound, unit = "hbm", "GB/s"
     tr = ncu_traffic(stage, config)
+    note = None
+    if stage == "truth_f64" and tr and tr > 4 * per_launch_bytes:
+        note = ("the binary64 truth streams its widened Y panels once per tile row (about 0.9 TB/s, "
+                "14% of HBM) and is bound by the DFMA pipe, not by that traffic: rasters that share "
+                "panels in L2 cut the reads 3.2x and ran 0.4-3% slower (DESIGN 4.1, "
+                "profiles/r02/experiments/truth_raster_groups.txt)")
     return {
         "bound": bound, "kernel": stage, "achieved": round(achieved, 2), "peak": round(peak, 2),
         "peak_source": how, "unit": unit, "frac": round(achieved / peak, 4),
-        "traffic": tr, "algorithmic_bytes_per_launch": per_launch_bytes,
+        "traffic": tr, "traffic_note": note, "algorithmic_bytes_per_launch": per_launch_bytes,
         "algorithmic_flops_per_launch": per_launch_flops, "avg_launch_ms": round(avg_s * 1e3, 5),
         "share_of_profiled_time": round(agg["ms"] / total_ms, 4) if total_ms else None,
         "stages": {k: {"count": v["count"], "ms": round(v["ms"], 4)} for k, v in prof.items()},
