@@ -19,8 +19,8 @@ import randbc.cli  # noqa: E402
 
 from paper_1905_07439_b200 import engine  # noqa: E402
 
-engine.install(randbc._engine)
-top = int(sys.argv[1]) if len(sys.argv) > 1 else 35
+engine.install(randbc._engine, wide="--wide" in sys.argv)
+top = int(next((a for a in sys.argv[1:] if a.isdigit()), 35))
 with tempfile.TemporaryDirectory() as d:
     out = Path(d) / "s2.csv"
     pr = cProfile.Profile()
