@@ -410,3 +410,21 @@ def test_error_trial_stream_limits():
     # pageable operands (plain numpy): the copies are staged, the values the same
     tp = st.submit(np.array(A), np.array(B), packed=np.array(P))
     assert np.array_equal(st.result(tp)["err_rand"], r0["err_rand"])
+
+
+@pytest.mark.parametrize("label", ["f64", "f32"])
+@pytest.mark.parametrize("which", ["x", "y"])
+def test_ring_leaves_broadcast_operand(label, which):
+    """The ring kernel with a broadcast operand (batch stride 0): every slot
+    copy of that operand reads the same 27 x 27 block."""
+    from paper_1905_07439_b200 import engine
+    from paper_1905_07439_b200.precision import parse_precision
+
+    mode = parse_precision(label)
+    g = np.random.default_rng(29)
+    T = 2600
+    x = mode.array(g.standard_normal((1 if which == "x" else T, 27, 27)))
+    y = mode.array(g.standard_normal((1 if which == "y" else T, 27, 27)))
+    got = engine.leaf_matmul(x, y, mode)
+    want = oracle.leaf(np.broadcast_to(x, (T, 27, 27)), np.broadcast_to(y, (T, 27, 27)))
+    assert got.shape == (T, 27, 27) and got.tobytes() == want.tobytes()
