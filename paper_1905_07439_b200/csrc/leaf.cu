@@ -952,7 +952,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
 // covers two outputs of a row, the A element broadcast, so a k step of an
 // 8 x 8 fragment issues 64 FP instructions instead of 128.  Same chains as
 // leaf_tiled_kernel.
-template <int BM, int BN, int BK, int TM, int TN, int MINB>
+template <int BM, int BN, int BK, int TM, int TN, int MINB, bool PEEL>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
     leaf_f32v_kernel(int M, int K, int N, const float* __restrict__ x, int64_t xs,
                      const float* __restrict__ y, int64_t ys, float* __restrict__ out,
@@ -1041,29 +1041,45 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
   load_tile(0);
   store_tile(0);
   __syncthreads();
-  for (int kt = 0; kt < ktiles; ++kt) {
+  // One k tile.  ptxas leaves a tile's loop-carried accumulators in other
+  // registers than it found them and restores them with about 44 MOVs at the
+  // end of the tile body (7.5% of all instructions with tiles of 8 steps),
+  // and a non-FP instruction costs the FMA pipe a dispatch cycle.  Tiles of
+  // 16 steps halve that share; PEEL takes the first tile (whose first step
+  // initialises the chains) out of the loop.  Config 5 leaves (128 x 128):
+  // 8 steps 31.9 TFLOP/s, peeled 32.6, 16 steps 33.6, 16 steps peeled 32.8
+  // (spills at the 128-register bound).  Config 1 leaves (64 x 64): 28.4,
+  // 29.0, 29.8, 30.0.  Neither compiling the partial-tile path out nor two
+  // tiles per loop trip changes the MOV count per tile.
+  auto ktile = [&](int kt, auto first_tag) {
+    constexpr bool kFirst = decltype(first_tag)::value;
     const int buf = kt & 1;
     if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
     const float* a0 = &As[buf][0][ty * 4];
     const float* b0 = &Bs[buf][0][tx * 4];
     if ((kt + 1) * BK <= K) {
-      if (kt == 0) {
-        kstep(a0, b0, true);
+      if (kFirst) kstep(a0, b0, true);
 #pragma unroll
-        for (int kk = 1; kk < BK; ++kk) kstep(a0 + kk * (BM + APAD), b0 + kk * BN, false);
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < BK; ++kk) kstep(a0 + kk * (BM + APAD), b0 + kk * BN, false);
-      }
+      for (int kk = kFirst ? 1 : 0; kk < BK; ++kk)
+        kstep(a0 + kk * (BM + APAD), b0 + kk * BN, false);
     } else {
       const int kmax = K - kt * BK;
 #pragma unroll 1
       for (int kk = 0; kk < kmax; ++kk)
-        kstep(a0 + kk * (BM + APAD), b0 + kk * BN, kt == 0 && kk == 0);
+        kstep(a0 + kk * (BM + APAD), b0 + kk * BN, kFirst && kk == 0);
     }
     if (kt + 1 < ktiles) {
       store_tile(buf ^ 1);
       __syncthreads();
+    }
+  };
+  if constexpr (PEEL) {
+    ktile(0, std::true_type{});
+    for (int kt = 1; kt < ktiles; ++kt) ktile(kt, std::false_type{});
+  } else {
+    for (int kt = 0; kt < ktiles; ++kt) {
+      if (kt == 0) ktile(kt, std::true_type{});
+      else ktile(kt, std::false_type{});
     }
   }
   float* ob = out + b * (int64_t)M * N;
@@ -1091,7 +1107,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
     }
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int MINB>
+template <int BM, int BN, int BK, int TM, int TN, int MINB, bool PEEL>
 cudaError_t run_f32v(int64_t batch, int64_t M, int64_t K, int64_t N, const void* x, int64_t xs,
                      const void* y, int64_t ys, void* out, cudaStream_t st) {
   const int tiles_m = (int)((M + BM - 1) / BM);
@@ -1102,14 +1118,14 @@ cudaError_t run_f32v(int64_t batch, int64_t M, int64_t K, int64_t N, const void*
     const int64_t full = (nb / 65535) * 65535;
     if (full > 0) {
       dim3 grid(tiles_m * tiles_n, 65535, (unsigned)(full / 65535));
-      leaf_f32v_kernel<BM, BN, BK, TM, TN, MINB><<<grid, NT, 0, st>>>(
+      leaf_f32v_kernel<BM, BN, BK, TM, TN, MINB, PEEL><<<grid, NT, 0, st>>>(
           (int)M, (int)K, (int)N, (const float*)x + b0 * xs, xs, (const float*)y + b0 * ys, ys,
           (float*)out + b0 * M * N, tiles_n, kF2NegZero);
     }
     if (nb > full) {
       dim3 grid(tiles_m * tiles_n, (unsigned)(nb - full), 1);
       const int64_t bb = b0 + full;
-      leaf_f32v_kernel<BM, BN, BK, TM, TN, MINB><<<grid, NT, 0, st>>>(
+      leaf_f32v_kernel<BM, BN, BK, TM, TN, MINB, PEEL><<<grid, NT, 0, st>>>(
           (int)M, (int)K, (int)N, (const float*)x + bb * xs, xs, (const float*)y + bb * ys, ys,
           (float*)out + bb * M * N, tiles_n, kF2NegZero);
     }
@@ -1292,13 +1308,13 @@ cudaError_t launch_leaf(int dtype_in, int dtype_out, int64_t batch, int64_t M, i
                      (ys % 4 == 0 || batch == 1) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
                      ((uintptr_t)out % 16 == 0);
     const int forced = tile_override();
-    // 128 x 128 x 8 tiles, 8 x 8 per thread (k tiles of 16 measured equal)
+    // 128 x 128 x 16 tiles, 8 x 8 per thread
     if (vec && M >= 128 && N >= 128 && forced == 0)
-      return run_f32v<128, 128, 8, 8, 8, 2>(batch, M, K, N, x, xs, y, ys, out, st);
+      return run_f32v<128, 128, 16, 8, 8, 2, false>(batch, M, K, N, x, xs, y, ys, out, st);
     // 64-wide leaves (config 1): 4 x 8 per thread, 128 threads (26.2 vs
     // 20.5 TFLOP/s for 8 x 8 per thread)
     if (vec && M >= 64 && N >= 64 && forced == 0)
-      return run_f32v<64, 64, 8, 4, 8, 4>(batch, M, K, N, x, xs, y, ys, out, st);
+      return run_f32v<64, 64, 16, 4, 8, 4, true>(batch, M, K, N, x, xs, y, ys, out, st);
     return leaf_dispatch<float, float>(batch, M, K, N, x, xs, y, ys, out, st);
   }
   if (dtype_out == kF16 && dtype_in == kF16) {
