@@ -28,6 +28,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+// The same wait with a suspend-time hint (ns): the waiting thread is parked
+// by the hardware instead of spinning through try_wait / branch instructions,
+// which would take dispatch cycles from the warps that compute.
+__device__ __forceinline__ void mbar_wait_parked(uint64_t* bar, unsigned parity, unsigned ns) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAITP_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAITP_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity), "r"(ns) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }

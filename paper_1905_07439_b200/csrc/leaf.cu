@@ -575,7 +575,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     if (lane == 0) {
       for (int i = 0; i < n; ++i) {
         const int s = i % NSLOT, round = i / NSLOT;
-        if (round > 0) mbar_wait(&empty[s], (unsigned)((round - 1) & 1));
+        if (round > 0) mbar_wait_parked(&empty[s], (unsigned)((round - 1) & 1), 2000);
         const T* gx = x + (lo + i) * xs;
         const T* gy = y + (lo + i) * ys;
         const unsigned bx = span_bytes(gx, E * sizeof(T)), by = span_bytes(gy, E * sizeof(T));
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   const int it = r / CJ, jt = r % CJ;
   for (int i = warp; i < n; i += NW) {
     const int s = i % NSLOT;
-    mbar_wait(&full[s], (unsigned)((i / NSLOT) & 1));
+    mbar_wait_parked(&full[s], (unsigned)((i / NSLOT) & 1), 1000);
     const T* gx = x + (lo + i) * xs;
     const T* gy = y + (lo + i) * ys;
     unsigned char* slot = ring_smem + (size_t)s * 2 * SPAN;
