@@ -8,11 +8,15 @@
 //  1. widen: X and Y to binary64 in 128-wide k-major panels, zero-padded to
 //     whole tiles (HBM-bound, ~1% of a large product).  One k tile of one
 //     operand is then a single contiguous span.
-//  2. truth_bulk_kernel: 128 x 128 x 16 tiles, 8 x 8 outputs per thread,
+//  2. truth_bulk_kernel: 128 x 128 x 32 tiles, 8 x 8 outputs per thread,
 //     one CTA of 256 threads per SM.  Operand tiles arrive by two bulk copies
 //     per stage (cp.async.bulk, the TMA engine, issued by one lane) into a
-//     4-stage shared-memory ring completed on mbarriers, so the threads issue
-//     nothing but 16-byte fragment loads and the multiply-adds.
+//     3-stage shared-memory ring completed on mbarriers, so the threads issue
+//     nothing but 16-byte fragment loads and the multiply-adds.  (A DFMA
+//     holds the pipe's dispatch for two cycles and every other instruction
+//     costs it one, so the per-stage waits, arrives and loop control are
+//     worth amortising: k tiles of 16 x 4 stages 38.3 ms per 8192^3 product,
+//     24 x 4: 37.4, 32 x 3: 37.2, 48 x 2: 42.5.)
 //
 // Rounding: for binary32/binary16 operands the widened products carry at most
 // 48 significant bits and are exact in binary64, so fl(acc + fl(a*b)) ==
@@ -32,7 +36,7 @@ namespace rbc {
 
 namespace {
 
-constexpr int kBM = 128, kBN = 128, kBK = 16, kTM = 8, kTN = 8, kStages = 4;
+constexpr int kBM = 128, kBN = 128, kBK = 32, kTM = 8, kTN = 8, kStages = 3;
 constexpr int kThreads = (kBM / kTM) * (kBN / kTN);  // 256
 
 template <class TIn>
