@@ -1048,8 +1048,9 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
   // 16 steps halve that share; PEEL takes the first tile (whose first step
   // initialises the chains) out of the loop.  Config 5 leaves (128 x 128):
   // 8 steps 31.9 TFLOP/s, peeled 32.6, 16 steps 33.6, 16 steps peeled 32.8
-  // (spills at the 128-register bound).  Config 1 leaves (64 x 64): 28.4,
-  // 29.0, 29.8, 30.0.  Neither compiling the partial-tile path out nor two
+  // (spills at the 128-register bound); 32 steps (dynamic shared memory) 32.9
+  // fetched at once and 31.8 fetched in two slices, both spilling.  Config 1
+  // leaves (64 x 64): 28.4, 29.0, 29.8, 30.0.  Neither compiling the partial-tile path out nor two
   // tiles per loop trip changes the MOV count per tile.
   auto ktile = [&](int kt, auto first_tag) {
     constexpr bool kFirst = decltype(first_tag)::value;
