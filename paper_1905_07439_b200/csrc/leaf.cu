@@ -1050,8 +1050,9 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
   // 8 steps 31.9 TFLOP/s, peeled 32.6, 16 steps 33.6, 16 steps peeled 32.8
   // (spills at the 128-register bound); 32 steps (dynamic shared memory) 32.9
   // fetched at once and 31.8 fetched in two slices, both spilling.  Config 1
-  // leaves (64 x 64): 28.4, 29.0, 29.8, 30.0.  Neither compiling the partial-tile path out nor two
-  // tiles per loop trip changes the MOV count per tile.
+  // leaves (64 x 64): 28.4, 29.0, 29.8, 30.0.  Neither compiling the
+  // partial-tile path out nor two tiles per loop trip changes the MOV count
+  // per tile.
   auto ktile = [&](int kt, auto first_tag) {
     constexpr bool kFirst = decltype(first_tag)::value;
     const int buf = kt & 1;
